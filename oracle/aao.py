@@ -1,0 +1,139 @@
+"""AaO matvec 𝓜u, preconditioner matvec P_α z, sequential CN, dense 𝓜 and P_α (ORACLE).
+
+Test infrastructure only (see oracle/__init__.py).
+
+Plain definitions written out:
+  PAPER.md:331-351 (§3.2)  Q1 = I − ½Ã, Q2 = I + ½Ã;
+                           𝓜 = block-bidiagonal(diag Q1, sub-diag −Q2);
+                           P_α = 𝓜 with the extra top-right block −αQ2.
+  PAPER.md:198-203 (Eq. 2.2) 𝓜 = B1 ⊗ I − B2 ⊗ Ã, B1 = tridiag(−1,1,0), B2 = ½ tridiag(1,1,0).
+  PAPER.md:244-266 (Eq. 3.1) P_α = C1^(α) ⊗ I − C2^(α) ⊗ Ã.
+  PAPER.md:125-128 (Eq. 2.1) CN step (I − τ/2 A) u^{k+1} = (I + τ/2 A) u^k + τ f^{k+½}.
+Vectors are arrays of shape (N, m) (1D) or (N, n, n) (2D, [t][y][x]).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from .problem import Operator1D, apply_L
+
+
+def tau_of(w) -> float:
+    return w.T / w.N
+
+
+def Q1(op, tau, z):
+    """Q1 z = z − ½ τ L_h z."""
+    return z - 0.5 * tau * apply_L(op, z)
+
+
+def Q2(op, tau, z):
+    """Q2 z = z + ½ τ L_h z."""
+    return z + 0.5 * tau * apply_L(op, z)
+
+
+def apply_M(w, op, u: np.ndarray) -> np.ndarray:
+    """𝓜u by the block form of PAPER.md:337-343: y_0 = Q1u_0, y_t = Q1u_t − Q2u_{t−1}."""
+    tau = tau_of(w)
+    y = Q1(op, tau, u)
+    y[1:] -= Q2(op, tau, u[:-1])
+    return y
+
+
+def apply_P(w, op, z: np.ndarray, alpha: float | None = None) -> np.ndarray:
+    """P_α z by the block form of PAPER.md:344-350: as 𝓜 plus (P z)_0 −= α Q2 z_{N−1}."""
+    alpha = w.alpha if alpha is None else alpha
+    tau = tau_of(w)
+    y = apply_M(w, op, z)
+    y[0] -= alpha * Q2(op, tau, z[-1])
+    return y
+
+
+def spatial_sparse(op) -> sp.csr_matrix:
+    if isinstance(op, Operator1D):
+        m = op.m
+        return sp.diags([op.lo[1:], op.di, op.up[:-1]], [-1, 0, 1], shape=(m, m), format="csr")
+    n = op.n
+    I = sp.identity(n, format="csr")
+    Lx = sp.diags([np.full(n - 1, op.xs), np.full(n, op.xd), np.full(n - 1, op.xu)], [-1, 0, 1])
+    Ly = sp.diags([np.full(n - 1, op.ys), np.full(n, op.yd), np.full(n - 1, op.yu)], [-1, 0, 1])
+    return (sp.kron(I, Lx) + sp.kron(Ly, I) + op.shift * sp.identity(n * n)).tocsr()
+
+
+class Q1Solver:
+    """Solves Q1 x = r = (I − ½τL_h) x = r.  1D: banded LU (solve_banded); 2D: sparse LU."""
+
+    def __init__(self, op, tau):
+        self.op, self.tau = op, tau
+        if isinstance(op, Operator1D):
+            m = op.m
+            ab = np.zeros((3, m))
+            ab[0, 1:] = -0.5 * tau * op.up[:-1]
+            ab[1, :] = 1.0 - 0.5 * tau * op.di
+            ab[2, :-1] = -0.5 * tau * op.lo[1:]
+            self.ab = ab
+            self.lu = None
+        else:
+            Q = sp.identity(op.m) - 0.5 * tau * spatial_sparse(op)
+            self.lu = spla.splu(Q.tocsc())
+
+    def __call__(self, r: np.ndarray) -> np.ndarray:
+        if self.lu is None:
+            return sla.solve_banded((1, 1), self.ab, r)
+        shp = r.shape
+        return self.lu.solve(r.reshape(-1)).reshape(shp)
+
+
+def solve_sequential(w, op, b: np.ndarray) -> np.ndarray:
+    """The exact AaO solution by CN time stepping:
+    Q1 u_t = b_t + Q2 u_{t−1}, u_{−1} := 0 (u⁰ enters through ξ in b_0)."""
+    tau = tau_of(w)
+    solve = Q1Solver(op, tau)
+    u = np.empty_like(b)
+    prev = np.zeros_like(b[0])
+    for t in range(w.N):
+        u[t] = solve(b[t] + Q2(op, tau, prev))
+        prev = u[t]
+    return u
+
+
+# ------------------------------------------------------------------------------- dense (tiny)
+
+def B1(N):
+    """B1 = tridiag(−1, 1, 0) ∈ R^{N×N}."""
+    return np.eye(N) - np.eye(N, k=-1)
+
+
+def B2(N):
+    """B2 = ½ tridiag(1, 1, 0)."""
+    return 0.5 * (np.eye(N) + np.eye(N, k=-1))
+
+
+def C1(N, alpha):
+    """α-circulant C1^(α): B1 with top-right entry −α."""
+    C = B1(N)
+    C[0, N - 1] += -alpha
+    return C
+
+
+def C2(N, alpha):
+    """α-circulant C2^(α): B2 with top-right entry +α/2."""
+    C = B2(N)
+    C[0, N - 1] += 0.5 * alpha
+    return C
+
+
+def dense_M(w, op) -> np.ndarray:
+    """𝓜 = B1 ⊗ I − B2 ⊗ Ã, Ã = τ L_h."""
+    At = tau_of(w) * op.dense()
+    return np.kron(B1(w.N), np.eye(op.m)) - np.kron(B2(w.N), At)
+
+
+def dense_P(w, op, alpha=None) -> np.ndarray:
+    """P_α = C1^(α) ⊗ I − C2^(α) ⊗ Ã (Eq. 3.1)."""
+    alpha = w.alpha if alpha is None else alpha
+    At = tau_of(w) * op.dense()
+    return np.kron(C1(w.N, alpha), np.eye(op.m)) - np.kron(C2(w.N, alpha), At)
