@@ -1,0 +1,177 @@
+/*
+ * cnpint — B200-native (sm_100a, fp64) all-at-once Crank–Nicolson solver with the block
+ * α-circulant parallel-in-time preconditioner of arxiv 2401.16113.
+ *
+ * C ABI.  Plain pointers and sizes only; no torch types.  The caller owns every buffer.
+ *
+ * Notation: N = number of time steps (the paper's M), m = number of spatial
+ * unknowns (the paper's N), τ = T/N, Ã = τ L_h, Q1 = I − ½Ã, Q2 = I + ½Ã.
+ *
+ * ----------------------------------------------------------------------------------------
+ * Device vector layout (every d_* vector argument)
+ *   fp64, block t (0-based) holds u^{t+1} (Eq. 2.2 unknown ordering).
+ *   1D:  [N][ld]          element (t, x)    at  t*ld + x,            0 <= x < nx
+ *   2D:  [N][ny][ld]      element (t, y, x) at  (t*ny + y)*ld + x,   0 <= x < nx, 0 <= y < ny
+ *   ld = cnpint_ld(ctx) >= nx (padded row pitch, multiple of 4 doubles = 32 B so that rows
+ *   start 32-B aligned; x fastest).  Padding columns x >= nx must be zero on input and are
+ *   written as zero on output.  Total length: cnpint_vec_elems(ctx) doubles.  The paper's
+ *   lexicographic order fixes neither the fastest index nor padding: our choice.
+ * Host vector layout (the *_host entry points): packed, no padding:
+ *   1D [N][nx], 2D [N][ny][nx], fp64, C order.
+ *
+ * Streams and synchronisation
+ *   Every call enqueues on the stream given to cnpint_create (a cudaStream_t passed as void*,
+ *   e.g. torch.cuda.current_stream().cuda_stream) and returns without synchronising, EXCEPT
+ *   cnpint_gmres*, cnpint_*_host and cnpint_device_status, which synchronise that stream.
+ *   Outputs may not alias inputs.  One handle per host thread.
+ *
+ * Ownership
+ *   The workspace (cnpint_workspace_bytes bytes of device memory, 256-B aligned) is owned by
+ *   the caller and must outlive the handle.  The library never allocates device memory after
+ *   cnpint_create, except a small pinned host staging area for residual estimates.  Host
+ *   coefficient arrays are copied at create and may be freed afterwards.
+ *
+ * Errors
+ *   Argument errors are detected synchronously (CNPINT_EINVAL / CNPINT_EUNSUPPORTED) and
+ *   nothing is enqueued.  CUDA launch/runtime failures return CNPINT_ECUDA.  A zero or
+ *   non-finite pivot in the shifted tridiagonal solve sets a device status word (SPEC.md:298
+ *   SingularPreconditioner) reported as CNPINT_ESINGULAR by cnpint_gmres / cnpint_device_status.
+ *   cnpint_last_error(ctx) returns a human-readable message for the last failure.
+ */
+#ifndef CNPINT_H
+#define CNPINT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cnpint_ctx cnpint_ctx;
+
+typedef enum {
+  CNPINT_OK = 0,
+  CNPINT_EINVAL = -1,        /* bad argument (sizes, alpha, tol, null pointers, workspace) */
+  CNPINT_EUNSUPPORTED = -2,  /* valid but unsupported (N not a power of two, N > 65536, ...) */
+  CNPINT_ECUDA = -3,         /* CUDA runtime/launch error */
+  CNPINT_ESINGULAR = -4,     /* zero / non-finite pivot in a shifted solve (device status) */
+  CNPINT_ENOCONV = -5,       /* GMRES reached maxit without meeting tol (report filled in) */
+  CNPINT_EBREAKDOWN = -6     /* non-finite GMRES scalar (NaN/Inf in the Arnoldi process) */
+} cnpint_status;
+
+/* Spatial operator L_h (NOT multiplied by τ; the library forms Ã = τ L_h).
+ * "A ∈ R^{N×N} the spatial discretization matrix of 𝓛"; Assumption 3.1
+ * (PAPER.md:235-238): negative semi-definite and diagonalisable.
+ *   1D (dim = 1, ny = 1):  (L_h u)_i = sub_i u_{i−1} + diag_i u_i + sup_i u_{i+1},
+ *                          u_{−1} = u_{nx} = 0 (homogeneous Dirichlet).
+ *       toeplitz = 1: constant rows (sub, diag, sup) = (xs, xd, xu); the arrays are ignored.
+ *       toeplitz = 0: per-row host arrays sub/diag/sup of length nx (sub[0], sup[nx−1] unused).
+ *   2D (dim = 2):          L_h = I_y ⊗ L_x + L_y ⊗ I_x + shift·I,  L_x = tridiag(xs, xd, xu)
+ *                          (nx×nx Toeplitz), L_y = tridiag(ys, yd, yu) (ny×ny Toeplitz).
+ *       Requires xs*xu > 0 and ys*yu > 0 (diagonal similarity to a symmetric Toeplitz matrix,
+ *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two. */
+typedef struct {
+  int dim;
+  int nx, ny;
+  int toeplitz;
+  const double* sub;
+  const double* diag;
+  const double* sup;
+  double xs, xd, xu;
+  double ys, yd, yu;
+  double shift;
+} cnpint_operator;
+
+typedef struct {
+  int iterations;      /* total inner Arnoldi steps ("Its") */
+  int restarts;        /* completed restart cycles that did not converge */
+  int converged;       /* 1 if the true residual ||b − 𝓜u||/||b|| <= tol */
+  double relres_est;   /* last Givens estimate |g_{j+1}|/||b|| */
+  double relres_true;  /* ||b − 𝓜u||/||b|| at the last cycle end */
+  double seconds;      /* host wall time inside the call */
+  double* history;     /* caller host array (may be NULL): estimate after every inner step */
+  int history_cap;     /* capacity of history */
+} cnpint_gmres_report;
+
+/* Bytes of device workspace for a handle with these sizes (0 on invalid arguments).
+ * restart_max >= 1 sizes the GMRES Krylov basis (restart_max + 1 vectors); pass 0 to size
+ * a handle for apply_A / apply_P / apply_Pinv only (cnpint_gmres then returns EINVAL). */
+size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max);
+
+/* Create a handle.  N: time steps, power of two, 2 <= N <= 65536.  T > 0: horizon (τ = T/N).
+ * alpha in (0, 1): the α of C1^(α), C2^(α) (α = 1 is P_1, out of scope).
+ * d_workspace: device pointer, >= cnpint_workspace_bytes bytes, 256-B aligned.
+ * cuda_stream: cudaStream_t (may be NULL = legacy default stream). */
+cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op,
+                            int restart_max, void* d_workspace, size_t ws_bytes, void* cuda_stream);
+
+void cnpint_destroy(cnpint_ctx* ctx);
+const char* cnpint_last_error(const cnpint_ctx* ctx);
+cnpint_status cnpint_set_stream(cnpint_ctx* ctx, void* cuda_stream);
+
+int64_t cnpint_ld(const cnpint_ctx* ctx);          /* row pitch in doubles */
+int64_t cnpint_vec_elems(const cnpint_ctx* ctx);   /* doubles per device vector (incl. padding) */
+int64_t cnpint_spec_elems(const cnpint_ctx* ctx);  /* complex entries of the half spectrum */
+
+/* y = 𝓜u,  𝓜 = B1 ⊗ I − B2 ⊗ Ã (Eq. 2.2), i.e. by the block form of
+ * y_0 = Q1 u_0, y_t = Q1 u_t − Q2 u_{t−1}.  Kernel K1, one HBM pass. */
+cnpint_status cnpint_apply_A(cnpint_ctx* ctx, const double* d_u, double* d_y);
+
+/* v = P_α z  (PAPER.md:344-350 block form; test hook): as 𝓜 plus (Pz)_0 −= α Q2 z_{N−1}. */
+cnpint_status cnpint_apply_P(cnpint_ctx* ctx, const double* d_z, double* d_v);
+
+/* z = P_α⁻¹ v via the diagonalisation P_α = (V⊗I)(D1⊗I − D2⊗Ã)(V⁻¹⊗I), V = Λ_α⁻¹𝔽*
+ * (Eq. 3.2), solving only k = 0..N/2 (Remark 3.1).
+ * v must be real (the conjugate halving relies on it).  1D: K2 (Γ_α-scaled real FFT along t)
+ * → K3 (N/2+1 complex tridiagonal solves) → K4 (C2R inverse FFT, Γ_α⁻¹, 1/N).
+ * 2D: DST fast diagonalisation in space around a fused time pass. */
+cnpint_status cnpint_apply_Pinv(cnpint_ctx* ctx, const double* d_v, double* d_z);
+
+/* Stage entry points of the 1D P_α⁻¹ (per-kernel parity tests and timing).
+ * Half spectrum layout: complex128 interleaved (re, im), [N/2+1][ld] (row k = frequency k),
+ * unnormalised forward DFT: d_what[k][x] = Σ_t e^{−2πikt/N} α^{t/N} v[t][x] (step (a) times √N).
+ * cnpint_shifted_solve solves (λ1_k I − λ2_k Ã) ẑ_k = ŵ_k with λ1_k = 1 − a e^{−2πik/N},
+ * λ2_k = ½(1 + a e^{−2πik/N}), a = α^{1/N} (FFT-consistent reading of Eq. eigCx, R3).
+ * cnpint_time_ifft applies z[t][x] = α^{−t/N} (1/N) Σ_{k<N} e^{+2πikt/N} ẑ_k (ẑ_{N−k} = conj ẑ_k). */
+cnpint_status cnpint_time_fft(cnpint_ctx* ctx, const double* d_v, double* d_what);
+cnpint_status cnpint_shifted_solve(cnpint_ctx* ctx, const double* d_what, double* d_zhat);
+cnpint_status cnpint_time_ifft(cnpint_ctx* ctx, const double* d_zhat, double* d_z);
+
+/* Right-preconditioned restarted GMRES(restart) on 𝓜P_α⁻¹ y = b, u = P_α⁻¹ y, zero initial
+ * guess.  Stops when the Givens estimate |g_{j+1}|/||b|| <= tol and then
+ * confirms the true residual ||b − 𝓜u||/||b|| <= tol at the cycle end (else restarts).
+ * Arnoldi: classical Gram–Schmidt with one reorthogonalisation (CGS2), fused device kernels;
+ * Hessenberg least squares (Givens) on device; one 8-byte device→host read per inner step.
+ * 0 < tol < 1, 1 <= restart <= restart_max, maxit >= 1 (total inner steps).
+ * Returns CNPINT_OK, CNPINT_ENOCONV (maxit reached; u holds the last iterate, so
+ * maxit = j <= restart returns the j-th GMRES iterate) or an error.  rep may be NULL. */
+cnpint_status cnpint_gmres(cnpint_ctx* ctx, const double* d_b, double* d_u, double tol, int restart,
+                           int maxit, cnpint_gmres_report* rep);
+
+/* Host-buffer variants (end-to-end: H2D copy of the input, the device computation, D2H copy of
+ * the result, all on the handle's stream; synchronises).  Host layout: packed (see top). */
+cnpint_status cnpint_apply_Pinv_host(cnpint_ctx* ctx, const double* h_v, double* h_z);
+cnpint_status cnpint_apply_A_host(cnpint_ctx* ctx, const double* h_u, double* h_y);
+cnpint_status cnpint_gmres_host(cnpint_ctx* ctx, const double* h_b, double* h_u, double tol, int restart,
+                                int maxit, cnpint_gmres_report* rep);
+
+/* Synchronise the stream and report deferred device errors (CNPINT_ESINGULAR), clearing them. */
+cnpint_status cnpint_device_status(cnpint_ctx* ctx);
+
+/* Number of kernels this handle has launched since create (instrumentation for bench.py). */
+int64_t cnpint_launch_count(const cnpint_ctx* ctx);
+
+/* K0: fp64 stream copy dst[i] = src[i], i < n (128-bit loads/stores) — the same-run HBM
+ * bandwidth reference.  Enqueued on cuda_stream. */
+cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, void* cuda_stream);
+
+/* Test hook (negative controls): 0 = none, 1 = flip the sign of the FFT twiddles,
+ * 2 = use the printed Eq. eigCx ordering λ1_k = 1 − a e^{+2πik/N} (R3).
+ * The parity suite must fail with either set. */
+cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CNPINT_H */

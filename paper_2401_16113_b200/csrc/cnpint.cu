@@ -1,0 +1,603 @@
+// cnpint host side: the C ABI of include/cnpint.h — handle, workspace carve-up, fp64 tables, the
+// P_α⁻¹ pipelines and the restarted right-preconditioned GMRES control loop.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+
+int matvec_partial_blocks(const cnpint_ctx* c);
+cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out);
+cudaError_t launch_dst_x_acc(cnpint_ctx* c, const double* in, double* out);
+
+namespace {
+
+const size_t ALIGN = 256;
+size_t up_align(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
+
+bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+struct Layout {
+  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
+  size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
+  size_t V, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
+  size_t total;
+};
+
+int64_t ld_of(int nx) { return ((int64_t)nx + 3) / 4 * 4; }
+
+// Validates sizes; returns a message or nullptr.
+const char* check_op(int N, const cnpint_operator* op, int* unsupported) {
+  *unsupported = 0;
+  if (!op) return "operator is NULL";
+  if (op->dim != 1 && op->dim != 2) return "op->dim must be 1 or 2";
+  if (op->nx < 1 || (op->dim == 2 && op->ny < 1)) return "nx/ny must be >= 1";
+  if (op->dim == 1 && op->ny != 1 && op->ny != 0) return "1D operator requires ny = 1";
+  if (N < 2) return "N must be >= 2";
+  if (!is_pow2(N) || N > 65536) { *unsupported = 1; return "N must be a power of two in [2, 65536]"; }
+  if (op->dim == 1) {
+    if (!op->toeplitz && (!op->sub || !op->diag || !op->sup)) return "non-Toeplitz 1D operator needs sub/diag/sup";
+    // K3 keeps <= 16 (Toeplitz) / 8 (variable) rows per thread in registers, <= 256 threads per system
+    if (op->nx > (op->toeplitz ? 4096 : 2048)) { *unsupported = 1; return "1D nx > 4096 (Toeplitz) / 2048 unsupported"; }
+  } else {
+    if (!is_pow2((long)op->nx + 1) || !is_pow2((long)op->ny + 1)) {
+      *unsupported = 1;
+      return "2D requires nx+1 and ny+1 powers of two (DST-I via FFT)";
+    }
+    if (op->nx + 1 > 4096 || op->ny + 1 > 4096) { *unsupported = 1; return "2D n+1 > 4096 unsupported"; }
+    if (!(op->xs * op->xu > 0.0) || !(op->ys * op->yu > 0.0))
+      return "2D requires xs*xu > 0 and ys*yu > 0 (diagonal symmetrisation)";
+  }
+  return nullptr;
+}
+
+Layout layout(int N, const cnpint_operator* op, int restart_max) {
+  Layout L;
+  std::memset(&L, 0, sizeof(L));
+  const int nx = op->nx, ny = op->dim == 2 ? op->ny : 1;
+  const int64_t ld = ld_of(nx);
+  const int64_t vec = (int64_t)N * ny * ld;
+  const int H = N / 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += up_align(bytes ? bytes : 1); return o; };
+  L.lo = take(ld * 8); L.di = take(ld * 8); L.up = take(ld * 8);
+  L.tw = take((size_t)N * 16);
+  L.gam = take((size_t)N * 8); L.igam = take((size_t)N * 8);
+  L.lam1 = take((size_t)(H + 1) * 16); L.lam2 = take((size_t)(H + 1) * 16);
+  L.sk = take((size_t)(H + 1) * 16); L.il2 = take((size_t)(H + 1) * 16);
+  if (op->dim == 2) {
+    L.dxi = take(nx * 8); L.dx = take(nx * 8); L.dyi = take(ny * 8); L.dy = take(ny * 8);
+    L.ex = take(ld * 8); L.ey = take(ny * 8);
+    L.twx = take((size_t)2 * (nx + 1) * 16); L.twy = take((size_t)2 * (ny + 1) * 16);
+  }
+  L.tables_end = off;
+  L.spec = op->dim == 1 ? take((size_t)(H + 1) * ld * 16) : take(16);
+  L.tmp1 = take(vec * 8); L.tmp2 = take(vec * 8); L.tmp3 = take(vec * 8);
+  L.io1 = take(vec * 8); L.io2 = take(vec * 8); L.io3 = take(vec * 8);
+  if (restart_max >= 1) {
+    L.V = take((size_t)(restart_max + 1) * vec * 8);
+    L.c1 = take((restart_max + 2) * 8); L.c2 = take((restart_max + 2) * 8); L.scl = take((restart_max + 2) * 8);
+    L.H = take((size_t)(restart_max + 1) * restart_max * 8);
+    L.cs = take(restart_max * 8); L.sn = take(restart_max * 8); L.g = take((restart_max + 2) * 8);
+    L.y = take(restart_max * 8); L.coef = take((restart_max + 2) * 8);
+  }
+  // partial sums: dots/updates use CNP_RED_BLOCKS rows of (MAX_DOT+1); the residual matvec one per block
+  {
+    cnpint_ctx tmp;
+    std::memset(&tmp, 0, sizeof(tmp));
+    tmp.dim = op->dim; tmp.N = N; tmp.ld = ld; tmp.ny = ny;
+    size_t mv = (size_t)matvec_partial_blocks(&tmp);
+    size_t rows = CNP_RED_BLOCKS * (CNP_MAX_DOT + 1);
+    L.part = take((rows > mv ? rows : mv) * 8);
+  }
+  L.scal = take(16 * 8);
+  L.status = take(64);
+  L.total = off;
+  return L;
+}
+
+void seterr(cnpint_ctx* c, const char* fmt, ...) {
+  if (!c) return;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(c->err, sizeof(c->err), fmt, ap);
+  va_end(ap);
+}
+
+cnpint_status cuda_fail(cnpint_ctx* c, cudaError_t e, const char* where) {
+  seterr(c, "CUDA error in %s: %s", where, cudaGetErrorString(e));
+  return CNPINT_ECUDA;
+}
+
+#define CK(expr)                                          \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, #expr); \
+  } while (0)
+
+// ------------------------------------------------------------------------- tables (host, long double)
+void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& img, const Layout& L) {
+  const int N = c->N, H = c->H;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  auto put = [&](size_t off, const void* src, size_t bytes) { std::memcpy(img.data() + off, src, bytes); };
+  // rows
+  std::vector<double> lo(c->ld, 0.0), di(c->ld, 0.0), up(c->ld, 0.0);
+  if (c->dim == 1) {
+    for (int i = 0; i < c->nx; ++i) {
+      lo[i] = op->toeplitz ? op->xs : op->sub[i];
+      di[i] = op->toeplitz ? op->xd : op->diag[i];
+      up[i] = op->toeplitz ? op->xu : op->sup[i];
+    }
+    lo[0] = 0.0;
+    up[c->nx - 1] = 0.0;
+  }
+  put(L.lo, lo.data(), c->ld * 8); put(L.di, di.data(), c->ld * 8); put(L.up, up.data(), c->ld * 8);
+  // twiddles ω_N^q = e^{-2πiq/N}
+  std::vector<double2> tw(N);
+  for (int q = 0; q < N; ++q) {
+    long double th = 2.0L * PI * (long double)q / (long double)N;
+    tw[q] = make_double2((double)cosl(th), (double)(-sinl(th)));
+    if (c->debug & 1) tw[q].y = -tw[q].y;
+  }
+  put(L.tw, tw.data(), N * 16);
+  // γ_t = α^{t/N}, 1/(N γ_t)
+  std::vector<double> gam(N), igam(N);
+  const long double lna = logl((long double)c->alpha);
+  for (int t = 0; t < N; ++t) {
+    long double g = expl(lna * (long double)t / (long double)N);
+    gam[t] = (double)g;
+    igam[t] = (double)(1.0L / ((long double)N * g));
+  }
+  put(L.gam, gam.data(), N * 8); put(L.igam, igam.data(), N * 8);
+  // λ1_k = 1 − a e^{−iθ_k}, λ2_k = ½(1 + a e^{−iθ_k}), θ_k = 2πk/N (FFT-consistent, R3)
+  std::vector<double2> l1(H + 1), l2(H + 1), sk(H + 1), il2(H + 1);
+  const long double a = expl(lna / (long double)N);
+  const long double one_m_a = -expm1l(lna / (long double)N);
+  for (int k = 0; k <= H; ++k) {
+    long double th = 2.0L * PI * (long double)k / (long double)N;
+    long double sh = sinl(0.5L * th);
+    long double sn = sinl(th), cs = cosl(th);
+    if (c->debug & 2) sn = -sn;  // printed Eq. eigCx ordering (negative control)
+    long double r1 = one_m_a + 2.0L * a * sh * sh, i1 = a * sn;        // 1 − a cos θ + i a sin θ
+    long double r2 = 0.5L * (1.0L + a * cs), i2 = -0.5L * a * sn;      // ½(1 + a cos θ) − ½ i a sin θ
+    long double den = r2 * r2 + i2 * i2;
+    l1[k] = make_double2((double)r1, (double)i1);
+    l2[k] = make_double2((double)r2, (double)i2);
+    sk[k] = make_double2((double)((r1 * r2 + i1 * i2) / den), (double)((i1 * r2 - r1 * i2) / den));
+    il2[k] = make_double2((double)(r2 / den), (double)(-i2 / den));
+  }
+  put(L.lam1, l1.data(), (H + 1) * 16); put(L.lam2, l2.data(), (H + 1) * 16);
+  put(L.sk, sk.data(), (H + 1) * 16); put(L.il2, il2.data(), (H + 1) * 16);
+  if (c->dim == 2) {
+    auto axis = [&](int n, double s, double d, double u, size_t offi, size_t offd, size_t offe, size_t offtw,
+                    int64_t elen) {
+      std::vector<double> Di(n), Dd(n), e(elen, 0.0);
+      long double rho = sqrtl((long double)s / (long double)u);
+      long double sq = sqrtl((long double)s * (long double)u);
+      for (int j = 1; j <= n; ++j) {
+        Di[j - 1] = (double)powl(rho, -(long double)j);
+        Dd[j - 1] = (double)(powl(rho, (long double)j) * 2.0L / (long double)(n + 1));
+        e[j - 1] = (double)((long double)d + 2.0L * sq * cosl(PI * (long double)j / (long double)(n + 1)));
+      }
+      std::vector<double2> t2(2 * (n + 1));
+      for (int q = 0; q < 2 * (n + 1); ++q) {
+        long double th = PI * (long double)q / (long double)(n + 1);
+        t2[q] = make_double2((double)cosl(th), (double)(-sinl(th)));
+      }
+      put(offi, Di.data(), n * 8); put(offd, Dd.data(), n * 8); put(offe, e.data(), elen * 8);
+      put(offtw, t2.data(), 2 * (n + 1) * 16);
+    };
+    axis(c->nx, op->xs, op->xd, op->xu, L.dxi, L.dx, L.ex, L.twx, c->ld);
+    axis(c->ny, op->ys, op->yd, op->yu, L.dyi, L.dy, L.ey, L.twy, c->ny);
+  }
+}
+
+// P_α⁻¹ on device.  in/out may coincide only for 2D (in is consumed by the first pass).
+cnpint_status pinv_dev(cnpint_ctx* c, const double* in, const double* vscale, double* out, int accumulate) {
+  if (c->dim == 1) {
+    CK(launch_time_fft(c, in, vscale, c->d_spec));
+    CK(launch_shifted_solve(c, c->d_spec, c->d_spec));
+    CK(launch_time_ifft(c, c->d_spec, out, accumulate));
+  } else {
+    // W⁻¹ (x then y), fused time pass, W (y then x)
+    double* a = (in == c->d_tmp1 || out == c->d_tmp1) ? c->d_io2 : c->d_tmp1;
+    double* b = (in == c->d_tmp2 || out == c->d_tmp2) ? c->d_io2 : c->d_tmp2;
+    if (a == b) b = c->d_io1;
+    CK(launch_dst_x(c, in, a, nullptr, 0));
+    CK(launch_dst_y(c, a, b, 0));
+    CK(launch_time_pass_2d(c, b, a, vscale));  // GMRES scale folded into the Γ-scaling
+    CK(launch_dst_y(c, a, b, 1));
+    if (accumulate) CK(launch_dst_x_acc(c, b, out));
+    else CK(launch_dst_x(c, b, out, nullptr, 1));
+  }
+  return CNPINT_OK;
+}
+
+cnpint_status check_vec(cnpint_ctx* c, const void* p, const char* name) {
+  if (!p) { seterr(c, "%s is NULL", name); return CNPINT_EINVAL; }
+  if (((uintptr_t)p) & 15) { seterr(c, "%s must be 16-byte aligned", name); return CNPINT_EINVAL; }
+  return CNPINT_OK;
+}
+
+}  // namespace
+
+// ============================================================================== C ABI
+extern "C" {
+
+size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max) {
+  int uns = 0;
+  if (check_op(N, op, &uns) || restart_max < 0) return 0;
+  return layout(N, op, restart_max).total;
+}
+
+cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op,
+                            int restart_max, void* d_workspace, size_t ws_bytes, void* cuda_stream) {
+  if (!out) return CNPINT_EINVAL;
+  *out = nullptr;
+  int uns = 0;
+  const char* msg = check_op(N, op, &uns);
+  if (msg) return uns ? CNPINT_EUNSUPPORTED : CNPINT_EINVAL;
+  if (!(T > 0.0) || !std::isfinite(T)) return CNPINT_EINVAL;
+  if (!(alpha > 0.0 && alpha < 1.0)) return CNPINT_EINVAL;
+  if (restart_max < 0 || restart_max > 1000) return CNPINT_EINVAL;
+  Layout L = layout(N, op, restart_max);
+  if (!d_workspace || ws_bytes < L.total || ((uintptr_t)d_workspace & (ALIGN - 1))) return CNPINT_EINVAL;
+  if (op->dim == 1 && !op->toeplitz) {
+    for (int i = 0; i < op->nx; ++i)
+      if (!std::isfinite(op->sub[i]) || !std::isfinite(op->diag[i]) || !std::isfinite(op->sup[i])) return CNPINT_EINVAL;
+  } else {
+    double v[7] = {op->xs, op->xd, op->xu, op->ys, op->yd, op->yu, op->shift};
+    for (double x : v)
+      if (!std::isfinite(x)) return CNPINT_EINVAL;
+  }
+  cnpint_ctx* c = new (std::nothrow) cnpint_ctx;
+  if (!c) return CNPINT_EINVAL;
+  std::memset(c, 0, sizeof(*c));
+  c->dim = op->dim; c->nx = op->nx; c->ny = op->dim == 2 ? op->ny : 1; c->N = N; c->H = N / 2;
+  c->toeplitz = op->dim == 2 ? 1 : op->toeplitz;
+  c->ld = ld_of(op->nx); c->slice = (int64_t)c->ny * c->ld; c->vec = (int64_t)N * c->slice;
+  c->spec_rows = c->H + 1; c->spec_elems = c->spec_rows * c->slice;
+  c->T = T; c->tau = T / N; c->alpha = alpha; c->lnalpha = std::log(alpha); c->a = std::exp(c->lnalpha / N);
+  c->xs = op->xs; c->xd = op->xd; c->xu = op->xu; c->ys = op->ys; c->yd = op->yd; c->yu = op->yu;
+  c->shift = op->dim == 2 ? op->shift : 0.0;
+  c->restart_max = restart_max;
+  c->stream = (cudaStream_t)cuda_stream;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  c->num_sms = CNP_NUM_SMS_DEFAULT;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  c->ws = (char*)d_workspace; c->ws_bytes = ws_bytes;
+  char* w = c->ws;
+  c->d_lo = (double*)(w + L.lo); c->d_di = (double*)(w + L.di); c->d_up = (double*)(w + L.up);
+  c->d_tw = (double2*)(w + L.tw); c->d_gam = (double*)(w + L.gam); c->d_igam = (double*)(w + L.igam);
+  c->d_lam1 = (double2*)(w + L.lam1); c->d_lam2 = (double2*)(w + L.lam2);
+  c->d_sk = (double2*)(w + L.sk); c->d_il2 = (double2*)(w + L.il2);
+  c->d_spec = (double2*)(w + L.spec);
+  c->d_tmp1 = (double*)(w + L.tmp1); c->d_tmp2 = (double*)(w + L.tmp2); c->d_tmp3 = (double*)(w + L.tmp3);
+  c->d_io1 = (double*)(w + L.io1); c->d_io2 = (double*)(w + L.io2); c->d_io3 = (double*)(w + L.io3);
+  if (op->dim == 2) {
+    c->d_dxi = (double*)(w + L.dxi); c->d_dx = (double*)(w + L.dx); c->d_dyi = (double*)(w + L.dyi);
+    c->d_dy = (double*)(w + L.dy); c->d_ex = (double*)(w + L.ex); c->d_ey = (double*)(w + L.ey);
+    c->d_twx = (double2*)(w + L.twx); c->d_twy = (double2*)(w + L.twy);
+  }
+  if (restart_max >= 1) {
+    c->d_V = (double*)(w + L.V); c->d_c1 = (double*)(w + L.c1); c->d_c2 = (double*)(w + L.c2);
+    c->d_scl = (double*)(w + L.scl); c->d_H = (double*)(w + L.H); c->d_cs = (double*)(w + L.cs);
+    c->d_sn = (double*)(w + L.sn); c->d_g = (double*)(w + L.g); c->d_y = (double*)(w + L.y);
+    c->d_coef = (double*)(w + L.coef);
+  }
+  c->d_part = (double*)(w + L.part);
+  c->d_scal = (double*)(w + L.scal);
+  c->d_status = (int*)(w + L.status);
+  // tables: build a host image of the table region [0, tables_end), upload, zero the rest
+  cnpint_status st = CNPINT_OK;
+  {
+    std::vector<char> img(L.tables_end, 0);
+    make_tables(c, op, img, L);
+    cudaError_t e = cudaMemcpyAsync(w, img.data(), L.tables_end, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.tables_end, 0, L.total - L.tables_end, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_pinned, 16 * sizeof(double));
+    if (e != cudaSuccess) st = cuda_fail(c, e, "cnpint_create");
+  }
+  if (st != CNPINT_OK) {
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return CNPINT_OK;
+}
+
+void cnpint_destroy(cnpint_ctx* c) {
+  if (!c) return;
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  delete c;
+}
+
+const char* cnpint_last_error(const cnpint_ctx* c) { return c ? c->err : "null handle"; }
+
+cnpint_status cnpint_set_stream(cnpint_ctx* c, void* s) {
+  if (!c) return CNPINT_EINVAL;
+  c->stream = (cudaStream_t)s;
+  return CNPINT_OK;
+}
+
+int64_t cnpint_ld(const cnpint_ctx* c) { return c ? c->ld : -1; }
+int64_t cnpint_vec_elems(const cnpint_ctx* c) { return c ? c->vec : -1; }
+int64_t cnpint_spec_elems(const cnpint_ctx* c) { return c ? c->spec_elems : -1; }
+int64_t cnpint_launch_count(const cnpint_ctx* c) { return c ? c->launches : -1; }
+
+cnpint_status cnpint_apply_A(cnpint_ctx* c, const double* u, double* y) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, u, "u") || check_vec(c, y, "y")) return CNPINT_EINVAL;
+  if (u == y) { seterr(c, "apply_A: output aliases input"); return CNPINT_EINVAL; }
+  CK(launch_matvec(c, u, y, 0, nullptr, nullptr));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_apply_P(cnpint_ctx* c, const double* z, double* v) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, z, "z") || check_vec(c, v, "v")) return CNPINT_EINVAL;
+  if (z == v) { seterr(c, "apply_P: output aliases input"); return CNPINT_EINVAL; }
+  CK(launch_matvec(c, z, v, 1, nullptr, nullptr));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_apply_Pinv(cnpint_ctx* c, const double* v, double* z) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, v, "v") || check_vec(c, z, "z")) return CNPINT_EINVAL;
+  if (v == z) { seterr(c, "apply_Pinv: output aliases input"); return CNPINT_EINVAL; }
+  return pinv_dev(c, v, nullptr, z, 0);
+}
+
+cnpint_status cnpint_time_fft(cnpint_ctx* c, const double* v, double* what) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, v, "v") || check_vec(c, what, "what")) return CNPINT_EINVAL;
+  if (c->dim != 1) { seterr(c, "stage entry points are 1D only"); return CNPINT_EUNSUPPORTED; }
+  CK(launch_time_fft(c, v, nullptr, (double2*)what));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_shifted_solve(cnpint_ctx* c, const double* what, double* zhat) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, what, "what") || check_vec(c, zhat, "zhat")) return CNPINT_EINVAL;
+  if (c->dim != 1) { seterr(c, "stage entry points are 1D only"); return CNPINT_EUNSUPPORTED; }
+  CK(launch_shifted_solve(c, (const double2*)what, (double2*)zhat));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_time_ifft(cnpint_ctx* c, const double* zhat, double* z) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, zhat, "zhat") || check_vec(c, z, "z")) return CNPINT_EINVAL;
+  if (c->dim != 1) { seterr(c, "stage entry points are 1D only"); return CNPINT_EUNSUPPORTED; }
+  CK(launch_time_ifft(c, (const double2*)zhat, z, 0));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_device_status(cnpint_ctx* c) {
+  if (!c) return CNPINT_EINVAL;
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (st) {
+    CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    seterr(c, "zero or non-finite pivot in a shifted solve (P_alpha singular to working precision)");
+    return CNPINT_ESINGULAR;
+  }
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_stream_copy(const double* src, double* dst, size_t n, void* stream) {
+  if (!src || !dst) return CNPINT_EINVAL;
+  cudaError_t e = launch_stream_copy(src, dst, n, (cudaStream_t)stream);
+  return e == cudaSuccess ? CNPINT_OK : CNPINT_ECUDA;
+}
+
+cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
+  if (!c) return CNPINT_EINVAL;
+  c->debug = flags;
+  // rebuild the table region with the new flags (synchronous)
+  cnpint_operator op;
+  std::memset(&op, 0, sizeof(op));
+  op.dim = c->dim; op.nx = c->nx; op.ny = c->ny; op.toeplitz = 1;
+  op.xs = c->xs; op.xd = c->xd; op.xu = c->xu; op.ys = c->ys; op.yd = c->yd; op.yu = c->yu; op.shift = c->shift;
+  // only tw / λ tables depend on the flags; they sit between L.tw and L.spec
+  Layout L = layout(c->N, &op, c->restart_max);
+  std::vector<char> img(L.tables_end, 0);
+  make_tables(c, &op, img, L);
+  // only the twiddle and λ tables depend on the flags: [tw, il2 end)
+  const size_t hi = L.il2 + up_align((size_t)(c->H + 1) * 16);
+  CK(cudaMemcpyAsync(c->ws + L.tw, img.data() + L.tw, hi - L.tw, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return CNPINT_OK;
+}
+
+// ------------------------------------------------------------------------------ GMRES
+cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
+                           cnpint_gmres_report* rep) {
+  if (!c) return CNPINT_EINVAL;
+  if (check_vec(c, d_b, "b") || check_vec(c, d_u, "u")) return CNPINT_EINVAL;
+  if (d_b == d_u) { seterr(c, "gmres: u aliases b"); return CNPINT_EINVAL; }
+  if (c->restart_max < 1) { seterr(c, "handle created with restart_max = 0"); return CNPINT_EINVAL; }
+  if (!(tol > 0.0 && tol < 1.0) || restart < 1 || restart > c->restart_max || maxit < 1) {
+    seterr(c, "gmres: need 0 < tol < 1, 1 <= restart <= restart_max, maxit >= 1");
+    return CNPINT_EINVAL;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  const int64_t vec = c->vec;
+  double* h = c->h_pinned;
+  std::vector<double*> V(restart + 1);
+  for (int i = 0; i <= restart; ++i) V[i] = c->d_V + (size_t)i * vec;
+  int its = 0, cycles = 0, converged = 0;
+  double est = 1.0, relres_true = 1.0;
+  cnpint_status result = CNPINT_OK;
+  const int mvblocks = matvec_partial_blocks(c);
+  CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
+  CK(cudaMemsetAsync(c->d_scal, 0, 16 * sizeof(double), c->stream));
+  // ||b||: first basis vector is b itself (x0 = 0 ⇒ r0 = b)
+  double* b_nc = const_cast<double*>(d_b);
+  V[0] = b_nc;
+  CK(launch_dots(c, &V[0], 1, d_b, c->d_part));
+  CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
+  CK(launch_small(c, 0, 0, 1));
+  CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
+    if (rep) { rep->iterations = 0; rep->restarts = 0; rep->converged = 1; rep->relres_est = 0; rep->relres_true = 0; }
+    return CNPINT_OK;
+  }
+  if (!std::isfinite(h[0])) { seterr(c, "gmres: ||b|| not finite"); return CNPINT_EBREAKDOWN; }
+  double* z = c->dim == 1 ? c->d_tmp1 : c->d_tmp3;
+  double* tcomb = c->dim == 1 ? c->d_tmp2 : c->d_io1;
+  while (true) {
+    int jdone = 0;
+    bool stop_inner = false;
+    for (int j = 0; j < restart && !stop_inner; ++j) {
+      // z = P_α⁻¹ v_j  (v_j = s_j Ṽ_j; the scale is folded into the Γ-scaling)
+      cnpint_status st = pinv_dev(c, V[j], c->d_scl + j, z, 0);
+      if (st != CNPINT_OK) return st;
+      // w = 𝓜 z, written straight into the slot of Ṽ_{j+1}
+      double* w = V[j + 1];
+      CK(launch_matvec(c, z, w, 0, nullptr, nullptr));
+      const int nv = j + 1;
+      if (nv <= CNP_MAX_DOT) {
+        CK(launch_dots(c, V.data(), nv, w, c->d_part));
+        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, nv, c->d_c1));
+        CK(launch_update(c, V.data(), nv, c->d_c1, 0, w, w, 1, 0, c->d_part));
+        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, nv, c->d_c2));
+        CK(launch_update(c, V.data(), nv, c->d_c2, 0, w, w, 0, 1, c->d_part));
+        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
+      } else {
+        // groups of CNP_MAX_DOT: dots, update (no fusion), dots, update, norm
+        for (int pass = 0; pass < 2; ++pass) {
+          double* cd = pass == 0 ? c->d_c1 : c->d_c2;
+          for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
+            int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
+            CK(launch_dots(c, V.data() + g0, ng, w, c->d_part));
+            CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, ng, cd + g0));
+          }
+          for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
+            int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
+            // coefficients cd[g0..] with scales scl[g0..]: shift the scale pointer via a temporary swap
+            double* saved = c->d_scl;
+            c->d_scl = saved + g0;
+            const bool last = pass == 1 && g0 + ng == nv;
+            cudaError_t e = launch_update(c, V.data() + g0, ng, cd + g0, 0, w, w, 0, last ? 1 : 0, c->d_part);
+            c->d_scl = saved;
+            CK(e);
+            if (last) CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
+          }
+        }
+      }
+      CK(launch_small(c, 1, j, 0));
+      CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      ++its;
+      jdone = j + 1;
+      est = h[1];
+      if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
+      if (h[3] != 0.0) {
+        seterr(c, "gmres: non-finite scalar in the Arnoldi process");
+        return CNPINT_EBREAKDOWN;
+      }
+      if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
+    }
+    // cycle end: y = H⁻¹g, t = V y, u += P⁻¹ t, r = b − 𝓜u
+    CK(launch_small(c, 2, jdone, 0));
+    {
+      std::vector<double*> Vc(V.begin(), V.begin() + jdone);
+      for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
+        int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
+        CK(launch_update(c, Vc.data() + g0, ng, c->d_coef + g0, 1, g0 == 0 ? nullptr : tcomb, tcomb, 0, 0,
+                         c->d_part));
+      }
+    }
+    {
+      cnpint_status st = pinv_dev(c, tcomb, nullptr, d_u, 1);
+      if (st != CNPINT_OK) return st;
+    }
+    // true residual into the workspace slot of Ṽ_0 (b is never overwritten)
+    V[0] = c->d_V;
+    CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part));
+    CK(launch_reduce_n(c, c->d_part, mvblocks, 1, 1, c->d_scal + 2));
+    CK(launch_small(c, 0, 0, 0));
+    CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    relres_true = h[4];
+    ++cycles;
+    if (relres_true <= tol) { converged = 1; break; }
+    if (its >= maxit) { result = CNPINT_ENOCONV; break; }
+    if (!std::isfinite(relres_true)) { seterr(c, "gmres: residual not finite"); result = CNPINT_EBREAKDOWN; break; }
+  }
+  cnpint_status dst = cnpint_device_status(c);
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->iterations = its;
+    rep->restarts = cycles - 1;
+    rep->converged = converged;
+    rep->relres_est = est;
+    rep->relres_true = relres_true;
+    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+  }
+  if (dst != CNPINT_OK) return dst;
+  if (result == CNPINT_ENOCONV) seterr(c, "gmres: maxit reached (relres %.3e > tol %.3e)", relres_true, tol);
+  return result;
+}
+
+// ------------------------------------------------------------------------------ host variants
+static cnpint_status h2d_vec(cnpint_ctx* c, const double* h, double* d) {
+  CK(cudaMemcpy2DAsync(d, c->ld * sizeof(double), h, c->nx * sizeof(double), c->nx * sizeof(double),
+                       (size_t)c->N * c->ny, cudaMemcpyHostToDevice, c->stream));
+  return CNPINT_OK;
+}
+static cnpint_status d2h_vec(cnpint_ctx* c, const double* d, double* h) {
+  CK(cudaMemcpy2DAsync(h, c->nx * sizeof(double), d, c->ld * sizeof(double), c->nx * sizeof(double),
+                       (size_t)c->N * c->ny, cudaMemcpyDeviceToHost, c->stream));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_apply_Pinv_host(cnpint_ctx* c, const double* h_v, double* h_z) {
+  if (!c || !h_v || !h_z) return CNPINT_EINVAL;
+  cnpint_status st;
+  if ((st = h2d_vec(c, h_v, c->d_io1))) return st;
+  if ((st = pinv_dev(c, c->d_io1, nullptr, c->d_io2, 0))) return st;
+  if ((st = d2h_vec(c, c->d_io2, h_z))) return st;
+  CK(cudaStreamSynchronize(c->stream));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_apply_A_host(cnpint_ctx* c, const double* h_u, double* h_y) {
+  if (!c || !h_u || !h_y) return CNPINT_EINVAL;
+  cnpint_status st;
+  if ((st = h2d_vec(c, h_u, c->d_io1))) return st;
+  CK(launch_matvec(c, c->d_io1, c->d_io2, 0, nullptr, nullptr));
+  if ((st = d2h_vec(c, c->d_io2, h_y))) return st;
+  CK(cudaStreamSynchronize(c->stream));
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_gmres_host(cnpint_ctx* c, const double* h_b, double* h_u, double tol, int restart, int maxit,
+                                cnpint_gmres_report* rep) {
+  if (!c || !h_b || !h_u) return CNPINT_EINVAL;
+  // GMRES uses tmp1/tmp2 (1D) or tmp1-3 + io1 (2D) internally; b and u live in io2 / io3.
+  double* db = c->d_io2;
+  double* du = c->d_io3;
+  cnpint_status st = h2d_vec(c, h_b, db);
+  if (st) return st;
+  st = cnpint_gmres(c, db, du, tol, restart, maxit, rep);
+  if (st != CNPINT_OK && st != CNPINT_ENOCONV) return st;
+  cnpint_status st2 = d2h_vec(c, du, h_u);
+  if (st2) return st2;
+  CK(cudaStreamSynchronize(c->stream));
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,52 @@
+// Common device helpers for cnpint (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CNP_DEV __device__ __forceinline__
+
+// ------------------------------------------------------------------ complex (double2) helpers
+CNP_DEV double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+CNP_DEV double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+CNP_DEV double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+CNP_DEV double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+CNP_DEV double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+CNP_DEV double2 cmul_conj(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+// a - b*c  (complex)
+CNP_DEV double2 cfms(double2 a, double2 b, double2 c) {
+  return make_double2(a.x - fma(b.x, c.x, -b.y * c.y), a.y - fma(b.x, c.y, b.y * c.x));
+}
+// a - r*c  (r real)
+CNP_DEV double2 crfms(double2 a, double r, double2 c) { return make_double2(fma(-r, c.x, a.x), fma(-r, c.y, a.y)); }
+CNP_DEV double2 crecip(double2 a) {
+  double d = 1.0 / fma(a.x, a.x, a.y * a.y);
+  return make_double2(a.x * d, -a.y * d);
+}
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+CNP_DEV double2 cmul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+CNP_DEV bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+
+// ------------------------------------------------------------------ reductions
+CNP_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Padded shared-memory index for complex FFT buffers: one pad entry every 16 elements breaks the
+// power-of-two strides of the Stockham stages into bank-conflict-free patterns.
+CNP_DEV int padi(int i) { return i + (i >> 4); }
+static inline int padi_host(int i) { return i + (i >> 4); }
+
+// Streaming (evict-first) global loads/stores for single-use vector traffic.
+CNP_DEV double2 ldg_cs2(const double2* p) { return __ldcs(p); }
+CNP_DEV void stg_cs2(double2* p, double2 v) { __stcs(p, v); }
+CNP_DEV double ldg_cs(const double* p) { return __ldcs(p); }
+CNP_DEV void stg_cs(double* p, double v) { __stcs(p, v); }

@@ -1,0 +1,94 @@
+// Internal (non-ABI) declarations shared by the cnpint host code and kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/cnpint.h"
+
+#define CNP_NUM_SMS_DEFAULT 148
+// Deterministic two-stage reductions use a fixed number of partial-sum blocks.
+#define CNP_RED_BLOCKS 1184   // 8 x 148
+#define CNP_RED_THREADS 256
+#define CNP_MAX_DOT 8         // basis vectors handled per dot/update launch
+
+struct cnpint_ctx {
+  // problem
+  int dim, nx, ny, N, H, toeplitz;
+  int64_t ld, slice, vec, spec_rows, spec_elems;
+  double T, tau, alpha, a, lnalpha;
+  double xs, xd, xu, ys, yd, yu, shift;
+  int restart_max;
+  cudaStream_t stream;
+  int debug;
+  int num_sms;
+  // workspace carve-up (device pointers)
+  char* ws;
+  size_t ws_bytes;
+  double* d_lo;        // [ld] τ-free 1D rows (zero padded; lo[0] = up[nx-1] = 0)
+  double* d_di;
+  double* d_up;
+  double2* d_tw;       // [N] ω_N^q = e^{-2πiq/N}
+  double* d_gam;       // [N] γ_t = α^{t/N}
+  double* d_igam;      // [N] 1/(N γ_t)
+  double2* d_lam1;     // [H+1] λ1_k
+  double2* d_lam2;     // [H+1] λ2_k
+  double2* d_sk;       // [H+1] s_k = λ1_k/λ2_k
+  double2* d_il2;      // [H+1] 1/λ2_k
+  double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
+  double* d_tmp1;      // [vec] scratch vectors
+  double* d_tmp2;
+  double* d_tmp3;
+  double* d_io1;       // [vec] host-API staging / 2D scratch
+  double* d_io2;
+  double* d_io3;
+  // 2D fast diagonalisation tables
+  double* d_dxi;       // [nx] D_x^{-1} entries   ρ_x^{-i}
+  double* d_dx;        // [nx] D_x entries        ρ_x^{i} * 2/(nx+1) (DST normalisation folded)
+  double* d_dyi;       // [ny]
+  double* d_dy;        // [ny]
+  double* d_ex;        // [nx] eigenvalues of L_x
+  double* d_ey;        // [ny] eigenvalues of L_y
+  double2* d_twx;      // [nx+1] e^{-2πiq/(2(nx+1))}
+  double2* d_twy;      // [ny+1]
+  // GMRES
+  double* d_V;         // [(restart_max+1)][vec]
+  double* d_part;      // [CNP_RED_BLOCKS][CNP_MAX_DOT+1]
+  double* d_c1;        // [restart_max+1] raw dots (pass 1)
+  double* d_c2;        // [restart_max+1] raw dots (pass 2)
+  double* d_scl;       // [restart_max+1] basis scales s_i (v_i = s_i Ṽ_i)
+  double* d_H;         // [(restart_max+1) * restart_max] column-major Hessenberg (ld = restart_max+1)
+  double* d_cs;        // [restart_max]
+  double* d_sn;        // [restart_max]
+  double* d_g;         // [restart_max+1]
+  double* d_y;         // [restart_max]
+  double* d_coef;      // [restart_max+1] combination coefficients
+  double* d_scal;      // [8] misc scalars: 0 = ||b||, 1 = est, 2 = beta^2, 3 = nonfinite flag
+  int* d_status;       // device status word (bit 0: singular pivot)
+  double* h_pinned;    // pinned host scalars [8]
+  double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
+  int64_t launches;
+  char err[512];
+};
+
+// ------------------------------------------------------------------ kernel launchers (return cudaError_t)
+cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStream_t s);
+
+// y = 𝓜u (mode 0), y = P_α u (mode 1), y = b − 𝓜u (mode 2, b given); optional Σ y² partials
+cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part);
+
+cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
+cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat);
+cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
+
+// 2D
+cudaError_t launch_dst_x(cnpint_ctx* c, const double* in, double* out, const double* vscale, int inverse);
+cudaError_t launch_dst_y(cnpint_ctx* c, const double* in, double* out, int inverse);
+cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
+
+// GMRES helpers
+cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w, double* part);
+cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int accumulate_sq);
+cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,
+                          double* w, double* wout, int want_dots, int want_norm, double* part);
+cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg);

@@ -1,0 +1,243 @@
+// GMRES kernels (K7 Arnoldi CGS2, K8 Hessenberg/Givens on device, K9 cycle end helpers).
+//
+// Right-preconditioned restarted GMRES (textbook algorithm, Saad Alg. 9.5).  The
+// Krylov basis is stored UNNORMALISED: v_i = s_i Ṽ_i with s_i on device, so no separate
+// normalisation pass is needed (the consumer of Ṽ_{j+1} — K2's Γ-scaling, or the dot/update
+// kernels — folds s_i in).  Classical Gram–Schmidt with one reorthogonalisation (CGS2):
+//   pass 1  c1 = Ṽᵀw                          (k_dots)
+//   pass 2  w ← w − Σ c1_i s_i² Ṽ_i ; c2 = Ṽᵀw  (k_update, fused dots)
+//   pass 3  w ← w − Σ c2_i s_i² Ṽ_i ; ‖w‖²      (k_update, fused norm) → stored as Ṽ_{j+1}
+// Every reduction is two-stage and deterministic: a fixed grid writes per-block partial sums,
+// one block per output sums them in a fixed order (bitwise reproducible runs, no atomics).
+#include "common.cuh"
+#include "internal.h"
+
+struct VPtrs {
+  const double* p[CNP_MAX_DOT];
+};
+
+// per-block reduction of NV accumulators; writes part[blockIdx.x * stride + i]
+template <int NV>
+CNP_DEV void block_reduce_write(double (&acc)[NV], double* part, int stride) {
+  __shared__ double red[CNP_RED_THREADS / 32][NV > 0 ? NV : 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double v = warp_sum(acc[i]);
+    if (lane == 0) red[w][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double s = 0.0;
+    for (int k = 0; k < CNP_RED_THREADS / 32; ++k) s += red[k][threadIdx.x];
+    part[(size_t)blockIdx.x * stride + threadIdx.x] = s;
+  }
+}
+
+// partial dots: part[b][i] = Σ Ṽ_i·w over block b's elements (grid-stride over double2)
+template <int NV>
+__global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double* __restrict__ w, size_t n2,
+                                                           double* __restrict__ part, int stride) {
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+    const double2 x = w2[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 v = ldg_cs2(reinterpret_cast<const double2*>(V.p[i]) + e);
+      acc[i] = fma(v.x, x.x, fma(v.y, x.y, acc[i]));
+    }
+  }
+  block_reduce_write<NV>(acc, part, stride);
+}
+
+// w_out = w − Σ_i coef_i Ṽ_i with coef_i = cd[i]·s_i² (MODE 0) or coef_i = cd[i] (MODE 1, combine,
+// w may be null), optionally fused partial dots with Ṽ (DOTS) or Σ w_out² (NORM).
+template <int NV, int MODE, bool DOTS, bool NORM>
+__global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const double* __restrict__ cd,
+                                                             const double* __restrict__ scl, const double* w,
+                                                             double* wout, size_t n2, double* __restrict__ part,
+                                                             int stride) {
+  double coef[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? cd[i] * scl[i] * scl[i] : cd[i];
+  constexpr int NA = DOTS ? NV : 1;
+  double acc[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* o2 = reinterpret_cast<double2*>(wout);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+    double2 x = w2 ? w2[e] : make_double2(0.0, 0.0);
+    double2 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      v[i] = DOTS ? reinterpret_cast<const double2*>(V.p[i])[e] : ldg_cs2(reinterpret_cast<const double2*>(V.p[i]) + e);
+      if (MODE == 0) { x.x = fma(-coef[i], v[i].x, x.x); x.y = fma(-coef[i], v[i].y, x.y); }
+      else { x.x = fma(coef[i], v[i].x, x.x); x.y = fma(coef[i], v[i].y, x.y); }
+    }
+    o2[e] = x;
+    if constexpr (DOTS) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = fma(v[i].x, x.x, fma(v[i].y, x.y, acc[i]));
+    }
+    if constexpr (NORM) acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
+  }
+  if constexpr (DOTS) block_reduce_write<NV>(acc, part, stride);
+  else if constexpr (NORM) block_reduce_write<1>(acc, part, stride);
+}
+
+// out[i] (+)= Σ_b part[b*stride + i], one block per column, fixed order
+__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ part, int nparts, int stride,
+                                                double* __restrict__ out) {
+  __shared__ double red[256];
+  const int i = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += 256) s += part[(size_t)b * stride + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[i] = red[0];
+}
+
+// ---------------------------------------------------------------- tiny single-thread kernels
+// scal[0] = ||b||, scal[1] = estimate, scal[2] = ||w||² (reduced), scal[3] = non-finite flag,
+// scal[4] = true residual ||r||/||b||
+__global__ void k_cycle_start(double* scl, double* g, double* scal, int first, int rmax) {
+  if (threadIdx.x != 0) return;
+  const double beta = sqrt(scal[2]);
+  if (first) scal[0] = beta;
+  scal[4] = beta / scal[0];
+  scl[0] = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i <= rmax; ++i) g[i] = 0.0;
+  g[0] = beta;
+  if (!isfinite(beta)) scal[3] = 1.0;
+}
+
+__global__ void k_arnoldi_finalize(int j, int ldh, const double* c1, const double* c2, double* scl, double* H,
+                                   double* cs, double* sn, double* g, double* scal) {
+  if (threadIdx.x != 0) return;
+  double* h = H + (size_t)j * ldh;
+  for (int i = 0; i <= j; ++i) h[i] = scl[i] * (c1[i] + c2[i]);
+  const double beta = sqrt(scal[2]);
+  h[j + 1] = beta;
+  scl[j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i < j; ++i) {  // previous rotations
+    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double den = hypot(h[j], h[j + 1]);
+  const double c = den > 0.0 ? h[j] / den : 1.0;
+  const double s = den > 0.0 ? h[j + 1] / den : 0.0;
+  cs[j] = c;
+  sn[j] = s;
+  h[j] = den;
+  h[j + 1] = 0.0;
+  g[j + 1] = -s * g[j];
+  g[j] = c * g[j];
+  const double est = fabs(g[j + 1]) / scal[0];
+  scal[1] = est;
+  if (!isfinite(est) || !isfinite(den)) scal[3] = 1.0;
+  if (beta == 0.0) scal[5] = 1.0;  // happy breakdown
+}
+
+// y = H[0:k,0:k]^{-1} g[0:k]; coef_i = y_i s_i  (combination Σ coef_i Ṽ_i = V y)
+__global__ void k_backsolve(int k, int ldh, const double* H, const double* g, const double* scl, double* y,
+                            double* coef) {
+  if (threadIdx.x != 0) return;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int l = i + 1; l < k; ++l) s -= H[i + (size_t)l * ldh] * y[l];
+    y[i] = s / H[i + (size_t)i * ldh];
+  }
+  for (int i = 0; i < k; ++i) coef[i] = y[i] * scl[i];
+}
+
+// ---------------------------------------------------------------- launchers
+static size_t n2_of(const cnpint_ctx* c) { return (size_t)c->vec / 2; }
+
+template <int NV>
+static void dots_nv(cnpint_ctx* c, const VPtrs& V, const double* w, double* part) {
+  k_dots<NV><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, w, n2_of(c), part, CNP_MAX_DOT + 1);
+}
+
+cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* w, double* part) {
+  VPtrs V;
+  for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
+  switch (nv) {
+    case 1: dots_nv<1>(c, V, w, part); break;
+    case 2: dots_nv<2>(c, V, w, part); break;
+    case 3: dots_nv<3>(c, V, w, part); break;
+    case 4: dots_nv<4>(c, V, w, part); break;
+    case 5: dots_nv<5>(c, V, w, part); break;
+    case 6: dots_nv<6>(c, V, w, part); break;
+    case 7: dots_nv<7>(c, V, w, part); break;
+    case 8: dots_nv<8>(c, V, w, part); break;
+    default: return cudaErrorInvalidValue;
+  }
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out) {
+  k_reduce<<<ncols, 256, 0, c->stream>>>(part, nparts, stride, out);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int /*unused*/) {
+  return launch_reduce_n(c, part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, ncols, out);
+}
+
+template <int NV, int MODE, bool DOTS, bool NORM>
+static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w, double* wout, double* part) {
+  k_update<NV, MODE, DOTS, NORM><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, cd, c->d_scl, w, wout,
+                                                                                   n2_of(c), part, CNP_MAX_DOT + 1);
+}
+
+template <int NV>
+static void upd_sel(cnpint_ctx* c, const VPtrs& V, const double* cd, int mode, const double* w, double* wout,
+                    int dots, int norm, double* part) {
+  if (mode == 1) upd<NV, 1, false, false>(c, V, cd, w, wout, part);
+  else if (dots) upd<NV, 0, true, false>(c, V, cd, w, wout, part);
+  else if (norm) upd<NV, 0, false, true>(c, V, cd, w, wout, part);
+  else upd<NV, 0, false, false>(c, V, cd, w, wout, part);
+}
+
+// coefmode 0: w_out = w − Σ cd_i s_i² Ṽ_i.  coefmode 1: w_out = w + Σ cd_i Ṽ_i (w may be null).
+cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double* cd, int coefmode, double* w,
+                          double* wout, int want_dots, int want_norm, double* part) {
+  VPtrs V;
+  for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
+  switch (nv) {
+    case 1: upd_sel<1>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 2: upd_sel<2>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 3: upd_sel<3>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 4: upd_sel<4>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 5: upd_sel<5>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 6: upd_sel<6>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 7: upd_sel<7>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 8: upd_sel<8>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    default: return cudaErrorInvalidValue;
+  }
+  c->launches++;
+  return cudaGetLastError();
+}
+
+// op 0: cycle_start(first = arg); op 1: arnoldi_finalize(j); op 2: backsolve(k = j)
+cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg) {
+  const int ldh = c->restart_max + 1;
+  if (op == 0) k_cycle_start<<<1, 32, 0, c->stream>>>(c->d_scl, c->d_g, c->d_scal, arg, c->restart_max);
+  else if (op == 1)
+    k_arnoldi_finalize<<<1, 32, 0, c->stream>>>(j, ldh, c->d_c1, c->d_c2, c->d_scl, c->d_H, c->d_cs, c->d_sn, c->d_g,
+                                                c->d_scal);
+  else k_backsolve<<<1, 32, 0, c->stream>>>(j, ldh, c->d_H, c->d_g, c->d_scl, c->d_y, c->d_coef);
+  c->launches++;
+  return cudaGetLastError();
+}

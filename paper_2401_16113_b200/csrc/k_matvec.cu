@@ -1,0 +1,239 @@
+// K0 stream copy, K1 AaO matvec y = 𝓜u (1D / 2D), K10 P_α matvec, GMRES residual r = b − 𝓜u.
+//
+// PAPER.md:337-343 (§3.2): 𝓜 = block-bidiagonal with Q1 = I − ½Ã on the diagonal and −Q2 =
+// −(I + ½Ã) below it, Ã = τ L_h.  Row t:  y_t = Q1 u_t − Q2 u_{t−1} = (u_t − u_{t−1}) − ½τ L_h (u_t + u_{t−1}),
+// u_{−1} = 0.  PAPER.md:344-350: P_α adds −αQ2 u_{N−1} to row 0, i.e. the same formula with
+// u_{−1} := α u_{N−1}.  One HBM pass: each thread walks a chunk of time rows keeping u_{t−1} in
+// registers; x-neighbours come from warp shuffles, y-neighbours (2D) from a shared-memory row
+// exchange.  16 B/unknown of compulsory traffic (read u, write y).
+#include "common.cuh"
+#include "internal.h"
+
+#include <algorithm>
+
+// ------------------------------------------------------------------------------- K0 stream copy
+__global__ void __launch_bounds__(256) k_stream_copy(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                     size_t n2) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+  for (; i < n2; i += stride) stg_cs2(dst + i, ldg_cs2(src + i));
+}
+
+__global__ void k_copy_tail(const double* __restrict__ src, double* __restrict__ dst, size_t n) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && (n & 1)) dst[n - 1] = src[n - 1];
+}
+
+cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStream_t s) {
+  size_t n2 = n / 2;
+  int dev = 0, sms = CNP_NUM_SMS_DEFAULT;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  size_t blocks = std::min<size_t>((n2 + 255) / 256, (size_t)sms * 8);
+  if (blocks == 0) blocks = 1;
+  if (((uintptr_t)src | (uintptr_t)dst) & 15) return cudaErrorMisalignedAddress;
+  k_stream_copy<<<(unsigned)blocks, 256, 0, s>>>((const double2*)src, (double2*)dst, n2);
+  if (n & 1) k_copy_tail<<<1, 32, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------ block-level sum helper
+template <int NT>
+CNP_DEV void block_partial(double v, double* part) {
+  __shared__ double red[NT / 32];
+  v = warp_sum(v);
+  int w = threadIdx.x / 32 + threadIdx.y * (blockDim.x / 32);
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    double s = 0.0;
+    for (int i = 0; i < NT / 32; ++i) s += red[i];
+    part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (size_t)blockIdx.z)] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------- K1 1D
+// MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  NORM: per-block Σ y².
+template <int MODE, bool NORM>
+__global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, double* __restrict__ y,
+                                                  const double* __restrict__ b, const double* __restrict__ lo,
+                                                  const double* __restrict__ di, const double* __restrict__ up,
+                                                  int N, int64_t ld, double htau, double alpha, int tchunk,
+                                                  double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
+  const bool active = 2 * gx < ld;
+  const int64_t x0 = active ? 2 * gx : 0;
+  const int t0 = blockIdx.y * tchunk;
+  const int t1 = min(N, t0 + tchunk);
+  const bool hasL = active && lane == 0 && x0 > 0;
+  const bool hasR = lane == 31 && active && x0 + 2 < ld;
+  const int64_t xl = x0 - 1, xr = x0 + 2;
+
+  double lo0 = 0, lo1 = 0, di0 = 0, di1 = 0, up0 = 0, up1 = 0;
+  if (active) {
+    lo0 = lo[x0]; lo1 = lo[x0 + 1]; di0 = di[x0]; di1 = di[x0 + 1]; up0 = up[x0]; up1 = up[x0 + 1];
+  }
+  // previous row (u_{t0-1}) incl. halo
+  double2 pv = make_double2(0.0, 0.0);
+  double pl = 0.0, pr = 0.0;
+  if (t0 > 0) {
+    const double* r = u + (int64_t)(t0 - 1) * ld;
+    if (active) pv = *reinterpret_cast<const double2*>(r + x0);
+    if (hasL) pl = r[xl];
+    if (hasR) pr = r[xr];
+  } else if (MODE == 1) {
+    const double* r = u + (int64_t)(N - 1) * ld;
+    if (active) { pv = *reinterpret_cast<const double2*>(r + x0); pv.x *= alpha; pv.y *= alpha; }
+    if (hasL) pl = alpha * r[xl];
+    if (hasR) pr = alpha * r[xr];
+  }
+  double acc = 0.0;
+#pragma unroll 4
+  for (int t = t0; t < t1; ++t) {
+    const double* r = u + (int64_t)t * ld;
+    double2 cv = make_double2(0.0, 0.0);
+    double cl = 0.0, cr = 0.0;
+    if (active) cv = ldg_cs2(reinterpret_cast<const double2*>(r + x0));
+    if (hasL) cl = r[xl];
+    if (hasR) cr = r[xr];
+    const double s0 = cv.x + pv.x, s1 = cv.y + pv.y;
+    const double d0 = cv.x - pv.x, d1 = cv.y - pv.y;
+    double sl = __shfl_up_sync(0xffffffffu, s1, 1);
+    double sr = __shfl_down_sync(0xffffffffu, s0, 1);
+    if (lane == 0) sl = hasL ? cl + pl : 0.0;
+    if (lane == 31) sr = hasR ? cr + pr : 0.0;
+    double y0 = d0 - htau * fma(lo0, sl, fma(di0, s0, up0 * s1));
+    double y1 = d1 - htau * fma(lo1, s0, fma(di1, s1, up1 * sr));
+    if (MODE == 2) {
+      double2 bv = make_double2(0.0, 0.0);
+      if (active) bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * ld + x0));
+      y0 = bv.x - y0;
+      y1 = bv.y - y1;
+    }
+    if (active) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
+    if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
+    pv = cv; pl = cl; pr = cr;
+  }
+  if (NORM) block_partial<128>(acc, part);
+}
+
+// ------------------------------------------------------------------------------- K1 2D
+// Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread walks a
+// chunk of t.  y-neighbours of s = u_t + u_{t-1} are exchanged through a double-buffered shared
+// row array; the edge warps also carry the halo rows y0-1 and y0+8.
+template <int MODE, bool NORM>
+__global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
+                                                  const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
+                                                  double htau, double alpha, double cxs, double cxu, double cys,
+                                                  double cyu, double cdiag, int tchunk, double* __restrict__ part) {
+  __shared__ double2 S[2][10][32];
+  const int lane = threadIdx.x, wy = threadIdx.y;
+  const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
+  const int ybase = blockIdx.y * 8;
+  const int yrow = ybase + wy;
+  const int ntiles_t = gridDim.z;
+  const int t0 = blockIdx.z * tchunk;
+  const int t1 = min(N, t0 + tchunk);
+  (void)ntiles_t;
+  const bool colok = x0 < ld;
+  const bool rowok = yrow < ny;
+  const bool act = colok && rowok;
+  // halo rows handled by warp 0 (row ybase-1) and warp 7 (row ybase+8)
+  const int hrow = (wy == 0) ? ybase - 1 : (wy == 7 ? ybase + 8 : -1);
+  const bool hact = colok && hrow >= 0 && hrow < ny && (wy == 0 || wy == 7);
+  const bool hasL = act && lane == 0 && x0 > 0;
+  const bool hasR = act && lane == 31 && x0 + 2 < ld;
+  const int64_t slice = (int64_t)ny * ld;
+  const int64_t off = (int64_t)yrow * ld + x0;
+  const int64_t hoff = (int64_t)hrow * ld + x0;
+
+  double2 pv = make_double2(0, 0), ph = make_double2(0, 0);
+  double pl = 0, pr = 0;
+  if (t0 > 0 || MODE == 1) {
+    const double sc = (t0 > 0) ? 1.0 : alpha;
+    const double* r = u + (int64_t)((t0 > 0) ? t0 - 1 : N - 1) * slice;
+    if (act) pv = *reinterpret_cast<const double2*>(r + off);
+    if (hact) ph = *reinterpret_cast<const double2*>(r + hoff);
+    if (hasL) pl = r[off - 1];
+    if (hasR) pr = r[off + 2];
+    pv.x *= sc; pv.y *= sc; ph.x *= sc; ph.y *= sc; pl *= sc; pr *= sc;
+  }
+  double acc = 0.0;
+  int buf = 0;
+  for (int t = t0; t < t1; ++t) {
+    const double* r = u + (int64_t)t * slice;
+    double2 cv = make_double2(0, 0), ch = make_double2(0, 0);
+    double cl = 0, cr = 0;
+    if (act) cv = ldg_cs2(reinterpret_cast<const double2*>(r + off));
+    if (hact) ch = *reinterpret_cast<const double2*>(r + hoff);
+    if (hasL) cl = r[off - 1];
+    if (hasR) cr = r[off + 2];
+    const double2 s = make_double2(cv.x + pv.x, cv.y + pv.y);
+    S[buf][wy + 1][lane] = s;
+    if (wy == 0) S[buf][0][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
+    if (wy == 7) S[buf][9][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
+    __syncthreads();
+    const double2 sd = S[buf][wy][lane];       // row y-1
+    const double2 su = S[buf][wy + 2][lane];   // row y+1
+    double sl = __shfl_up_sync(0xffffffffu, s.y, 1);
+    double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
+    if (lane == 0) sl = hasL ? cl + pl : 0.0;
+    if (lane == 31) sr = hasR ? cr + pr : 0.0;
+    double y0 = (cv.x - pv.x) - htau * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
+    double y1 = (cv.y - pv.y) - htau * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
+    if (x0 >= nx) y0 = 0.0;
+    if (x0 + 1 >= nx) y1 = 0.0;
+    if (MODE == 2 && act) {
+      double2 bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * slice + off));
+      y0 = bv.x - y0;
+      y1 = bv.y - y1;
+    }
+    if (act) {
+      stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
+      if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
+    }
+    pv = cv; ph = ch; pl = cl; pr = cr;
+    buf ^= 1;
+  }
+  if (NORM) block_partial<256>(acc, part);
+}
+
+// ----------------------------------------------------------------------------------- launcher
+template <int MODE, bool NORM>
+static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part) {
+  const double htau = 0.5 * c->tau;
+  if (c->dim == 1) {
+    const int tchunk = c->N >= 4096 ? 32 : 16;
+    dim3 block(128);
+    dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
+    k_matvec1d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau,
+                                                         c->alpha, tchunk, part);
+  } else {
+    const int tchunk = 16;
+    dim3 block(32, 8);
+    dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
+    k_matvec2d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
+                                                         c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
+                                                         part);
+  }
+  c->launches++;
+  return cudaGetLastError();
+}
+
+int matvec_partial_blocks(const cnpint_ctx* c) {
+  if (c->dim == 1) {
+    const int tchunk = c->N >= 4096 ? 32 : 16;
+    return (int)(((c->ld / 2 + 127) / 128) * ((c->N + tchunk - 1) / tchunk));
+  }
+  return (int)(((c->ld + 63) / 64) * ((c->ny + 7) / 8) * ((c->N + 15) / 16));
+}
+
+cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part) {
+  switch (mode) {
+    case 0: return run_matvec<0, false>(c, u, y, nullptr, nullptr);
+    case 1: return run_matvec<1, false>(c, u, y, nullptr, nullptr);
+    case 2: return part ? run_matvec<2, true>(c, u, y, b, part) : run_matvec<2, false>(c, u, y, b, nullptr);
+    default: return cudaErrorInvalidValue;
+  }
+}

@@ -1,0 +1,311 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star):
+  * 𝓜u, P_α z: 1e-12 relative ℓ2 (elementwise-stable stencils).
+  * P_α⁻¹v: backward error ‖P_α z_gpu − v‖/‖v‖ ≤ 1e-12 with the ORACLE's P_α (hard bar), and forward
+    error against the oracle ≤ max(1e-12, 4 × the fp64 oracle's own forward error) where the
+    conditioning of P_α makes 1e-12 unattainable for any fp64 algorithm (reading R-tol).
+  * GMRES: iterates 1e-9 relative, iteration counts ±1, final u within 1e-8 of sequential CN.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import aao, gmres as ogmres, precond, problem
+from tests.gpu_util import rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2401_16113_b200 import problems  # noqa: E402
+from paper_2401_16113_b200.cnpint import CnpintError, OperatorSpec, Solver  # noqa: E402
+
+
+def solver_for(w, restart_max=0, alpha=None):
+    return problems.make_solver(w, restart_max, alpha)
+
+
+SMALL = {
+    "1d_small": synth.scaled(synth.C1, 31, 16, alpha=0.1),
+    "1d_tiny_pad": synth.scaled(synth.C1, 5, 8, alpha=0.1),
+    "1d_ragged": synth.scaled(synth.C1, 201, 64, alpha=0.05),
+    "1d_price": synth.scaled(synth.C3, 127, 32, alpha=0.01),
+    "1d_price_ragged": synth.scaled(synth.C3, 333, 128, alpha=0.01),
+    "1d_N2": synth.scaled(synth.C1, 63, 2, alpha=0.3),
+    "2d_small": synth.scaled(synth.C4, 15, 16, alpha=0.1),
+    "2d_mid": synth.scaled(synth.C4, 31, 64, alpha=0.01),
+    "c1": synth.C1,
+}
+
+
+# ------------------------------------------------------------------------------ operator data
+@pytest.mark.parametrize("name", list(SMALL))
+def test_operator_rows_match_oracle(name):
+    w = SMALL[name]
+    spec = problems.operator_spec(w)
+    op = problem.build_operator(w)
+    if w.dim == 1:
+        lo = np.full(w.n, spec.xs) if spec.toeplitz else spec.sub
+        di = np.full(w.n, spec.xd) if spec.toeplitz else spec.diag
+        up = np.full(w.n, spec.xu) if spec.toeplitz else spec.sup
+        assert rel(lo, op.lo) < 1e-14 and rel(di, op.di) < 1e-14 and rel(up, op.up) < 1e-14
+    else:
+        got = np.array([spec.xs, spec.xd, spec.xu, spec.ys, spec.yd, spec.yu, spec.shift])
+        exp = np.array([op.xs, op.xd, op.xu, op.ys, op.yd, op.yu, op.shift])
+        assert rel(got, exp) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "2d_small", "c1"])
+def test_rhs_matches_oracle(name):
+    w = SMALL[name]
+    s = solver_for(w)
+    b = s.to_host(problems.rhs(w, s))
+    assert rel(b, problem.assemble_rhs(w, problem.build_operator(w))) < 1e-13
+
+
+# ------------------------------------------------------------------------------ K1 / K10
+@pytest.mark.parametrize("name", list(SMALL))
+def test_apply_A_and_P(name):
+    w = SMALL[name]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    V = synth.random_vectors(w, 3, 11)
+    for v in V:
+        d = s.to_device(v)
+        y = s.empty()
+        s.apply_A(d, y)
+        assert rel(s.to_host(y), aao.apply_M(w, op, v)) < 1e-12
+        s.apply_P(d, y)
+        assert rel(s.to_host(y), aao.apply_P(w, op, v)) < 1e-12
+        assert float(y[..., w.n:].abs().max()) == 0.0 if s.ld > w.n else True
+
+
+# ------------------------------------------------------------------------------ P_α⁻¹
+@pytest.mark.parametrize("name", list(SMALL))
+def test_pinv_small(name):
+    w = SMALL[name]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    for v in synth.random_vectors(w, 3, 12):
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        zo = precond.pinv_dft(w, op, v)
+        assert rel(zg, zo) < 1e-12, name
+        assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+        if s.ld > w.n:
+            assert float(z[..., w.n:].abs().max()) == 0.0
+    assert s.device_status() == 0
+
+
+def test_pinv_c1_all_16_vectors():
+    w = synth.C1
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    V = synth.random_vectors(w)
+    assert V.shape[0] == 16
+    for v in V:
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12
+        assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "1d_ragged", "c1"])
+def test_stage_kernels(name):
+    """K2, K3, K4 separately against the oracle's steps (a), (b), (c) (unnormalised DFT)."""
+    w = SMALL[name]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 3)[0]
+    N, K = w.N, w.N // 2 + 1
+    g = precond.gamma(N, w.alpha)
+    what_o = np.fft.fft(g[:, None] * v, axis=0)[:K]                     # √N · 𝔽Λ_α v
+    what = s.empty_spec()
+    s.time_fft(s.to_device(v), what)
+    wg = torch.view_as_complex(what).cpu().numpy()[:, : w.n]
+    assert rel(wg, what_o) < 1e-13
+    l1, l2 = precond.lambdas_fft(N, w.alpha)
+    zhat_o = precond.shifted_solve(w, op, l1[:K], l2[:K], what_o)
+    zhat = s.empty_spec()
+    s.shifted_solve(what, zhat)
+    zh = torch.view_as_complex(zhat).cpu().numpy()[:, : w.n]
+    assert rel(zh, zhat_o) < 1e-12
+    full = np.concatenate([zhat_o, np.conj(zhat_o[1:N - K + 1][::-1])])
+    z_o = (np.fft.ifft(full, axis=0).real / g[:, None])
+    z = s.empty()
+    s.time_ifft(zhat, z)
+    assert rel(s.to_host(z), z_o) < 1e-13
+
+
+@pytest.mark.parametrize("debug", [1, 2])
+def test_negative_controls_break_parity(debug):
+    """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail."""
+    w = SMALL["1d_small"]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 5)[0]
+    s.set_debug(debug)
+    z = s.empty()
+    s.apply_Pinv(s.to_device(v), z)
+    assert rel(aao.apply_P(w, op, s.to_host(z)), v) > 1e-3
+    s.set_debug(0)
+    s.apply_Pinv(s.to_device(v), z)
+    assert rel(aao.apply_P(w, op, s.to_host(z)), v) < 1e-12
+
+
+# ------------------------------------------------------------------------------ full sizes
+def _full_size_pinv(w, alphas, extended):
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1)[0]
+    for alpha in alphas:
+        s = solver_for(w, alpha=alpha)
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        back = rel(aao.apply_P(w, op, zg, alpha), v)
+        assert back < 1e-12, (w.name, alpha, back)
+        if extended:
+            zt = precond.pinv_dft(w, op, v, alpha, extended=True)
+            z64 = precond.pinv_dft(w, op, v, alpha)
+            fwd, own = rel(zg, zt), rel(z64, zt)
+            assert fwd <= max(1e-12, 4 * own), (w.name, alpha, fwd, own)
+        else:
+            zo = precond.pinv_dft(w, op, v, alpha)
+            fwd = rel(zg, zo)
+            assert fwd < 5e-12, (w.name, alpha, fwd)
+        assert s.device_status() == 0
+
+
+def test_pinv_full_c2():
+    _full_size_pinv(synth.C2, synth.C2_ALPHAS, extended=True)
+
+
+def test_pinv_full_c3():
+    _full_size_pinv(synth.C3, [synth.C3.alpha], extended=True)
+
+
+def test_pinv_full_c4():
+    _full_size_pinv(synth.C4, [synth.C4.alpha], extended=False)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_apply_A_full(name):
+    w = synth.WORKLOADS[name]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1)[0]
+    y = s.empty()
+    s.apply_A(s.to_device(v), y)
+    assert rel(s.to_host(y), aao.apply_M(w, op, v)) < 1e-12
+
+
+# ------------------------------------------------------------------------------ GMRES
+def _gmres_case(w, alpha=None, check_iterates=True):
+    alpha = w.alpha if alpha is None else alpha
+    w = w.with_(alpha=alpha)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    s = solver_for(w, restart_max=w.restart)
+    bd = problems.rhs(w, s)
+    u = s.empty()
+    rep = s.gmres(bd, u, w.tol, w.restart)
+    ug = s.to_host(u)
+    uo, orep = ogmres.gmres_right(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
+                                  w.tol, w.restart)
+    useq = aao.solve_sequential(w, op, b)
+    assert rep["converged"] and rep["relres_true"] <= w.tol
+    assert abs(rep["iterations"] - orep.iterations) <= 1, (rep["iterations"], orep.iterations)
+    assert rel(ug, useq) < 1e-8
+    if check_iterates:
+        for j in range(1, min(rep["iterations"], orep.iterations) + 1):
+            uj = s.empty()
+            s.gmres(bd, uj, w.tol, w.restart, maxit=j)
+            uoj, _ = ogmres.gmres_right(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
+                                        w.tol, w.restart, maxit=j)
+            assert rel(s.to_host(uj), uoj) < 1e-9, j
+    return rep, orep
+
+
+def test_gmres_c1():
+    rep, orep = _gmres_case(synth.C1)
+    assert rep["iterations"] <= 5
+
+
+def test_gmres_small_price_and_2d():
+    _gmres_case(synth.scaled(synth.C3, 127, 256, restart=40))
+    _gmres_case(synth.scaled(synth.C4, 31, 64, restart=40))
+
+
+def test_gmres_restart_cycles():
+    """restart=2 forces several cycles; still converges to sequential CN."""
+    w = synth.scaled(synth.C1, 63, 64, alpha=0.5, restart=2)
+    op = problem.build_operator(w)
+    s = solver_for(w, restart_max=2)
+    u = s.empty()
+    rep = s.gmres(problems.rhs(w, s), u, 1e-10, 2, maxit=200)
+    assert rep["converged"] and rep["restarts"] >= 1
+    b = problem.assemble_rhs(w, op)
+    assert rel(s.to_host(u), aao.solve_sequential(w, op, b)) < 1e-8
+
+
+@pytest.mark.parametrize("alpha", synth.C2_ALPHAS)
+def test_gmres_c2(alpha):
+    _gmres_case(synth.C2, alpha, check_iterates=False)
+
+
+def test_gmres_c3_c4():
+    _gmres_case(synth.C3, check_iterates=False)
+    _gmres_case(synth.C4, check_iterates=False)
+
+
+# ------------------------------------------------------------------------------ API behaviour
+def test_host_entry_points_match_device():
+    w = SMALL["1d_ragged"]
+    s = solver_for(w, restart_max=w.restart)
+    v = synth.random_vectors(w, 1, 9)[0]
+    z = s.empty()
+    s.apply_Pinv(s.to_device(v), z)
+    assert rel(s.apply_Pinv_host(v), s.to_host(z)) == 0.0
+    y = s.empty()
+    s.apply_A(s.to_device(v), y)
+    assert rel(s.apply_A_host(v), s.to_host(y)) == 0.0
+    b = s.to_host(problems.rhs(w, s))
+    uh, rh = s.gmres_host(b, w.tol, w.restart)
+    u = s.empty()
+    s.gmres(s.to_device(b), u, w.tol, w.restart)
+    assert rel(uh, s.to_host(u)) == 0.0 and rh["converged"]
+
+
+def test_invalid_arguments():
+    w = SMALL["1d_small"]
+    spec = problems.operator_spec(w)
+    with pytest.raises(CnpintError):
+        Solver(24, 1.0, 0.1, spec)            # N not a power of two -> EUNSUPPORTED (workspace 0)
+    with pytest.raises(CnpintError):
+        Solver(16, 1.0, 1.0, spec)            # alpha = 1 (P_1) out of scope
+    with pytest.raises(CnpintError):
+        Solver(16, -1.0, 0.1, spec)
+    s = solver_for(w)
+    x = s.empty()
+    with pytest.raises(CnpintError):
+        s.apply_Pinv(x, x)                    # aliasing
+    with pytest.raises(CnpintError):
+        s.gmres(x, s.empty(), 1e-10, 5)       # no Krylov workspace
+
+
+def test_zero_rhs_and_determinism():
+    w = SMALL["1d_small"]
+    s = solver_for(w, restart_max=10)
+    u = s.empty()
+    rep = s.gmres(s.empty(), u, 1e-10, 10)
+    assert rep["iterations"] == 0 and float(u.abs().max()) == 0.0
+    b = problems.rhs(w, s)
+    u1, u2 = s.empty(), s.empty()
+    s.gmres(b, u1, 1e-10, 10)
+    s.gmres(b, u2, 1e-10, 10)
+    assert torch.equal(u1, u2)                # deterministic reductions: bitwise reproducible
