@@ -162,6 +162,18 @@ cnpint_status cnpint_device_status(cnpint_ctx* ctx);
 /* Number of kernels this handle has launched since create (instrumentation for bench.py). */
 int64_t cnpint_launch_count(const cnpint_ctx* ctx);
 
+/* Per-kernel-class profiler (bench.py's live roofline): CUDA events recorded on the handle's stream
+ * around every launch while enabled.  enable(ctx, 1) (re)starts the counters (synchronises);
+ * enable(ctx, 0) frees the events.  read() synchronises and returns, for kernel class kid
+ * (0 <= kid < cnpint_kernel_name() == NULL), the summed event durations in ms, the launch count and
+ * the ALGORITHMIC bytes those launches must move.  Classes:
+ * 0 K1 matvec, 1 K2 time FFT, 2 K3 tridiagonal, 3 K4 inverse time FFT, 4 K6 2D time pass,
+ * 5 K5 DST x, 6 K5 DST y, 7 K7 dots, 8 K7 update, 9 reductions, 10 GMRES scalar kernels. */
+cnpint_status cnpint_profile_enable(cnpint_ctx* ctx, int on);
+cnpint_status cnpint_profile_read(cnpint_ctx* ctx, int kernel_class, double* ms_total, int64_t* launches,
+                                  double* algo_bytes);
+const char* cnpint_kernel_name(int kernel_class);
+
 /* K0: fp64 stream copy dst[i] = src[i], i < n (128-bit loads/stores) — the same-run HBM
  * bandwidth reference.  Enqueued on cuda_stream. */
 cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, void* cuda_stream);

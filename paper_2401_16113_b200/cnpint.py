@@ -26,7 +26,8 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_ld", "cnpint_vec_elems", "cnpint_spec_elems", "cnpint_apply_A", "cnpint_apply_P",
            "cnpint_apply_Pinv", "cnpint_time_fft", "cnpint_shifted_solve", "cnpint_time_ifft", "cnpint_gmres",
            "cnpint_apply_Pinv_host", "cnpint_apply_A_host", "cnpint_gmres_host", "cnpint_device_status",
-           "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug"]
+           "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug", "cnpint_profile_enable",
+           "cnpint_profile_read", "cnpint_kernel_name"]
 
 
 class CnpintError(RuntimeError):
@@ -77,6 +78,9 @@ def load_library(path: str = LIB_PATH):
         "cnpint_gmres_host": (C.c_int, [vp, dp, dp, C.c_double, C.c_int, C.c_int, C.POINTER(GmresReport)]),
         "cnpint_device_status": (C.c_int, [vp]), "cnpint_launch_count": (i64, [vp]),
         "cnpint_stream_copy": (C.c_int, [vp, vp, C.c_size_t, vp]), "cnpint_set_debug": (C.c_int, [vp, C.c_int]),
+        "cnpint_profile_enable": (C.c_int, [vp, C.c_int]),
+        "cnpint_profile_read": (C.c_int, [vp, C.c_int, dp, C.POINTER(C.c_int64), dp]),
+        "cnpint_kernel_name": (C.c_char_p, [C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -264,6 +268,26 @@ class Solver:
 
     def launch_count(self) -> int:
         return int(self.lib.cnpint_launch_count(self.h))
+
+    def profile_enable(self, on: bool = True):
+        self._sync_stream()
+        self._check(self.lib.cnpint_profile_enable(self.h, int(on)), "profile_enable")
+
+    def profile_read(self):
+        """{kernel class: (ms_total, launches, algorithmic_bytes)} for classes with launches."""
+        out = {}
+        kid = 0
+        while True:
+            name = self.lib.cnpint_kernel_name(kid)
+            if not name:
+                break
+            ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+            self._check(self.lib.cnpint_profile_read(self.h, kid, C.byref(ms), C.byref(n), C.byref(by)),
+                        "profile_read")
+            if n.value:
+                out[name.decode()] = (ms.value, n.value, by.value)
+            kid += 1
+        return out
 
     def set_debug(self, flags: int):
         self._sync_stream()

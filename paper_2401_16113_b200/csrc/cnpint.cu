@@ -13,6 +13,52 @@
 #include "internal.h"
 
 int matvec_partial_blocks(const cnpint_ctx* c);
+
+// ------------------------------------------------------------------------------ profiler
+// Per-kernel-class CUDA-event timing on the handle's stream.  Events come from a pool that grows
+// during warm-up and is reused; recording an event pair costs ~1 µs of GPU time per launch.
+struct CnpProf {
+  std::vector<cudaEvent_t> ev[KID_COUNT];  // pairs: [2i] start, [2i+1] stop
+  size_t used[KID_COUNT];
+  double bytes[KID_COUNT];
+};
+
+static const char* const KNAMES[KID_COUNT] = {"K1_matvec", "K2_time_fft", "K3_tridiag", "K4_time_ifft",
+                                              "K6_time_pass_2d", "K5_dst_x", "K5_dst_y", "K7_dots",
+                                              "K7_update", "reduce", "K8_small"};
+
+void cnp_prof_begin(cnpint_ctx* c, int kid) {
+  CnpProf* p = (CnpProf*)c->prof;
+  if (!p) return;
+  size_t i = p->used[kid];
+  if (p->ev[kid].size() < 2 * (i + 1)) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    p->ev[kid].push_back(a);
+    p->ev[kid].push_back(b);
+  }
+  cudaEventRecord(p->ev[kid][2 * i], c->stream);
+}
+
+void cnp_prof_end(cnpint_ctx* c, int kid, double algo_bytes) {
+  c->launches++;
+  CnpProf* p = (CnpProf*)c->prof;
+  if (!p) return;
+  size_t i = p->used[kid];
+  cudaEventRecord(p->ev[kid][2 * i + 1], c->stream);
+  p->used[kid] = i + 1;
+  p->bytes[kid] += algo_bytes;
+}
+
+static void prof_free(cnpint_ctx* c) {
+  CnpProf* p = (CnpProf*)c->prof;
+  if (!p) return;
+  for (int k = 0; k < KID_COUNT; ++k)
+    for (cudaEvent_t e : p->ev[k]) cudaEventDestroy(e);
+  delete p;
+  c->prof = nullptr;
+}
 cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out);
 cudaError_t launch_dst_x_acc(cnpint_ctx* c, const double* in, double* out);
 
@@ -317,6 +363,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
 
 void cnpint_destroy(cnpint_ctx* c) {
   if (!c) return;
+  prof_free(c);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
 }
@@ -394,6 +441,45 @@ cnpint_status cnpint_device_status(cnpint_ctx* c) {
   }
   return CNPINT_OK;
 }
+
+cnpint_status cnpint_profile_enable(cnpint_ctx* c, int on) {
+  if (!c) return CNPINT_EINVAL;
+  if (!on) {
+    if (c->prof) CK(cudaStreamSynchronize(c->stream));
+    prof_free(c);
+    return CNPINT_OK;
+  }
+  if (!c->prof) c->prof = new (std::nothrow) CnpProf();
+  CnpProf* p = (CnpProf*)c->prof;
+  if (!p) return CNPINT_EINVAL;
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < KID_COUNT; ++k) { p->used[k] = 0; p->bytes[k] = 0.0; }
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_profile_read(cnpint_ctx* c, int kid, double* ms_total, int64_t* launches, double* algo_bytes) {
+  if (!c || kid < 0 || kid >= KID_COUNT) return CNPINT_EINVAL;
+  CnpProf* p = (CnpProf*)c->prof;
+  double ms = 0.0;
+  int64_t n = 0;
+  double by = 0.0;
+  if (p) {
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < p->used[kid]; ++i) {
+      float f = 0.f;
+      CK(cudaEventElapsedTime(&f, p->ev[kid][2 * i], p->ev[kid][2 * i + 1]));
+      ms += f;
+    }
+    n = (int64_t)p->used[kid];
+    by = p->bytes[kid];
+  }
+  if (ms_total) *ms_total = ms;
+  if (launches) *launches = n;
+  if (algo_bytes) *algo_bytes = by;
+  return CNPINT_OK;
+}
+
+const char* cnpint_kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? KNAMES[kid] : nullptr; }
 
 cnpint_status cnpint_stream_copy(const double* src, double* dst, size_t n, void* stream) {
   if (!src || !dst) return CNPINT_EINVAL;

@@ -12,6 +12,12 @@
 #define CNP_RED_THREADS 256
 #define CNP_MAX_DOT 8         // basis vectors handled per dot/update launch
 
+// kernel classes for the per-class event profiler (cnpint_profile_*)
+enum {
+  KID_MATVEC = 0, KID_FFT_FWD, KID_TRIDIAG, KID_FFT_INV, KID_TIMEPASS2D, KID_DST_X, KID_DST_Y,
+  KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_COUNT
+};
+
 struct cnpint_ctx {
   // problem
   int dim, nx, ny, N, H, toeplitz;
@@ -68,6 +74,7 @@ struct cnpint_ctx {
   double* h_pinned;    // pinned host scalars [8]
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
+  void* prof;          // CnpProf* (host event pools), null when profiling is off
   char err[512];
 };
 
@@ -92,3 +99,9 @@ cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* 
 cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,
                           double* w, double* wout, int want_dots, int want_norm, double* part);
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg);
+
+// profiler hooks (cnpint.cu); no-ops unless cnpint_profile_enable(ctx, 1)
+void cnp_prof_begin(cnpint_ctx* c, int kid);
+void cnp_prof_end(cnpint_ctx* c, int kid, double algo_bytes);
+static inline double cnp_units(const cnpint_ctx* c) { return (double)c->N * c->nx * c->ny; }
+static inline double cnp_spec_units(const cnpint_ctx* c) { return (double)(c->H + 1) * c->nx * c->ny; }

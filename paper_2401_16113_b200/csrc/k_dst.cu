@@ -120,9 +120,11 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
     attr = true;
   }
   const unsigned grid = (unsigned)((nlines + X - 1) / X);
+  const int kid = YPASS ? KID_DST_Y : KID_DST_X;
+  cnp_prof_begin(c, kid);
   k_dst<YPASS><<<grid, T, smem, c->stream>>>(in, out, n, logM, c->ld, c->ny, nlines, X, CS, pre, post,
                                             YPASS ? c->d_twy : c->d_twx, accumulate);
-  c->launches++;
+  cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
   return cudaGetLastError();
 }
 

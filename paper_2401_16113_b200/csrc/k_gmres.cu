@@ -170,6 +170,7 @@ static void dots_nv(cnpint_ctx* c, const VPtrs& V, const double* w, double* part
 cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* w, double* part) {
   VPtrs V;
   for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
+  cnp_prof_begin(c, KID_DOTS);
   switch (nv) {
     case 1: dots_nv<1>(c, V, w, part); break;
     case 2: dots_nv<2>(c, V, w, part); break;
@@ -181,13 +182,14 @@ cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* 
     case 8: dots_nv<8>(c, V, w, part); break;
     default: return cudaErrorInvalidValue;
   }
-  c->launches++;
+  cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c) * (nv + 1));
   return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out) {
+  cnp_prof_begin(c, KID_REDUCE);
   k_reduce<<<ncols, 256, 0, c->stream>>>(part, nparts, stride, out);
-  c->launches++;
+  cnp_prof_end(c, KID_REDUCE, 0.0);
   return cudaGetLastError();
 }
 
@@ -215,6 +217,7 @@ cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double
                           double* wout, int want_dots, int want_norm, double* part) {
   VPtrs V;
   for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
+  cnp_prof_begin(c, KID_UPDATE);
   switch (nv) {
     case 1: upd_sel<1>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
     case 2: upd_sel<2>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
@@ -226,18 +229,19 @@ cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double
     case 8: upd_sel<8>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
     default: return cudaErrorInvalidValue;
   }
-  c->launches++;
+  cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (w ? 2 : 1)));
   return cudaGetLastError();
 }
 
 // op 0: cycle_start(first = arg); op 1: arnoldi_finalize(j); op 2: backsolve(k = j)
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg) {
   const int ldh = c->restart_max + 1;
+  cnp_prof_begin(c, KID_SMALL);
   if (op == 0) k_cycle_start<<<1, 32, 0, c->stream>>>(c->d_scl, c->d_g, c->d_scal, arg, c->restart_max);
   else if (op == 1)
     k_arnoldi_finalize<<<1, 32, 0, c->stream>>>(j, ldh, c->d_c1, c->d_c2, c->d_scl, c->d_H, c->d_cs, c->d_sn, c->d_g,
                                                 c->d_scal);
   else k_backsolve<<<1, 32, 0, c->stream>>>(j, ldh, c->d_H, c->d_g, c->d_scl, c->d_y, c->d_coef);
-  c->launches++;
+  cnp_prof_end(c, KID_SMALL, 0.0);
   return cudaGetLastError();
 }

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
 template <int MODE, bool NORM>
 static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part) {
   const double htau = 0.5 * c->tau;
+  cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
@@ -217,7 +218,7 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
                                                          c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
                                                          part);
   }
-  c->launches++;
+  cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));
   return cudaGetLastError();
 }
 

@@ -205,10 +205,14 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
     attr_done[MODE] = true;
   }
   unsigned grid = (unsigned)((W + f.X - 1) / f.X);
+  const int kid = MODE == 0 ? KID_FFT_FWD : MODE == 1 ? KID_FFT_INV : KID_TIMEPASS2D;
+  const double bytes = MODE == 2 ? 16.0 * cnp_units(c)
+                                 : 8.0 * cnp_units(c) * (accumulate ? 2.0 : 1.0) + 16.0 * cnp_spec_units(c);
+  cnp_prof_begin(c, kid);
   k_time_fft<MODE><<<grid, f.T, f.smem, c->stream>>>(vin, spin, vout, spout, vscale, c->N, f.logH, W, f.X, f.CS,
                                                     c->d_tw, c->d_gam, c->d_igam, accumulate, c->d_lam1, c->d_lam2,
                                                     c->d_ex, c->d_ey, c->tau * c->shift, c->tau, c->ld);
-  c->launches++;
+  cnp_prof_end(c, kid, bytes);
   return cudaGetLastError();
 }
 

@@ -333,10 +333,12 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
   const int m = c->nx;
   const int K = c->H + 1;
   const int64_t W = c->ld;
+  cnp_prof_begin(c, KID_TRIDIAG);
+  const double bytes = 32.0 * cnp_spec_units(c);
   if (m < 64) {
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
                                                             m, W, c->tau, K, c->d_status);
-    c->launches++;
+    cnp_prof_end(c, KID_TRIDIAG, bytes);
     return cudaGetLastError();
   }
   const int LM = c->toeplitz ? 16 : 8;
@@ -368,6 +370,6 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
     k_tridiag<false, 8><<<K, P, smem, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, m, W,
                                                     c->tau, c->d_status);
   }
-  c->launches++;
+  cnp_prof_end(c, KID_TRIDIAG, bytes);
   return cudaGetLastError();
 }
