@@ -180,7 +180,9 @@ cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, v
 
 /* Test hook (negative controls): 0 = none, 1 = flip the sign of the FFT twiddles,
  * 2 = use the printed Eq. eigCx ordering λ1_k = 1 − a e^{+2πik/N} (R3).
- * The parity suite must fail with either set. */
+ * The parity suite must fail with either set.  Bit 4 (not a negative control) routes Toeplitz
+ * shifted solves through the generic merge tree instead of the tabulated fast tree, so that the
+ * parity suite covers both K3 variants on the same inputs. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

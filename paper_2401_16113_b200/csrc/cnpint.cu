@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <complex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -70,7 +71,7 @@ size_t up_align(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 
 struct Layout {
-  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
+  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
   size_t V, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
   size_t total;
@@ -90,7 +91,10 @@ const char* check_op(int N, const cnpint_operator* op, int* unsupported) {
   if (op->dim == 1) {
     if (!op->toeplitz && (!op->sub || !op->diag || !op->sup)) return "non-Toeplitz 1D operator needs sub/diag/sup";
     // K3 keeps <= 16 (Toeplitz) / 8 (variable) rows per thread in registers, <= 256 threads per system
-    if (op->nx > (op->toeplitz ? 4096 : 2048)) { *unsupported = 1; return "1D nx > 4096 (Toeplitz) / 2048 unsupported"; }
+    if (op->nx > (op->toeplitz ? 4096 : 2048) || op->nx < 2) {
+      *unsupported = 1;
+      return "1D needs 2 <= nx <= 4096 (Toeplitz) / 2048 (variable rows)";
+    }
   } else {
     if (!is_pow2((long)op->nx + 1) || !is_pow2((long)op->ny + 1)) {
       *unsupported = 1;
@@ -117,6 +121,10 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   L.gam = take((size_t)N * 8); L.igam = take((size_t)N * 8);
   L.lam1 = take((size_t)(H + 1) * 16); L.lam2 = take((size_t)(H + 1) * 16);
   L.sk = take((size_t)(H + 1) * 16); L.il2 = take((size_t)(H + 1) * 16);
+  if (op->dim == 1 && op->toeplitz) {
+    const TriCfg t = tri_cfg(nx, 1);
+    L.tri = take(t.small ? 16 : (size_t)(H + 1) * t.tabstride * 16);
+  }
   if (op->dim == 2) {
     L.dxi = take(nx * 8); L.dx = take(nx * 8); L.dyi = take(ny * 8); L.dy = take(ny * 8);
     L.ex = take(ld * 8); L.ey = take(ny * 8);
@@ -204,6 +212,7 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
   // λ1_k = 1 − a e^{−iθ_k}, λ2_k = ½(1 + a e^{−iθ_k}), θ_k = 2πk/N (FFT-consistent, R3)
   std::vector<double2> l1(H + 1), l2(H + 1), sk(H + 1), il2(H + 1);
   const long double a = expl(lna / (long double)N);
+  const long double a_ld = a;
   const long double one_m_a = -expm1l(lna / (long double)N);
   for (int k = 0; k <= H; ++k) {
     long double th = 2.0L * PI * (long double)k / (long double)N;
@@ -220,6 +229,92 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
   }
   put(L.lam1, l1.data(), (H + 1) * 16); put(L.lam2, l2.data(), (H + 1) * 16);
   put(L.sk, sk.data(), (H + 1) * 16); put(L.il2, il2.data(), (H + 1) * 16);
+  if (c->dim == 1 && c->toeplitz) {
+    // K3 Toeplitz chunk tables (k_tridiag.cu): forward pivots and backward spike coefficients of a
+    // chunk of Lc = Lmin or Lmin+1 rows of (s_k I − Ã)/1 with a = −τ lo, c = −τ up, b = s_k − τ di.
+    const TriCfg t = tri_cfg(c->nx, 1);
+    if (!t.small) {
+      typedef std::complex<long double> cld;
+      const int Lt = t.L, st = t.tabstride;
+      std::vector<double2> tab((size_t)(H + 1) * st, make_double2(0.0, 0.0));
+      const long double tau = (long double)c->T / (long double)N;
+      const long double a = -tau * (long double)op->xs, cc = -tau * (long double)op->xu;
+      std::vector<cld> inv(Lt), al(Lt), ga(Lt), ap(Lt), gp(Lt);
+      auto d2 = [](cld z) { return make_double2((double)z.real(), (double)z.imag()); };
+      for (int k = 0; k <= H; ++k) {
+        long double th = 2.0L * PI * (long double)k / (long double)N;
+        long double sh = sinl(0.5L * th), sn = sinl(th), cs = cosl(th);
+        if (c->debug & 2) sn = -sn;
+        const cld l1(one_m_a + 2.0L * a_ld * sh * sh, a_ld * sn), l2(0.5L * (1.0L + a_ld * cs), -0.5L * a_ld * sn);
+        const cld b = l1 / l2 - cld(tau * (long double)op->xd, 0.0L);
+        double2* tb = tab.data() + (size_t)k * st;
+        for (int j = 1; j < Lt; ++j) {
+          const cld piv = (j == 1) ? b : b - a * ga[j - 1];
+          inv[j] = 1.0L / piv;
+          ga[j] = cc * inv[j];
+          al[j] = (j == 1) ? a * inv[j] : -a * al[j - 1] * inv[j];
+          tb[j] = d2(inv[j]);
+        }
+        struct SegC { cld fa, fb, fc, ga, gb, gc; };
+        SegC chunk[2];
+        for (int v = 0; v < 2; ++v) {
+          const int Lc = t.Lmin + v;
+          if (Lc < 2 || Lc > Lt) continue;
+          double2* tv = tb + Lt + v * (2 * Lt + 3);
+          cld fb, fc;
+          if (Lc >= 3) {
+            ap[Lc - 2] = al[Lc - 2];
+            gp[Lc - 2] = ga[Lc - 2];
+            for (int j = Lc - 3; j >= 1; --j) {
+              ap[j] = al[j] - ga[j] * ap[j + 1];
+              gp[j] = -ga[j] * gp[j + 1];
+            }
+            for (int j = 1; j <= Lc - 2; ++j) { tv[3 + j] = d2(ap[j]); tv[3 + Lt + j] = d2(gp[j]); }
+            fb = b - cc * ap[1];
+            fc = -cc * gp[1];
+          } else {
+            fb = b;
+            fc = cld(cc, 0.0L);
+          }
+          tv[0] = d2(al[Lc - 1]);
+          tv[1] = d2(fb);
+          tv[2] = d2(fc);
+          chunk[v] = SegC{cld(a, 0.0L), fb, fc, al[Lc - 1], cld(1.0L, 0.0L), ga[Lc - 1]};
+        }
+        if (t.fast) {
+          // fast tree (k_tridiag.cu MODE_FAST): standard segments S (chunks of Ls rows) and the
+          // last segment Z (its last chunk has Lmin rows) merged level by level.
+          const int P = 32 * t.G;
+          const int nlong = c->nx - P * t.Lmin;
+          SegC S = chunk[nlong ? 1 : 0], Z = chunk[0];
+          double2* tt = tb + 5 * Lt + 6;
+          auto merge = [&](const SegC& A, const SegC& B, double2* cf) {
+            const cld det = A.gb * B.fb - A.gc * B.fa;
+            const cld id = 1.0L / det;
+            const cld P1 = -B.fb * A.ga * id, P2 = A.gc * B.fc * id;
+            const cld R1 = B.fa * A.ga * id, R2 = -A.gb * B.fc * id;
+            cf[0] = d2(B.fb * id); cf[1] = d2(-A.gc * id);   // P0 = pa gd_A + pb fd_B
+            cf[2] = d2(A.gb * id); cf[3] = d2(-B.fa * id);   // R0 = ra fd_B + rb gd_A
+            cf[4] = d2(P1); cf[5] = d2(P2); cf[6] = d2(R1); cf[7] = d2(R2);
+            cf[8] = d2(A.fc); cf[9] = d2(B.ga);
+            return SegC{A.fa, A.fb + A.fc * P1, A.fc * P2, B.ga * R1, B.gb + B.ga * R2, B.gc};
+          };
+          for (int q = 0; q < t.nlv; ++q) {
+            const SegC S2 = merge(S, S, tt + (2 * q) * 10);
+            const SegC Z2 = merge(S, Z, tt + (2 * q + 1) * 10);
+            S = S2;
+            Z = Z2;
+          }
+          const cld det = Z.fb * Z.gb - Z.fc * Z.ga;
+          const cld id = 1.0L / det;
+          double2* r = tt + t.nlv * 20;
+          r[0] = d2(Z.gb * id); r[1] = d2(-Z.fc * id);
+          r[2] = d2(-Z.ga * id); r[3] = d2(Z.fb * id);
+        }
+      }
+      put(L.tri, tab.data(), tab.size() * 16);
+    }
+  }
   if (c->dim == 2) {
     auto axis = [&](int n, double s, double d, double u, size_t offi, size_t offd, size_t offe, size_t offtw,
                     int64_t elen) {
@@ -324,6 +419,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_tw = (double2*)(w + L.tw); c->d_gam = (double*)(w + L.gam); c->d_igam = (double*)(w + L.igam);
   c->d_lam1 = (double2*)(w + L.lam1); c->d_lam2 = (double2*)(w + L.lam2);
   c->d_sk = (double2*)(w + L.sk); c->d_il2 = (double2*)(w + L.il2);
+  c->d_tritab = (double2*)(w + L.tri);
   c->d_spec = (double2*)(w + L.spec);
   c->d_tmp1 = (double*)(w + L.tmp1); c->d_tmp2 = (double*)(w + L.tmp2); c->d_tmp3 = (double*)(w + L.tmp3);
   c->d_io1 = (double*)(w + L.io1); c->d_io2 = (double*)(w + L.io2); c->d_io3 = (double*)(w + L.io3);
@@ -499,8 +595,8 @@ cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
   Layout L = layout(c->N, &op, c->restart_max);
   std::vector<char> img(L.tables_end, 0);
   make_tables(c, &op, img, L);
-  // only the twiddle and λ tables depend on the flags: [tw, il2 end)
-  const size_t hi = L.il2 + up_align((size_t)(c->H + 1) * 16);
+  // only the twiddle, λ and K3 chunk tables depend on the flags: [tw, tables_end)
+  const size_t hi = L.tables_end;
   CK(cudaMemcpyAsync(c->ws + L.tw, img.data() + L.tw, hi - L.tw, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return CNPINT_OK;

@@ -50,3 +50,32 @@ CNP_DEV double2 ldg_cs2(const double2* p) { return __ldcs(p); }
 CNP_DEV void stg_cs2(double2* p, double2 v) { __stcs(p, v); }
 CNP_DEV double ldg_cs(const double* p) { return __ldcs(p); }
 CNP_DEV void stg_cs(double* p, double v) { __stcs(p, v); }
+
+// Asynchronous 16-byte global→shared copies (cp.async, LDGSTS): no register staging, any number
+// in flight; completion per thread by commit/wait groups, then a barrier for visibility.
+CNP_DEV void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+CNP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+CNP_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// Named barrier over `count` threads (multiple of 32); id 1..15 (0 is __syncthreads).
+CNP_DEV void named_sync(int id, int count) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory"); }
+
+template <typename T>
+CNP_DEV T shfl_down(T v, int d);
+template <>
+CNP_DEV double2 shfl_down<double2>(double2 v, int d) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
+CNP_DEV double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+CNP_DEV double2 cneg(double2 a) { return make_double2(-a.x, -a.y); }
+CNP_DEV double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+CNP_DEV double2 crfma(double r, double2 b, double2 c) { return make_double2(fma(r, b.x, c.x), fma(r, b.y, c.y)); }

@@ -18,6 +18,19 @@ enum {
   KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_COUNT
 };
 
+// K3 launch configuration (k_tridiag.cu): G warps per system, L = max rows per thread chunk,
+// Lmin = shortest chunk, tabstride = complex entries per frequency of the Toeplitz chunk table.
+struct TriCfg {
+  int small, G, logG, L, Lmin, tabstride, NS, padsh, smask, fast, nlv;
+  size_t smem;
+};
+TriCfg tri_cfg(int m, int toeplitz);
+// rows allocated per system in shared memory: m rounded up to the swizzle block (and to even)
+static inline __host__ __device__ int tri_rows_alloc(int m, int padsh) {
+  const int B = (1 << padsh) > 2 ? (1 << padsh) : 2;
+  return (m + B - 1) / B * B;
+}
+
 struct cnpint_ctx {
   // problem
   int dim, nx, ny, N, H, toeplitz;
@@ -41,6 +54,7 @@ struct cnpint_ctx {
   double2* d_lam2;     // [H+1] λ2_k
   double2* d_sk;       // [H+1] s_k = λ1_k/λ2_k
   double2* d_il2;      // [H+1] 1/λ2_k
+  double2* d_tritab;   // [H+1][tabstride] Toeplitz chunk tables of K3 (1D Toeplitz only)
   double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
   double* d_tmp1;      // [vec] scratch vectors
   double* d_tmp2;

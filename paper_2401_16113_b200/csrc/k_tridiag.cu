@@ -1,294 +1,401 @@
 // K3: step (b) of Eq. 3.2 for a tridiagonal L_h — the N/2+1 complex
-// shifted systems (λ1_k I − λ2_k Ã) ẑ_k = ŵ_k, k = 0..N/2 (Remark 3.1 halving), one CTA per k.
+// shifted systems (λ1_k I − λ2_k Ã) ẑ_k = ŵ_k, k = 0..N/2 (Remark 3.1 halving).
 //
 // Each system is divided by λ2_k (Re λ2_k > 0) so that the off-diagonals stay
 // real: rows  a_i x_{i−1} + b_i x_i + c_i x_{i+1} = d_i  with  a_i = −τ lo_i, c_i = −τ up_i (real),
-// b_i = s_k − τ di_i, s_k = λ1_k/λ2_k, d_i = ŵ_i/λ2_k.  Diagonal dominance holds for every k
-// (Re s_k > 0 and −di ≥ lo + up), so no pivoting is needed; a zero or non-finite pivot
-// still sets the device status word (SPEC.md:298 SingularPreconditioner).
+// b_i = s_k − τ di_i, s_k = λ1_k/λ2_k, d_i = ŵ_i/λ2_k.  Every system is diagonally dominant
+// (R22), so no pivoting is needed; a zero or non-finite pivot still sets the device
+// status word (SPEC.md:298 SingularPreconditioner).
 //
-// Algorithm (partition method = per-thread Thomas + PCR-style reduced system):
-//  level 1  thread p owns rows [i0, i1) (≈ m/P rows, in registers).  A modified Thomas sweep
-//           (forward elimination relative to x_{i0}, backward relative to x_{i1−1}) leaves two
-//           "interface" rows per chunk coupling (x_{i0−1}, x_{i0}, x_{i1−1}) and (x_{i0}, x_{i1−1},
-//           x_{i1}); interior unknowns are x_i = δ'_i − α'_i x_{i0} − γ'_i x_{i1−1}.
-//           Toeplitz operators: α, γ, 1/pivot depend only on the position inside the chunk, so
-//           they are computed once per CTA into shared tables and each thread only sweeps δ.
-//  levels   the 2P interface rows form a tridiagonal system, reduced again by 8-row chunks
-//           (2P → P/2 → …) until ≤ 16 rows remain, solved by one thread (Thomas), then
-//           back-substituted level by level.
-// The row data is staged in shared memory with a padded index (bank-conflict free chunk reads).
+// Design (B200).  One system per G warps (P = 32G threads), NS systems per CTA, two or more CTAs
+// per SM so that one CTA's HBM traffic overlaps another's arithmetic.  The system is brought into
+// shared memory by cp.async (LDGSTS, no register staging) and written back coalesced.  Per system:
+//   level 1   thread p owns a contiguous chunk of Lmin or Lmin+1 rows (long chunks first), held in
+//             registers; a chunk-local elimination (forward sweep keeping the chunk's first unknown
+//             as a spike, backward sweep keeping the last) leaves every interior unknown as
+//             x_j = δ'_j − α'_j x_first − γ'_j x_last and two interface rows per chunk:
+//               F: fa x_{first−1} + fb x_first + fc x_last = fd
+//               G: ga x_first + gb x_last + gc x_{last+1} = gd
+//   tree      adjacent segments are merged pairwise (log2 P levels: 5 by warp shuffles, the rest
+//             through shared memory): merging A = [s, m] and B = [m+1, e] solves the 2×2 system of
+//             A's G row and B's F row for (x_m, x_{m+1}) as affine functions of (x_s, x_e) and
+//             substitutes them into A's F row and B's G row.  The root gives a 2×2 system for
+//             (x_0, x_{m−1}); the stored affine maps then hand every chunk its two boundary values.
+//   back-sub  x_j = δ'_j − α'_j x_first − γ'_j x_last in place, coalesced store.
+// Three variants (template MODE):
+//   MODE_VAR   variable rows (c3): everything computed per row.
+//   MODE_TOEP  Toeplitz rows: the chunk coefficients (pivots, α', γ', F/G rows) depend only on k
+//              and on the position in the chunk, so they are tabulated at cnpint_create (host, long
+//              double); each thread only sweeps its right-hand side.
+//   MODE_FAST  Toeplitz rows with equal chunks except the last (m = P·Ls − r, r ∈ {0, …}): every
+//              merge's coefficient part is data independent and identical along a tree level
+//              (two variants: with / without the last segment), so it is tabulated too and the tree
+//              only carries the right-hand sides fd, gd (2 complex per merge instead of 8).
+// Rows live in shared memory at sidx(i) = i ^ ((i >> padsh) & smask): an XOR swizzle inside each
+// chunk-length block that keeps both the coalesced copies and the per-thread chunk reads
+// bank-conflict free without padding.
 #include "common.cuh"
 #include "internal.h"
 
-struct Row4 {
-  double2 a, b, c, d;
+#include <cstring>
+
+namespace {
+
+struct Seg {
+  double2 fa, fb, fc, fd, ga, gb, gc, gd;
 };
 
-// Generic 8-row chunk forward/backward (general complex coefficients).  In: rows r[0..7].
-// Out: interface rows f, l; interior coefficients (α', γ', δ') for rows 1..6 stored back into
-// r[j].a, r[j].c, r[j].d.
-CNP_DEV bool chunk8(Row4* r, Row4& f, Row4& l) {
-  double2 al[8], ga[8], de[8];
-  bool ok = true;
-  {
-    const double2 inv = crecip(r[1].b);
-    ok &= cfinite(inv);
-    al[1] = cmul(r[1].a, inv);
-    ga[1] = cmul(r[1].c, inv);
-    de[1] = cmul(r[1].d, inv);
-  }
-#pragma unroll
-  for (int j = 2; j < 8; ++j) {
-    const double2 piv = cfms(r[j].b, r[j].a, ga[j - 1]);
-    const double2 inv = crecip(piv);
-    ok &= cfinite(inv);
-    const double2 ai = cmul(r[j].a, inv);
-    al[j] = make_double2(-(ai.x * al[j - 1].x - ai.y * al[j - 1].y), -(ai.x * al[j - 1].y + ai.y * al[j - 1].x));
-    ga[j] = cmul(r[j].c, inv);
-    de[j] = cmul(cfms(r[j].d, r[j].a, de[j - 1]), inv);
-  }
-  l.a = al[7]; l.b = make_double2(1.0, 0.0); l.c = ga[7]; l.d = de[7];
-  double2 ap = make_double2(0.0, 0.0), gp = make_double2(-1.0, 0.0), dp = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int j = 6; j >= 1; --j) {
-    const double2 na = cfms(al[j], ga[j], ap);
-    const double2 ng = make_double2(-(ga[j].x * gp.x - ga[j].y * gp.y), -(ga[j].x * gp.y + ga[j].y * gp.x));
-    const double2 nd = cfms(de[j], ga[j], dp);
-    ap = na; gp = ng; dp = nd;
-    r[j].a = ap; r[j].c = gp; r[j].d = dp;
-  }
-  f.a = r[0].a;
-  f.b = cfms(r[0].b, r[0].c, ap);
-  f.c = make_double2(-(r[0].c.x * gp.x - r[0].c.y * gp.y), -(r[0].c.x * gp.y + r[0].c.y * gp.x));
-  f.d = cfms(r[0].d, r[0].c, dp);
-  return ok;
+CNP_DEV Seg shfl_seg(const Seg& s, int d) {
+  Seg r;
+  r.fa = shfl_down<double2>(s.fa, d); r.fb = shfl_down<double2>(s.fb, d);
+  r.fc = shfl_down<double2>(s.fc, d); r.fd = shfl_down<double2>(s.fd, d);
+  r.ga = shfl_down<double2>(s.ga, d); r.gb = shfl_down<double2>(s.gb, d);
+  r.gc = shfl_down<double2>(s.gc, d); r.gd = shfl_down<double2>(s.gd, d);
+  return r;
 }
 
-// Solve the reduced system stored as Row4 array `lv0` of size n0 (power of two, >= 2) in shared
-// memory.  Scratch for deeper levels follows lv0.  Result x_i written into lv0[i].d.
-CNP_DEV void solve_reduced(Row4* lv0, int n0, int tid, int* status) {
-  // level sizes: n0, n0/4, ... until <= 16
-  Row4* lv[8];
-  int nn[8];
-  int L = 0;
-  lv[0] = lv0;
-  nn[0] = n0;
-  while (nn[L] > 16) {
-    lv[L + 1] = lv[L] + nn[L];
-    nn[L + 1] = nn[L] / 4;
-    ++L;
-  }
-  // downward: reduce level l into level l+1
-  for (int l = 0; l < L; ++l) {
-    const int nt = nn[l] / 8;
-    if (tid < nt) {
-      Row4 r[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = lv[l][8 * tid + j];
-      Row4 f, g;
-      bool ok = chunk8(r, f, g);
-      if (!ok) atomicOr(status, 1);
-#pragma unroll
-      for (int j = 1; j < 7; ++j) lv[l][8 * tid + j] = r[j];
-      lv[l + 1][2 * tid] = f;
-      lv[l + 1][2 * tid + 1] = g;
-    }
-    __syncthreads();
-  }
-  // bottom: Thomas by one thread
-  if (tid == 0) {
-    Row4* r = lv[L];
-    const int n = nn[L];
-    double2 cp[16], dp[16];
-    double2 inv = crecip(r[0].b);
-    bool ok = cfinite(inv);
-    cp[0] = cmul(r[0].c, inv);
-    dp[0] = cmul(r[0].d, inv);
-    for (int i = 1; i < n; ++i) {
-      inv = crecip(cfms(r[i].b, r[i].a, cp[i - 1]));
-      ok &= cfinite(inv);
-      cp[i] = cmul(r[i].c, inv);
-      dp[i] = cmul(cfms(r[i].d, r[i].a, dp[i - 1]), inv);
-    }
-    double2 x = dp[n - 1];
-    r[n - 1].d = x;
-    for (int i = n - 2; i >= 0; --i) {
-      x = cfms(dp[i], cp[i], x);
-      r[i].d = x;
-    }
-    if (!ok) atomicOr(status, 1);
-  }
-  __syncthreads();
-  // upward back-substitution
-  for (int l = L - 1; l >= 0; --l) {
-    const int nt = nn[l] / 8;
-    if (tid < nt) {
-      const double2 x0 = lv[l + 1][2 * tid].d;
-      const double2 x7 = lv[l + 1][2 * tid + 1].d;
-      Row4* r = lv[l] + 8 * tid;
-#pragma unroll
-      for (int j = 1; j < 7; ++j) r[j].d = cfms(cfms(r[j].d, r[j].a, x0), r[j].c, x7);
-      r[0].d = x0;
-      r[7].d = x7;
-    }
-    __syncthreads();
-  }
+// Merge segment A (in place) with its right neighbour B; the affine maps
+//   x_m = P0 + P1 x_s + P2 x_e,  x_{m+1} = R0 + R1 x_s + R2 x_e
+// are written to cf[0..5].  Returns false on a zero / non-finite 2x2 determinant.
+CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf) {
+  const double2 det = csub(cmul(A.gb, B.fb), cmul(A.gc, B.fa));
+  const double2 id = crecip(det);
+  const double2 P0 = cmul(csub(cmul(B.fb, A.gd), cmul(A.gc, B.fd)), id);
+  const double2 P1 = cneg(cmul(cmul(B.fb, A.ga), id));
+  const double2 P2 = cmul(cmul(A.gc, B.fc), id);
+  const double2 R0 = cmul(csub(cmul(A.gb, B.fd), cmul(B.fa, A.gd)), id);
+  const double2 R1 = cmul(cmul(B.fa, A.ga), id);
+  const double2 R2 = cneg(cmul(cmul(A.gb, B.fc), id));
+  cf[0] = P0; cf[1] = P1; cf[2] = P2; cf[3] = R0; cf[4] = R1; cf[5] = R2;
+  A.fb = cfma(A.fc, P1, A.fb);
+  A.fd = cfms(A.fd, A.fc, P0);
+  A.fc = cmul(A.fc, P2);
+  A.ga = cmul(B.ga, R1);
+  A.gb = cfma(B.ga, R2, B.gb);
+  A.gd = cfms(B.gd, B.ga, R0);
+  A.gc = B.gc;
+  return cfinite(id);
 }
 
-// Main kernel.  TOEP: constant rows (lo, di, up taken from index 1).  LMAX: max rows per thread.
-template <bool TOEP, int LMAX>
-__global__ void __launch_bounds__(256) k_tridiag(const double2* __restrict__ what, double2* __restrict__ zhat,
-                                                 const double* __restrict__ lo, const double* __restrict__ di,
-                                                 const double* __restrict__ up, const double2* __restrict__ sk,
-                                                 const double2* __restrict__ il2, int m, int64_t W, double tau,
-                                                 int* __restrict__ status) {
+CNP_DEV void unmerge(const double2* cf, double2 xs, double2 xe, double2& xm, double2& xm1) {
+  xm = cfma(cf[2], xe, cfma(cf[1], xs, cf[0]));
+  xm1 = cfma(cf[5], xe, cfma(cf[4], xs, cf[3]));
+}
+
+}  // namespace
+
+enum { MODE_VAR = 0, MODE_TOEP = 1, MODE_FAST = 2 };
+
+// Toeplitz table per frequency k (tri_cfg().tabstride complex entries):
+//   [0, L)                   inv_j = 1/pivot_j of the chunk forward sweep (j = 1..L−1)
+//   v = 0, 1 (chunk length Lmin + v), base L + v(2L+3):
+//     +0 α_{len−1} (G row ga)   +1 F row fb   +2 F row fc   +3.. α'_j (j < L)   +3+L.. γ'_j (j < L)
+//   fast tree, base 5L+6, level q = 0..NLV−1, variant v (0 standard, 1 merge with the last
+//   segment), 10 entries: pa pb ra rb P1 P2 R1 R2 fcA gaB, with
+//     P0 = pa gd_A + pb fd_B,  R0 = ra fd_B + rb gd_A,  fd ← fd_A − fcA P0,  gd ← gd_B − gaB R0,
+//     x_m = P0 + P1 x_s + P2 x_e,  x_{m+1} = R0 + R1 x_s + R2 x_e;
+//   root (4 entries): x_0 = c0 fd + c1 gd,  x_{m−1} = c2 fd + c3 gd.
+template <int MODE, int L>
+__global__ void __launch_bounds__(256)
+    k_tridiag(const double2* __restrict__ what, double2* __restrict__ zhat, const double* __restrict__ lo,
+              const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
+              const double2* __restrict__ il2, const double2* __restrict__ tab, int m, int64_t W, int K, int G,
+              int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status) {
+  constexpr bool TOEP = MODE != MODE_VAR;
+  constexpr bool FAST = MODE == MODE_FAST;
+  constexpr int NCF = FAST ? 2 : 6;  // stored coefficients per merge
+  constexpr int L1S = 5 * L + 6;
   extern __shared__ double2 smem[];
-  double2* D = smem;  // padded data [padi(m)]
-  __shared__ double2 tal[LMAX], tga[LMAX], tiv[LMAX];      // Toeplitz forward tables (pos 1..LMAX-1)
-  __shared__ double2 tba[2][LMAX], tbg[2][LMAX];           // Toeplitz backward tables (two lengths)
-  const int k = blockIdx.x;
-  const int tid = threadIdx.x, P = blockDim.x;
-  const double2 s = sk[k];
-  const double2 il = il2[k];
-  const double2* src = what + (int64_t)k * W;
-  // ---- coalesced load of row k, scaled by 1/λ2_k
-  for (int i = tid; i < m; i += P) D[padi(i)] = cmul(ldg_cs2(src + i), il);
-  const int i0 = (int)(((int64_t)tid * m) / P);
-  const int i1 = (int)(((int64_t)(tid + 1) * m) / P);
-  const int len = i1 - i0;
-  const int lmin = m / P;
-  if (TOEP) {
-    if (tid == 0) {
+  const int nwarp = NS * G, P = 32 * G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp / G, wg = warp - g * G, p = wg * 32 + lane;
+  const int MP = tri_rows_alloc(m, padsh);
+  const int per_sys = TOEP ? MP + TS : 3 * MP;
+  double2* const D = smem + g * per_sys;
+  double2* const T = D + MP;                 // Toeplitz table
+  double2* const Ap = D + MP;                // variable rows: α'
+  double2* const Gp = D + 2 * MP;            //                γ'
+  double2* const coefw = smem + NS * per_sys;            // [nwarp][31][NCF]
+  double2* const coefx = coefw + nwarp * 31 * NCF;       // [NS][15][NCF]
+  double2* const segr = coefx + NS * 15 * NCF;           // [nwarp][8]
+  double2* const bnd = segr + nwarp * 8;                 // [nwarp][2]
+  auto sidx = [&](int i) { return i ^ ((i >> padsh) & smask); };
+  const int k = blockIdx.x * NS + g;
+  const bool act = k < K;  // uniform over the system's warps
+  // ---------------- asynchronous load of the system (and its table) into shared memory
+  if (act) {
+    const double2* src = what + (int64_t)k * W;
+    for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
+    if (TOEP)
+      for (int i = p; i < TS; i += P) cp_async16(T + i, tab + (size_t)k * TS + i);
+  }
+  cp_async_commit();
+  const int Lmin = m / P, nlong = m - P * Lmin;
+  const int len = p < nlong ? Lmin + 1 : Lmin;
+  const int i0 = p < nlong ? p * (Lmin + 1) : nlong * (Lmin + 1) + (p - nlong) * Lmin;
+  const int i1 = i0 + len;
+  bool ok = true;
+  double2 il = make_double2(0.0, 0.0), skk = il;
+  if (act) { il = il2[k]; skk = sk[k]; }
+  cp_async_wait<0>();
+  __syncthreads();
+  Seg sg;
+  if (act) {
+    double2 dl[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) dl[j] = (j < len) ? cmul(D[sidx(i0 + j)], il) : make_double2(0.0, 0.0);
+    if (TOEP) {
+      const double2* tv = T + L + (len - Lmin) * (2 * L + 3);
       const double a = -tau * lo[1], c = -tau * up[1];
-      const double2 b = make_double2(s.x - tau * di[1], s.y);
-      double2 g = make_double2(0.0, 0.0), al = make_double2(0.0, 0.0);
-      for (int j = 1; j < LMAX; ++j) {
-        const double2 piv = (j == 1) ? b : crfms(b, a, g);
-        const double2 inv = crecip(piv);
-        if (!cfinite(inv)) atomicOr(status, 1);
-        al = (j == 1) ? cscale(inv, a) : cscale(cmul(al, inv), -a);
-        g = cscale(inv, c);
-        tal[j] = al; tga[j] = g; tiv[j] = inv;
+      // forward: δ_1 = d_1 inv_1, δ_j = (d_j − a δ_{j−1}) inv_j
+      double2 last = dl[0];
+#pragma unroll
+      for (int j = 1; j < L; ++j) {
+        if (j < len) {
+          last = cmul(j == 1 ? dl[1] : crfms(dl[j], a, last), T[j]);
+          dl[j] = last;
+        }
       }
-      for (int which = 0; which < 2; ++which) {
-        const int L = lmin + which;
-        double2 ap = make_double2(0.0, 0.0), gp = make_double2(-1.0, 0.0);
-        if (L - 1 < LMAX) { tba[which][L - 1] = ap; tbg[which][L - 1] = gp; }
-        for (int j = L - 2; j >= 1; --j) {
-          const double2 na = cfms(tal[j], tga[j], ap);
-          const double2 ng = make_double2(-(tga[j].x * gp.x - tga[j].y * gp.y), -(tga[j].x * gp.y + tga[j].y * gp.x));
-          ap = na; gp = ng;
-          tba[which][j] = ap; tbg[which][j] = gp;
+      sg.gd = last;
+      if (!FAST) {
+        sg.ga = tv[0];
+        sg.gb = make_double2(1.0, 0.0);
+        sg.gc = cscale(T[len - 1], c);
+      }
+      // backward: δ'_j = δ_j − γ_j δ'_{j+1}, γ_j = c inv_j  (δ'_{len−2} = δ_{len−2})
+#pragma unroll
+      for (int j = L - 3; j >= 1; --j)
+        if (j <= len - 3) dl[j] = cfms(dl[j], cscale(T[j], c), dl[j + 1]);
+      if (!FAST) {
+        sg.fa = make_double2(i0 == 0 ? 0.0 : a, 0.0);
+        sg.fb = tv[1];
+        sg.fc = tv[2];
+      }
+      sg.fd = len >= 3 ? crfms(dl[0], c, dl[1]) : dl[0];
+#pragma unroll
+      for (int j = 1; j < L - 1; ++j)
+        if (j <= len - 2) D[sidx(i0 + j)] = dl[j];
+    } else {
+      double2 ap[L], gp[L];
+      double2 alp = make_double2(0.0, 0.0), gam = alp, last = dl[0];
+#pragma unroll
+      for (int j = 1; j < L; ++j) {
+        if (j < len) {
+          const int i = i0 + j;
+          const double a = -tau * lo[i], c = -tau * up[i];
+          const double2 bb = make_double2(skk.x - tau * di[i], skk.y);
+          const double2 piv = (j == 1) ? bb : crfms(bb, a, gam);
+          const double2 inv = crecip(piv);
+          ok &= cfinite(inv);
+          alp = (j == 1) ? cscale(inv, a) : cscale(cmul(alp, inv), -a);
+          gam = cscale(inv, c);
+          last = (j == 1) ? cmul(dl[1], inv) : cmul(crfms(dl[j], a, last), inv);
+          dl[j] = last;
+          ap[j] = alp;
+          gp[j] = gam;
+        }
+      }
+      sg.ga = alp;
+      sg.gb = make_double2(1.0, 0.0);
+      sg.gc = gam;
+      sg.gd = last;
+#pragma unroll
+      for (int j = L - 3; j >= 1; --j) {
+        if (j <= len - 3) {
+          const double2 gj = gp[j];
+          dl[j] = cfms(dl[j], gj, dl[j + 1]);
+          ap[j] = cfms(ap[j], gj, ap[j + 1]);
+          gp[j] = cneg(cmul(gj, gp[j + 1]));
+        }
+      }
+      const double a0 = -tau * lo[i0], c0 = -tau * up[i0];
+      const double2 b0 = make_double2(skk.x - tau * di[i0], skk.y);
+      sg.fa = make_double2(a0, 0.0);
+      if (len >= 3) {
+        sg.fb = crfms(b0, c0, ap[1]);
+        sg.fc = cscale(gp[1], -c0);
+        sg.fd = crfms(dl[0], c0, dl[1]);
+      } else {
+        sg.fb = b0;
+        sg.fc = make_double2(c0, 0.0);
+        sg.fd = dl[0];
+      }
+#pragma unroll
+      for (int j = 1; j < L - 1; ++j) {
+        if (j <= len - 2) {
+          const int q = sidx(i0 + j);
+          D[q] = dl[j];
+          Ap[q] = ap[j];
+          Gp[q] = gp[j];
         }
       }
     }
   }
-  __syncthreads();
-  // ---- level 1: per-thread modified Thomas on rows [i0, i1)
-  double2 dl[LMAX];
-  double2 alr[TOEP ? 1 : LMAX], gar[TOEP ? 1 : LMAX];
+  // ---------------- tree up: 5 warp levels
+  double2* cw = coefw + warp * 31 * NCF;
+  const double2* TT = T + L1S;  // fast-tree table
+  if (act) {
 #pragma unroll
-  for (int j = 0; j < LMAX; ++j) dl[j] = (j < len) ? D[padi(i0 + j)] : make_double2(0.0, 0.0);
-  bool ok = true;
-  Row4 f, l;
-  if (TOEP) {
-    const double a = -tau * lo[1], c = -tau * up[1];
-    const double2 b = make_double2(s.x - tau * di[1], s.y);
-    // forward δ (positions 1..len-1)
-    double2 dprev = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = 1; j < LMAX; ++j) {
-      if (j < len) {
-        const double2 num = (j == 1) ? dl[1] : crfms(dl[j], a, dprev);
-        dprev = cmul(num, tiv[j]);
-        dl[j] = dprev;
+    for (int lv = 1; lv <= 5; ++lv) {
+      const int sft = 1 << (lv - 1);
+      const bool left = (lane & ((1 << lv) - 1)) == 0;
+      double2* slot = cw + (32 - (64 >> lv) + (lane >> lv)) * NCF;
+      if (FAST) {
+        const double2 fdB = shfl_down<double2>(sg.fd, sft), gdB = shfl_down<double2>(sg.gd, sft);
+        if (left) {
+          const int v = (wg == G - 1 && lane + 2 * sft == 32) ? 1 : 0;
+          const double2* cf = TT + ((lv - 1) * 2 + v) * 10;
+          const double2 P0 = cfma(cf[0], sg.gd, cmul(cf[1], fdB));
+          const double2 R0 = cfma(cf[2], fdB, cmul(cf[3], sg.gd));
+          slot[0] = P0;
+          slot[1] = R0;
+          sg.fd = cfms(sg.fd, cf[8], P0);
+          sg.gd = cfms(gdB, cf[9], R0);
+        }
+      } else {
+        const Seg B = shfl_seg(sg, sft);
+        if (left) ok &= merge(sg, B, slot);
       }
     }
-    const int which = len - lmin;
-    l.a = tal[len - 1]; l.b = make_double2(1.0, 0.0); l.c = tga[len - 1]; l.d = dl[len - 1];
-    if (i1 == m) l.c = make_double2(0.0, 0.0);
-    // backward δ' (positions len-2..1)
-    double2 dp = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = LMAX - 2; j >= 1; --j) {
-      if (j <= len - 2) {
-        dp = cfms(dl[j], tga[j], dp);
-        dl[j] = dp;
-      }
+  }
+  double2 xs = make_double2(0.0, 0.0), xe = make_double2(0.0, 0.0);
+  auto root = [&](const Seg& t) {
+    if (FAST) {
+      const double2* r = TT + (5 + logG) * 20;
+      xs = cfma(r[0], t.fd, cmul(r[1], t.gd));
+      xe = cfma(r[2], t.fd, cmul(r[3], t.gd));
+      return;
     }
-    const double2 ap1 = (len >= 3) ? tba[which][1] : make_double2(0.0, 0.0);
-    const double2 gp1 = (len >= 3) ? tbg[which][1] : make_double2(-1.0, 0.0);
-    const double2 dp1 = (len >= 3) ? dl[1] : make_double2(0.0, 0.0);
-    f.a = make_double2(i0 == 0 ? 0.0 : a, 0.0);
-    f.b = cfms(b, make_double2(c, 0.0), ap1);
-    f.c = cscale(gp1, -c);
-    f.d = crfms(dl[0], c, dp1);
+    // fb x_0 + fc x_{m−1} = fd ; ga x_0 + gb x_{m−1} = gd  (x_{−1} = x_m = 0)
+    const double2 det = csub(cmul(t.fb, t.gb), cmul(t.fc, t.ga));
+    const double2 id = crecip(det);
+    ok &= cfinite(id);
+    xs = cmul(csub(cmul(t.fd, t.gb), cmul(t.fc, t.gd)), id);
+    xe = cmul(csub(cmul(t.fb, t.gd), cmul(t.ga, t.fd)), id);
+  };
+  if (G == 1) {
+    if (act && lane == 0) root(sg);
   } else {
-    // general rows: coefficients per row
-    double2 dprev = make_double2(0.0, 0.0), gprev = make_double2(0.0, 0.0), aprev = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int j = 1; j < LMAX; ++j) {
-      if (j < len) {
-        const int i = i0 + j;
-        const double a = -tau * lo[i], c = -tau * up[i];
-        const double2 b = make_double2(s.x - tau * di[i], s.y);
-        const double2 piv = (j == 1) ? b : crfms(b, a, gprev);
-        const double2 inv = crecip(piv);
-        ok &= cfinite(inv);
-        aprev = (j == 1) ? cscale(inv, a) : cscale(cmul(aprev, inv), -a);
-        gprev = cscale(inv, c);
-        dprev = (j == 1) ? cmul(dl[1], inv) : cmul(crfms(dl[j], a, dprev), inv);
-        alr[j] = aprev; gar[j] = gprev; dl[j] = dprev;
+    // ---------------- cross-warp levels (warp 0 of the system, lanes 0..G−1)
+    if (lane == 0) {
+      double2* r = segr + warp * 8;
+      r[3] = sg.fd; r[7] = sg.gd;
+      if (!FAST) { r[0] = sg.fa; r[1] = sg.fb; r[2] = sg.fc; r[4] = sg.ga; r[5] = sg.gb; r[6] = sg.gc; }
+    }
+    named_sync(1 + g, 32 * G);
+    if (wg == 0 && act) {
+      Seg t = sg;
+      if (lane < G) {
+        const double2* r = segr + (g * G + lane) * 8;
+        t.fd = r[3]; t.gd = r[7];
+        if (!FAST) { t.fa = r[0]; t.fb = r[1]; t.fc = r[2]; t.ga = r[4]; t.gb = r[5]; t.gc = r[6]; }
+      }
+      double2* cx = coefx + g * 15 * NCF;
+      for (int lv = 1; lv <= logG; ++lv) {
+        const int sft = 1 << (lv - 1);
+        const bool left = (lane & ((1 << lv) - 1)) == 0 && lane < G;
+        double2* slot = cx + (G - (2 * G >> lv) + (lane >> lv)) * NCF;
+        if (FAST) {
+          const double2 fdB = shfl_down<double2>(t.fd, sft), gdB = shfl_down<double2>(t.gd, sft);
+          if (left) {
+            const int v = (lane + 2 * sft == G) ? 1 : 0;
+            const double2* cf = TT + ((5 + lv - 1) * 2 + v) * 10;
+            const double2 P0 = cfma(cf[0], t.gd, cmul(cf[1], fdB));
+            const double2 R0 = cfma(cf[2], fdB, cmul(cf[3], t.gd));
+            slot[0] = P0;
+            slot[1] = R0;
+            t.fd = cfms(t.fd, cf[8], P0);
+            t.gd = cfms(gdB, cf[9], R0);
+          }
+        } else {
+          const Seg B = shfl_seg(t, sft);
+          if (left) ok &= merge(t, B, slot);
+        }
+      }
+      if (lane == 0) root(t);
+      for (int lv = logG; lv >= 1; --lv) {
+        const int sft = 1 << (lv - 1);
+        const bool left = (lane & ((1 << lv) - 1)) == 0 && lane < G;
+        const bool right = (lane & ((1 << lv) - 1)) == sft && lane < G;
+        double2 xm = make_double2(0.0, 0.0), xm1 = xm;
+        if (left) {
+          const double2* slot = cx + (G - (2 * G >> lv) + (lane >> lv)) * NCF;
+          if (FAST) {
+            const int v = (lane + 2 * sft == G) ? 1 : 0;
+            const double2* cf = TT + ((5 + lv - 1) * 2 + v) * 10;
+            xm = cfma(cf[5], xe, cfma(cf[4], xs, slot[0]));
+            xm1 = cfma(cf[7], xe, cfma(cf[6], xs, slot[1]));
+          } else {
+            unmerge(slot, xs, xe, xm, xm1);
+          }
+        }
+        const double2 rs = shfl_up2(xm1, sft), re = shfl_up2(xe, sft);
+        if (left) xe = xm;
+        if (right) { xs = rs; xe = re; }
+      }
+      if (lane < G) {
+        bnd[(g * G + lane) * 2] = xs;
+        bnd[(g * G + lane) * 2 + 1] = xe;
       }
     }
-    l.a = aprev; l.b = make_double2(1.0, 0.0); l.c = gprev; l.d = dprev;
-    double2 ap = make_double2(0.0, 0.0), gp = make_double2(-1.0, 0.0), dp = make_double2(0.0, 0.0);
+    named_sync(1 + g, 32 * G);
+    if (lane == 0) {
+      xs = bnd[warp * 2];
+      xe = bnd[warp * 2 + 1];
+    }
+  }
+  if (act) {
+    // ---------------- tree down: 5 warp levels
 #pragma unroll
-    for (int j = LMAX - 2; j >= 1; --j) {
-      if (j <= len - 2) {
-        const double2 na = cfms(alr[j], gar[j], ap);
-        const double2 ng = make_double2(-(gar[j].x * gp.x - gar[j].y * gp.y), -(gar[j].x * gp.y + gar[j].y * gp.x));
-        dp = cfms(dl[j], gar[j], dp);
-        ap = na; gp = ng;
-        alr[j] = ap; gar[j] = gp; dl[j] = dp;
+    for (int lv = 5; lv >= 1; --lv) {
+      const int sft = 1 << (lv - 1);
+      const bool left = (lane & ((1 << lv) - 1)) == 0;
+      const bool right = (lane & ((1 << lv) - 1)) == sft;
+      double2 xm = make_double2(0.0, 0.0), xm1 = xm;
+      if (left) {
+        const double2* slot = cw + (32 - (64 >> lv) + (lane >> lv)) * NCF;
+        if (FAST) {
+          const int v = (wg == G - 1 && lane + 2 * sft == 32) ? 1 : 0;
+          const double2* cf = TT + ((lv - 1) * 2 + v) * 10;
+          xm = cfma(cf[5], xe, cfma(cf[4], xs, slot[0]));
+          xm1 = cfma(cf[7], xe, cfma(cf[6], xs, slot[1]));
+        } else {
+          unmerge(slot, xs, xe, xm, xm1);
+        }
+      }
+      const double2 rs = shfl_up2(xm1, sft), re = shfl_up2(xe, sft);
+      if (left) xe = xm;
+      if (right) { xs = rs; xe = re; }
+    }
+    // ---------------- back-substitution in place
+    D[sidx(i0)] = xs;
+    D[sidx(i1 - 1)] = xe;
+    if (TOEP) {
+      const double2* tv = T + L + (len - Lmin) * (2 * L + 3);
+#pragma unroll
+      for (int j = 1; j < L - 1; ++j) {
+        if (j <= len - 2) {
+          const int q = sidx(i0 + j);
+          D[q] = cfms(cfms(D[q], tv[3 + j], xs), tv[3 + L + j], xe);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 1; j < L - 1; ++j) {
+        if (j <= len - 2) {
+          const int q = sidx(i0 + j);
+          D[q] = cfms(cfms(D[q], Ap[q], xs), Gp[q], xe);
+        }
       }
     }
-    const double a0 = -tau * lo[i0], c0 = -tau * up[i0];
-    const double2 b0 = make_double2(s.x - tau * di[i0], s.y);
-    const double2 ap1 = (len >= 3) ? alr[1] : make_double2(0.0, 0.0);
-    const double2 gp1 = (len >= 3) ? gar[1] : make_double2(-1.0, 0.0);
-    const double2 dp1 = (len >= 3) ? dl[1] : make_double2(0.0, 0.0);
-    f.a = make_double2(a0, 0.0);
-    f.b = cfms(b0, make_double2(c0, 0.0), ap1);
-    f.c = cscale(gp1, -c0);
-    f.d = crfms(dl[0], c0, dp1);
     if (!ok) atomicOr(status, 1);
   }
-  __syncthreads();  // D is now free: reuse it for the reduced system
-  Row4* R = reinterpret_cast<Row4*>(smem);
-  R[2 * tid] = f;
-  R[2 * tid + 1] = l;
   __syncthreads();
-  solve_reduced(R, 2 * P, tid, status);
-  const double2 x0 = R[2 * tid].d, xl = R[2 * tid + 1].d;
-  __syncthreads();
-  // ---- back-substitute interior rows, stage into D, coalesced store
-  D[padi(i0)] = x0;
-  D[padi(i1 - 1)] = xl;
-  if (TOEP) {
-    const int which = len - lmin;
-#pragma unroll
-    for (int j = 1; j < LMAX - 1; ++j)
-      if (j <= len - 2) D[padi(i0 + j)] = cfms(cfms(dl[j], tba[which][j], x0), tbg[which][j], xl);
-  } else {
-#pragma unroll
-    for (int j = 1; j < LMAX - 1; ++j)
-      if (j <= len - 2) D[padi(i0 + j)] = cfms(cfms(dl[j], alr[j], x0), gar[j], xl);
+  if (act) {
+    double2* dst = zhat + (int64_t)k * W;
+    for (int i = p; i < m; i += P) stg_cs2(dst + i, D[sidx(i)]);
+    for (int i = m + p; i < W; i += P) dst[i] = make_double2(0.0, 0.0);
   }
-  __syncthreads();
-  double2* dst = zhat + (int64_t)k * W;
-  for (int i = tid; i < m; i += P) stg_cs2(dst + i, D[padi(i)]);
 }
 
 // Small-m path (m < 64): one thread per frequency, plain Thomas on the scaled system.
@@ -320,13 +427,68 @@ __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __res
     x = cfms(dp[i], cp[i], x);
     dst[i] = x;
   }
+  for (int i = m; i < W; ++i) dst[i] = make_double2(0.0, 0.0);
   if (!ok) atomicOr(status, 1);
 }
 
-static int pow2_at_least(int v) {
-  int p = 1;
-  while (p < v) p <<= 1;
-  return p;
+TriCfg tri_cfg(int m, int toeplitz) {
+  TriCfg t;
+  std::memset(&t, 0, sizeof(t));
+  t.small = m < 64;
+  // chunks of <= Lcap rows: Lcap = 16 (Toeplitz: only the right-hand side lives in registers) or 8
+  // (variable rows also carry α', γ'); G = warps per system, NS = systems per CTA (<= 8 warps).
+  const int Lcap = toeplitz ? 16 : 8;
+  int G = 1;
+  while (G < 16 && 32 * G * Lcap < m) G <<= 1;
+  t.G = G;
+  t.logG = 0;
+  while ((1 << t.logG) < G) ++t.logG;
+  const int P = 32 * G;
+  const int need = (m + P - 1) / P;
+  t.L = need <= 4 ? 4 : need <= 8 ? 8 : need <= 16 ? 16 : -1;
+  if (!toeplitz && t.L > 8) t.L = -1;
+  t.Lmin = m / P;
+  const int nlong = m - P * t.Lmin;
+  t.fast = toeplitz && (nlong == 0 || nlong == P - 1);
+  const int Ls = nlong ? t.Lmin + 1 : t.Lmin;  // swizzle block = the standard chunk length
+  t.padsh = 0;
+  while ((1 << (t.padsh + 1)) <= Ls) ++t.padsh;
+  t.smask = (1 << t.padsh) - 1;
+  if (t.smask > 7) t.smask = 7;
+  t.nlv = 5 + t.logG;
+  t.tabstride = toeplitz && t.L > 0 ? 5 * t.L + 6 + t.nlv * 20 + 4 : 0;
+  t.NS = G >= 8 ? 1 : 8 / G;
+  const int MP = tri_rows_alloc(m, t.padsh);
+  const int per_sys = toeplitz ? MP + t.tabstride : 3 * MP;
+  const int ncf = t.fast ? 2 : 6;
+  auto smem_of = [&](int ns) {
+    const int nw = ns * G;
+    return (size_t)(ns * per_sys + nw * 31 * ncf + ns * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
+  };
+  while (t.NS > 1 && smem_of(t.NS) > 110 * 1024) t.NS >>= 1;
+  t.smem = smem_of(t.NS);
+  return t;
+}
+
+template <int MODE, int L>
+static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_tridiag<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int K = c->H + 1;
+  const int grid = (K + t.NS - 1) / t.NS;
+  // shared memory of this variant (the generic trees store 6 coefficients per merge, the fast one 2)
+  const int ncf = MODE == MODE_FAST ? 2 : 6, nw = t.NS * t.G;
+  const int MP = tri_rows_alloc(c->nx, t.padsh);
+  const size_t smem = (size_t)(t.NS * (MODE == MODE_VAR ? 3 * MP : MP + t.tabstride) + nw * 31 * ncf +
+                               t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
+  k_tridiag<MODE, L><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
+      what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS,
+      t.padsh, t.smask, t.tabstride, c->tau, c->d_status);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat) {
@@ -335,41 +497,26 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
   const int64_t W = c->ld;
   cnp_prof_begin(c, KID_TRIDIAG);
   const double bytes = 32.0 * cnp_spec_units(c);
-  if (m < 64) {
+  const TriCfg t = tri_cfg(m, c->toeplitz);
+  cudaError_t e;
+  if (t.small) {
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
                                                             m, W, c->tau, K, c->d_status);
-    cnp_prof_end(c, KID_TRIDIAG, bytes);
-    return cudaGetLastError();
-  }
-  const int LM = c->toeplitz ? 16 : 8;
-  int P = pow2_at_least((m + LM - 1) / LM);
-  if (P < 32) P = 32;
-  while (P > 32 && m / P < 2) P >>= 1;
-  if (P > 256) return cudaErrorInvalidValue;
-  // shared memory: padded data, or the reduced system (2P rows + deeper levels), whichever is larger
-  size_t data = (size_t)(padi_host(m) + 1) * sizeof(double2);
-  size_t red = (size_t)(2 * P + P) * sizeof(Row4);
-  size_t smem = data > red ? data : red;
-  cudaError_t e;
-  if (c->toeplitz) {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k_tridiag<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k_tridiag<true, 16><<<K, P, smem, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, m, W,
-                                                    c->tau, c->d_status);
+    e = cudaGetLastError();
+  } else if (!c->toeplitz) {
+    e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, what, zhat)
+                                                                     : cudaErrorInvalidValue;
+  } else if (t.fast && !(c->debug & 4)) {
+    e = t.L == 4 ? run_tri<MODE_FAST, 4>(c, t, what, zhat)
+      : t.L == 8 ? run_tri<MODE_FAST, 8>(c, t, what, zhat)
+      : t.L == 16 ? run_tri<MODE_FAST, 16>(c, t, what, zhat)
+                  : cudaErrorInvalidValue;
   } else {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k_tridiag<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k_tridiag<false, 8><<<K, P, smem, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, m, W,
-                                                    c->tau, c->d_status);
+    e = t.L == 4 ? run_tri<MODE_TOEP, 4>(c, t, what, zhat)
+      : t.L == 8 ? run_tri<MODE_TOEP, 8>(c, t, what, zhat)
+      : t.L == 16 ? run_tri<MODE_TOEP, 16>(c, t, what, zhat)
+                  : cudaErrorInvalidValue;
   }
   cnp_prof_end(c, KID_TRIDIAG, bytes);
-  return cudaGetLastError();
+  return e;
 }

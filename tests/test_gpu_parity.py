@@ -142,6 +142,21 @@ def test_stage_kernels(name):
     assert rel(s.to_host(z), z_o) < 1e-13
 
 
+@pytest.mark.parametrize("name", ["1d_small", "1d_mid_fast", "c1", "1d_ragged"])
+@pytest.mark.parametrize("debug", [0, 4])
+def test_pinv_k3_tree_variants(name, debug):
+    """K3's tabulated fast tree (debug 0) and the generic merge tree (debug 4) both match the oracle."""
+    w = SMALL.get(name) or synth.scaled(synth.C1, 127, 64, alpha=0.01)
+    s = solver_for(w)
+    s.set_debug(debug)
+    op = problem.build_operator(w)
+    for v in synth.random_vectors(w, 2, 21):
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        assert rel(s.to_host(z), precond.pinv_dft(w, op, v)) < 1e-12, (name, debug)
+    assert s.device_status() == 0
+
+
 @pytest.mark.parametrize("debug", [1, 2])
 def test_negative_controls_break_parity(debug):
     """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail."""
