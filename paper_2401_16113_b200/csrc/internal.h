@@ -102,6 +102,16 @@ cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat);
 cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 
+// N <= 16384: x-pair packed thread-block-cluster variant (k_tfft.cu)
+struct TfftCfg {
+  int C, logN2, X, CS, T, ok;
+  size_t smem;
+};
+TfftCfg tfft_cfg(int N);
+cudaError_t launch_tfft_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
+cudaError_t launch_tfft_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
+cudaError_t launch_tfft_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
+
 // 2D
 cudaError_t launch_dst_x(cnpint_ctx* c, const double* in, double* out, const double* vscale, int inverse);
 cudaError_t launch_dst_y(cnpint_ctx* c, const double* in, double* out, int inverse);

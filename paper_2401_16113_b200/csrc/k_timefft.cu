@@ -216,12 +216,17 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
   return cudaGetLastError();
 }
 
+// N <= 16384 goes to the cluster kernels of k_tfft.cu; larger N stays here (one column per CTA,
+// even/odd time packing).  debug bit 8 forces this path (cross-check in the parity tests).
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what) {
+  if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_fwd(c, v, vscale, what);
   return run_fft<0>(c, v, nullptr, nullptr, what, vscale, 0);
 }
 cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate) {
+  if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_inv(c, zhat, z, accumulate);
   return run_fft<1>(c, nullptr, zhat, z, nullptr, nullptr, accumulate);
 }
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
+  if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_pass_2d(c, in, out, vscale);
   return run_fft<2>(c, in, nullptr, out, nullptr, vscale, 0);
 }
