@@ -142,7 +142,9 @@ cnpint_status cnpint_time_ifft(cnpint_ctx* ctx, const double* d_zhat, double* d_
  * guess.  Stops when the Givens estimate |g_{j+1}|/||b|| <= tol and then
  * confirms the true residual ||b − 𝓜u||/||b|| <= tol at the cycle end (else restarts).
  * Arnoldi: classical Gram–Schmidt with one reorthogonalisation (CGS2), fused device kernels;
- * Hessenberg least squares (Givens) on device; one 8-byte device→host read per inner step.
+ * Hessenberg least squares (Givens) on device; one 64-byte device→host read per inner step.
+ * The preconditioned directions z_j = P_α⁻¹ v_j are kept for the cycle, so the update is
+ * u += Σ_j y_j z_j (= P_α⁻¹ V y, same iterate) without a further P_α⁻¹ application.
  * 0 < tol < 1, 1 <= restart <= restart_max, maxit >= 1 (total inner steps).
  * Returns CNPINT_OK, CNPINT_ENOCONV (maxit reached; u holds the last iterate, so
  * maxit = j <= restart returns the j-th GMRES iterate) or an error.  rep may be NULL. */

@@ -73,7 +73,7 @@ bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 struct Layout {
   size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
-  size_t V, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
+  size_t V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
   size_t total;
 };
 
@@ -136,6 +136,7 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   L.io1 = take(vec * 8); L.io2 = take(vec * 8); L.io3 = take(vec * 8);
   if (restart_max >= 1) {
     L.V = take((size_t)(restart_max + 1) * vec * 8);
+    L.Z = take((size_t)restart_max * vec * 8);  // z_j = P_α⁻¹ v_j of the current cycle
     L.c1 = take((restart_max + 2) * 8); L.c2 = take((restart_max + 2) * 8); L.scl = take((restart_max + 2) * 8);
     L.H = take((size_t)(restart_max + 1) * restart_max * 8);
     L.cs = take(restart_max * 8); L.sn = take(restart_max * 8); L.g = take((restart_max + 2) * 8);
@@ -429,7 +430,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
     c->d_twx = (double2*)(w + L.twx); c->d_twy = (double2*)(w + L.twy);
   }
   if (restart_max >= 1) {
-    c->d_V = (double*)(w + L.V); c->d_c1 = (double*)(w + L.c1); c->d_c2 = (double*)(w + L.c2);
+    c->d_V = (double*)(w + L.V); c->d_Z = (double*)(w + L.Z); c->d_c1 = (double*)(w + L.c1); c->d_c2 = (double*)(w + L.c2);
     c->d_scl = (double*)(w + L.scl); c->d_H = (double*)(w + L.H); c->d_cs = (double*)(w + L.cs);
     c->d_sn = (double*)(w + L.sn); c->d_g = (double*)(w + L.g); c->d_y = (double*)(w + L.y);
     c->d_coef = (double*)(w + L.coef);
@@ -637,18 +638,18 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     return CNPINT_OK;
   }
   if (!std::isfinite(h[0])) { seterr(c, "gmres: ||b|| not finite"); return CNPINT_EBREAKDOWN; }
-  double* z = c->dim == 1 ? c->d_tmp1 : c->d_tmp3;
-  double* tcomb = c->dim == 1 ? c->d_tmp2 : c->d_io1;
+  std::vector<double*> Z(restart);
+  for (int i = 0; i < restart; ++i) Z[i] = c->d_Z + (size_t)i * vec;
   while (true) {
     int jdone = 0;
     bool stop_inner = false;
     for (int j = 0; j < restart && !stop_inner; ++j) {
-      // z = P_α⁻¹ v_j  (v_j = s_j Ṽ_j; the scale is folded into the Γ-scaling)
-      cnpint_status st = pinv_dev(c, V[j], c->d_scl + j, z, 0);
+      // z_j = P_α⁻¹ v_j  (v_j = s_j Ṽ_j; the scale is folded into the Γ-scaling), kept for the update
+      cnpint_status st = pinv_dev(c, V[j], c->d_scl + j, Z[j], 0);
       if (st != CNPINT_OK) return st;
-      // w = 𝓜 z, written straight into the slot of Ṽ_{j+1}
+      // w = 𝓜 z_j, written straight into the slot of Ṽ_{j+1}
       double* w = V[j + 1];
-      CK(launch_matvec(c, z, w, 0, nullptr, nullptr));
+      CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
       const int nv = j + 1;
       if (nv <= CNP_MAX_DOT) {
         CK(launch_dots(c, V.data(), nv, w, c->d_part));
@@ -692,19 +693,11 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       }
       if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
     }
-    // cycle end: y = H⁻¹g, t = V y, u += P⁻¹ t, r = b − 𝓜u
+    // cycle end: y = H⁻¹g, u += Σ y_j z_j  (= P⁻¹ V y: the stored z_j make the extra P⁻¹ unnecessary)
     CK(launch_small(c, 2, jdone, 0));
-    {
-      std::vector<double*> Vc(V.begin(), V.begin() + jdone);
-      for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
-        int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
-        CK(launch_update(c, Vc.data() + g0, ng, c->d_coef + g0, 1, g0 == 0 ? nullptr : tcomb, tcomb, 0, 0,
-                         c->d_part));
-      }
-    }
-    {
-      cnpint_status st = pinv_dev(c, tcomb, nullptr, d_u, 1);
-      if (st != CNPINT_OK) return st;
+    for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
+      int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
+      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, d_u, d_u, 0, 0, c->d_part));
     }
     // true residual into the workspace slot of Ṽ_0 (b is never overwritten)
     V[0] = c->d_V;

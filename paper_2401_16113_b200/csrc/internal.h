@@ -73,6 +73,7 @@ struct cnpint_ctx {
   double2* d_twy;      // [ny+1]
   // GMRES
   double* d_V;         // [(restart_max+1)][vec]
+  double* d_Z;         // [restart_max][vec] z_j = P_α⁻¹ v_j of the current restart cycle
   double* d_part;      // [CNP_RED_BLOCKS][CNP_MAX_DOT+1]
   double* d_c1;        // [restart_max+1] raw dots (pass 1)
   double* d_c2;        // [restart_max+1] raw dots (pass 2)
