@@ -70,7 +70,9 @@ typedef enum {
  *   2D (dim = 2):          L_h = I_y ⊗ L_x + L_y ⊗ I_x + shift·I,  L_x = tridiag(xs, xd, xu)
  *                          (nx×nx Toeplitz), L_y = tridiag(ys, yd, yu) (ny×ny Toeplitz).
  *       Requires xs*xu > 0 and ys*yu > 0 (diagonal similarity to a symmetric Toeplitz matrix,
- *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two. */
+ *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two <= 1024.
+ *   1D sizes: 2 <= nx <= 4096 (Toeplitz) or 2048 (variable rows).  N: power of two, 2..65536
+ *   (time-axis FFT on thread-block clusters up to N = 16384, one column per CTA beyond). */
 typedef struct {
   int dim;
   int nx, ny;

@@ -100,7 +100,7 @@ const char* check_op(int N, const cnpint_operator* op, int* unsupported) {
       *unsupported = 1;
       return "2D requires nx+1 and ny+1 powers of two (DST-I via FFT)";
     }
-    if (op->nx + 1 > 4096 || op->ny + 1 > 4096) { *unsupported = 1; return "2D n+1 > 4096 unsupported"; }
+    if (op->nx + 1 > 1024 || op->ny + 1 > 1024) { *unsupported = 1; return "2D n+1 > 1024 unsupported"; }
     if (!(op->xs * op->xu > 0.0) || !(op->ys * op->yu > 0.0))
       return "2D requires xs*xu > 0 and ys*yu > 0 (diagonal symmetrisation)";
   }

@@ -31,145 +31,9 @@
 
 namespace cg = cooperative_groups;
 
+#include "fft_tile.cuh"
+
 namespace {
-
-extern __shared__ double2 tf_smem[];
-
-// Shared column layout: one pad slot every 8 complex entries (8 × 16 B = one bank sweep), so the
-// strided butterfly writes (stride R entries) and the per-column reads are conflict free.
-CNP_DEV int pd(int i) { return i + (i >> 3); }
-__host__ __device__ constexpr int tf_cs(int logN2) { return (1 << logN2) + ((1 << logN2) >> 3) + 1; }
-// Per-stage twiddle table sizes: stage with NS > 1 and radix R stores ω_{NS R}^{r k} at [(r−1) NS + k].
-__host__ __device__ constexpr int tf_stage_tw(int logN2, int logNs = 0) {
-  return logNs >= logN2 ? 0
-                        : ((logNs > 0 ? ((1 << (logN2 - logNs >= 3 ? 3 : logN2 - logNs)) - 1) << logNs : 0) +
-                           tf_stage_tw(logN2, logNs + (logN2 - logNs >= 3 ? 3 : logN2 - logNs)));
-}
-
-template <bool INV>
-CNP_DEV void dft4r(double2& v0, double2& v1, double2& v2, double2& v3) {
-  double2 t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = cmul_mi<INV>(csub(v1, v3));
-  v0 = cadd(t0, t2);
-  v2 = csub(t0, t2);
-  v1 = cadd(t1, t3);
-  v3 = csub(t1, t3);
-}
-
-#define TF_C8 0.70710678118654752440
-
-template <bool INV>
-CNP_DEV double2 tw8_1(double2 a) {  // a · e^{∓iπ/4}
-  return INV ? make_double2(TF_C8 * (a.x - a.y), TF_C8 * (a.x + a.y))
-             : make_double2(TF_C8 * (a.x + a.y), TF_C8 * (a.y - a.x));
-}
-template <bool INV>
-CNP_DEV double2 tw8_3(double2 a) {  // a · e^{∓3iπ/4}
-  return INV ? make_double2(-TF_C8 * (a.x + a.y), TF_C8 * (a.x - a.y))
-             : make_double2(TF_C8 * (a.y - a.x), -TF_C8 * (a.x + a.y));
-}
-
-// v[k] ← Σ_r v[r] e^{∓2πi r k / R}  (forward −, inverse +)
-template <int R, bool INV>
-CNP_DEV void dftR(double2* v) {
-  if constexpr (R == 1) {
-    return;
-  } else if constexpr (R == 2) {
-    const double2 t = v[0];
-    v[0] = cadd(t, v[1]);
-    v[1] = csub(t, v[1]);
-  } else if constexpr (R == 4) {
-    dft4r<INV>(v[0], v[1], v[2], v[3]);
-  } else {
-    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
-    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
-    dft4r<INV>(e0, e1, e2, e3);
-    dft4r<INV>(o0, o1, o2, o3);
-    o1 = tw8_1<INV>(o1);
-    o2 = cmul_mi<INV>(o2);
-    o3 = tw8_3<INV>(o3);
-    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
-    v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
-    v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
-    v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
-  }
-}
-
-// One Stockham stage over all NC complex columns of length N2 = 2^LOGN2 (all sizes compile time):
-// column c at buf[c*CS + pd(i)].  Work item (c, j), j < N2/R: reads i = j + r N2/R, twiddles by
-// ω_{Ns R}^{r (j mod Ns)} (from this stage's table, laid out [r−1][k] so a warp reads it
-// contiguously), radix-R DFT, writes i = (j − j mod Ns) R + (j mod Ns) + r Ns.  All of a thread's
-// items are read before one barrier and written after it.  SCALE (first stage only): input i is
-// multiplied by gm[i]·s (gm = this CTA's residue slice of Γ_α, s = GMRES basis scale).
-template <int LOGR, bool INV, bool SCALE, int LOGN2, int NC, int LOGNS, int NT>
-CNP_DEV void stage(double2* buf, const double2* stw, const double* gm, double s) {
-  constexpr int R = 1 << LOGR;
-  constexpr int LOGPER = LOGN2 - LOGR;
-  constexpr int PER = 1 << LOGPER;
-  constexpr int NS = 1 << LOGNS;
-  constexpr int TOTAL = NC * PER;
-  constexpr int ITER = (TOTAL + NT - 1) / NT;
-  constexpr int CS = tf_cs(LOGN2);
-  double2 v[ITER][R];
-  int colj[ITER], jj[ITER];
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int q = it * NT + (int)threadIdx.x;
-    const bool on = (TOTAL % NT == 0) || q < TOTAL;
-    const int c = q >> LOGPER;
-    const int j = q & (PER - 1);
-    jj[it] = j;
-    colj[it] = c * CS;
-    if (on) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        v[it][r] = buf[c * CS + pd(j + r * PER)];
-        if (SCALE) v[it][r] = cscale(v[it][r], gm[j + r * PER] * s);
-      }
-      if (NS > 1) {
-        const int k = j & (NS - 1);
-#pragma unroll
-        for (int r = 1; r < R; ++r) {
-          double2 w = stw[(r - 1) * NS + k];
-          if (INV) w.y = -w.y;
-          v[it][r] = cmul(v[it][r], w);
-        }
-      }
-      dftR<R, INV>(v[it]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int q = it * NT + (int)threadIdx.x;
-    const bool on = (TOTAL % NT == 0) || q < TOTAL;
-    if (on) {
-      const int j = jj[it];
-      const int k = j & (NS - 1);
-      const int base = ((j - k) << LOGR) + k;
-#pragma unroll
-      for (int r = 0; r < R; ++r) buf[colj[it] + pd(base + r * NS)] = v[it][r];
-    }
-  }
-  __syncthreads();
-}
-
-template <bool INV, bool SCALE, int LOGN2, int NC, int NT, int LOGNS = 0>
-CNP_DEV void local_fft(double2* buf, const double2* stw, const double* gm, double s) {
-  if constexpr (LOGNS < LOGN2) {
-    constexpr int REM = LOGN2 - LOGNS;
-    constexpr int LOGR = REM >= 3 ? 3 : REM;
-    stage<LOGR, INV, SCALE && LOGNS == 0, LOGN2, NC, LOGNS, NT>(buf, stw, gm, s);
-    local_fft<INV, SCALE, LOGN2, NC, NT, LOGNS + LOGR>(buf, stw + (LOGNS > 0 ? ((1 << LOGR) - 1) << LOGNS : 0), gm,
-                                                        s);
-  }
-}
-
-// e^{−2πi num/den}, exact argument reduction by sincospi (den a power of two)
-CNP_DEV double2 expi_neg(int num, int den) {
-  double sn, cs;
-  sincospi(2.0 * (double)num / (double)den, &sn, &cs);
-  return make_double2(cs, -sn);
-}
 
 // Hermitian separation of one packed pair: (Z_k, Z_{N−k}) → (X_a[k], X_b[k])
 CNP_DEV void separate(double2 zk, double2 zm, double2& xa, double2& xb) {
@@ -266,23 +130,7 @@ __global__ void __launch_bounds__(256, 2)
     w.y *= sg;
     wc[tid] = w;
   }
-  {
-    int off = 0;
-    for (int logNs = 0; logNs < LOGN2;) {
-      const int lr = LOGN2 - logNs >= 3 ? 3 : LOGN2 - logNs;
-      if (logNs > 0) {
-        const int ns = 1 << logNs, cnt = ((1 << lr) - 1) << logNs;
-        for (int q = tid; q < cnt; q += NT) {
-          const int r = q / ns + 1, k = q - (r - 1) * ns;
-          double2 w = expi_neg(r * k, ns << lr);
-          w.y *= sg;
-          stw[off + q] = w;
-        }
-        off += cnt;
-      }
-      logNs += lr;
-    }
-  }
+  fill_stage_twiddles(stw, LOGN2, sg, tid, NT);
   auto wN = [&](int j) { return cmul(wc[j & (C - 1)], twl[j / C]); };  // ω_N^j, j < N
   auto lam_s = [&](const double2* l, int k) { return k <= H ? l[k] : cconj(l[N - k]); };
   const double s = (MODE != 1 && vscale) ? *vscale : 1.0;
@@ -313,7 +161,7 @@ __global__ void __launch_bounds__(256, 2)
   __syncthreads();
 
   if (MODE == 0 || MODE == 2) {
-    local_fft<false, true, LOGN2, NC, NT>(buf, stw, gm, s);
+    local_fft<false, TF_SCALE, LOGN2, NC, NT>(buf, stw, gm, s);
     cluster_barrier<C>();
     // ---- radix-C stage across the cluster for the owned families, then separation / divide
     const int items = nfam * NC;
@@ -477,7 +325,7 @@ __global__ void __launch_bounds__(256, 2)
   }
   // ---- every T_r[k2] has arrived: local inverse FFT, then residue rows with 1/(N γ_t)
   cluster_barrier<C>();
-  local_fft<true, false, LOGN2, NC, NT>(buf, stw, gm, 1.0);
+  local_fft<true, TF_PLAIN, LOGN2, NC, NT>(buf, stw, gm, 1.0);
   for (int q = tid; q < N2 * NC; q += NT) {
     const int n = q / NC, c = q - n * NC;
     const int col = col0 + 2 * c;
