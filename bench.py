@@ -142,13 +142,14 @@ def measured_hbm_peak():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """DRAM bytes per launch from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full capture of the
+    same workload (profiles/ncu_traffic.json, written from profiles/r01_ncu_full_summary.txt)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p))
-        if kernel in d:
-            return d[kernel]
+        d = json.load(open(p)).get(kernel)
+        if d and d.get("workload") == workload:
+            return d["bytes_per_launch"]
     return None
 
 
@@ -313,7 +314,8 @@ def run_gpu(args, rank, world, local):
         "matvec": {"ms": 1e3 * mv_s, "GBps": mv_gbps, "frac": mv_gbps / peak},
         "stream_copy_GBps": copy_best,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(dominant), "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": ncu_traffic(dominant, w.name),
+                     "algo_bytes_per_launch": d_by / d_cnt, "peak_source": peak_src,
                      "share_of_step": d_ms / total_prof_ms if total_prof_ms else None,
                      "frac_of_same_run_copy": achieved / copy_best if copy_best else None},
         "kernels": kernels,

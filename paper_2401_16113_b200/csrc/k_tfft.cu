@@ -351,9 +351,10 @@ TfftCfg tfft_cfg(int N) {
   TfftCfg f;
   int logN = 0;
   while ((1 << logN) < N) ++logN;
-  // default: local FFTs of N2 = 512 rows (C = N/512 CTAs per cluster) up to N = 4096, C = 8 beyond;
-  // tiles of 16 columns (128-B row segments) while N2 <= 512, 8 at N2 = 1024, 4 at N2 = 2048.
-  f.C = N >= 8192 ? 8 : N >= 1024 ? N / 512 : 1;
+  // default (measured, profiles/r01_tfft_sweep.txt): a pair of CTAs (C = 2) for 1024 <= N <= 4096,
+  // C = 8 beyond; tiles of 16 columns (128-B row segments) while N2 <= 512, 8 at N2 = 1024, 4 at
+  // N2 = 2048.
+  f.C = N >= 8192 ? 8 : N >= 1024 ? 2 : 1;
   if (const char* e = getenv("CNPINT_TFFT_C")) {  // tuning override (experiments only)
     const int v = atoi(e);
     if ((v == 1 || v == 2 || v == 4 || v == 8) && N / v >= 2 && N / v <= 2048) f.C = v;
