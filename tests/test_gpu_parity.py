@@ -324,3 +324,33 @@ def test_zero_rhs_and_determinism():
     s.gmres(b, u1, 1e-10, 10)
     s.gmres(b, u2, 1e-10, 10)
     assert torch.equal(u1, u2)                # deterministic reductions: bitwise reproducible
+
+
+# ------------------------------------------------------------------------------ c5 sweep
+@pytest.mark.parametrize("n,N", [(127, 256), (127, 1024)])
+def test_gmres_c5_small_vs_oracle(n, N):
+    """BASELINE configs[4], the two sizes the oracle finishes: GPU vs oracle GMRES counts (±1), true
+    residual, and the final u against sequential CN (1e-8)."""
+    _gmres_case(synth.c5(n, N), check_iterates=False)
+
+
+def test_gmres_c5_mesh_independence():
+    """BASELINE configs[4]: iteration counts stay the same across n ∈ {127, 255, 511} × N ∈ {256, 1024}
+    (Theorem 4.5 in spirit; SURVEY.md Appendix A expects 4 at every size)."""
+    its = {}
+    for n, N in synth.C5_SIZES:
+        w = synth.c5(n, N)
+        s = solver_for(w, restart_max=w.restart)
+        b = problems.rhs(w, s)
+        u = s.empty()
+        rep = s.gmres(b, u, w.tol, w.restart)
+        assert rep["converged"] and rep["relres_true"] <= w.tol, (n, N, rep)
+        its[(n, N)] = rep["iterations"]
+        # the AaO solution approximates the manufactured solution (second-order scheme)
+        ue = problems.exact(w, s)
+        err = float((u - ue).abs().max() / ue.abs().max())
+        assert err < 5e-5, (n, N, err)
+        del s, b, u, ue
+        torch.cuda.empty_cache()
+    assert max(its.values()) - min(its.values()) <= 1, its
+    assert all(3 <= v <= 6 for v in its.values()), its
