@@ -83,8 +83,16 @@ CNP_DEV void dftR(double2* v) {
 //   TF_ODDEXT odd extension of a sequence held in slots 1..N2/2−1: elements 0 and N2/2 are 0 and
 //             element i > N2/2 is −element(N2 − i) (the DST-I embedding of K5).
 enum { TF_PLAIN = 0, TF_SCALE = 1, TF_ODDEXT = 2 };
+// TF_SCALE's factor for element i is the time row t = i·cstride + crank:
+//   γ_t · s = ghi[t >> 6] · glo[t & 63] · s   (two-level table of Γ_α, see k_tfft.cu).
+struct TfScale {
+  const double* ghi;
+  const double* glo;
+  int cstride, crank;
+  double s;
+};
 template <int LOGR, bool INV, int FIRST, int LOGN2, int NC, int LOGNS, int NT>
-CNP_DEV void stage(double2* buf, const double2* stw, const double* gm, double s) {
+CNP_DEV void stage(double2* buf, const double2* stw, const TfScale& sc) {
   constexpr int R = 1 << LOGR;
   constexpr int LOGPER = LOGN2 - LOGR;
   constexpr int PER = 1 << LOGPER;
@@ -114,7 +122,10 @@ CNP_DEV void stage(double2* buf, const double2* stw, const double* gm, double s)
           v[it][r] = i > HALF ? make_double2(-x.x, -x.y) : x;
         } else {
           v[it][r] = buf[c * CS + pd(i)];
-          if (FIRST == TF_SCALE) v[it][r] = cscale(v[it][r], gm[i] * s);
+          if (FIRST == TF_SCALE) {
+            const int t = i * sc.cstride + sc.crank;
+            v[it][r] = cscale(v[it][r], sc.ghi[t >> 6] * sc.glo[t & 63] * sc.s);
+          }
         }
       }
       if (NS > 1) {
@@ -146,13 +157,12 @@ CNP_DEV void stage(double2* buf, const double2* stw, const double* gm, double s)
 }
 
 template <bool INV, int FIRST, int LOGN2, int NC, int NT, int LOGNS = 0>
-CNP_DEV void local_fft(double2* buf, const double2* stw, const double* gm, double s) {
+CNP_DEV void local_fft(double2* buf, const double2* stw, const TfScale& sc) {
   if constexpr (LOGNS < LOGN2) {
     constexpr int REM = LOGN2 - LOGNS;
     constexpr int LOGR = REM >= 3 ? 3 : REM;
-    stage<LOGR, INV, LOGNS == 0 ? FIRST : TF_PLAIN, LOGN2, NC, LOGNS, NT>(buf, stw, gm, s);
-    local_fft<INV, FIRST, LOGN2, NC, NT, LOGNS + LOGR>(buf, stw + (LOGNS > 0 ? ((1 << LOGR) - 1) << LOGNS : 0), gm,
-                                                        s);
+    stage<LOGR, INV, LOGNS == 0 ? FIRST : TF_PLAIN, LOGN2, NC, LOGNS, NT>(buf, stw, sc);
+    local_fft<INV, FIRST, LOGN2, NC, NT, LOGNS + LOGR>(buf, stw + (LOGNS > 0 ? ((1 << LOGR) - 1) << LOGNS : 0), sc);
   }
 }
 

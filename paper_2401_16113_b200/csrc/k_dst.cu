@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256, 2)
       }
       __syncthreads();
     }
-    local_fft<false, TF_ODDEXT, LOGE, NC, NT>(buf, stw, nullptr, 1.0);
+    local_fft<false, TF_ODDEXT, LOGE, NC, NT>(buf, stw, TfScale{nullptr, nullptr, 1, 0, 1.0});
     // ---- F_k = −2i S(a)_k + 2 S(b)_k, k = 1..n: S(a) = −Im F/2, S(b) = Re F/2, then post-scale
     if (!YPASS) {
       const int line0 = tile * NC * 2;

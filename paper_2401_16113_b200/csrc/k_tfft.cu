@@ -61,19 +61,23 @@ CNP_DEV void cluster_barrier() {
 
 }  // namespace
 
-// Shared memory (complex entries): data[NC·CS] | twl[N2] (ω_{N2}^q) | stw[stage tables] | wc[C]
-// (ω_N^j, j < C) | gm[N2], ig[N2] (doubles: Γ_α and 1/(NΓ_α) of this CTA's residue class) |
-// l1[N/2+1], l2[N/2+1] (λ tables, MODE 2 only).  Everything but data is loaded once per CTA.
+// Shared memory (complex entries): data[NC·CS] | stw[stage tables] | whi[N/64], wlo[64] (ω_N^j =
+// whi[j >> 6]·wlo[j & 63]) | ghi, glo, ihi, ilo (doubles: Γ_α and 1/(NΓ_α) as two-level tables,
+// γ_t = ghi[t >> 6]·glo[t & 63]) | l1[N/2+1], l2[N/2+1] (λ tables, MODE 2 only).  Everything but
+// data is built once per CTA; the two-level tables keep it small (a few KB at any N).
 template <int MODE, int C, int LOGN2, int NC>
 struct TfLayout {
   static constexpr int N2 = 1 << LOGN2;
+  static constexpr int N = N2 * C;
+  static constexpr int LO = N < 64 ? N : 64;
+  static constexpr int HI = N / LO;
   static constexpr int CS = tf_cs(LOGN2);
-  static constexpr int off_twl = NC * CS;
-  static constexpr int off_stw = off_twl + N2;
-  static constexpr int off_wc = off_stw + tf_stage_tw(LOGN2);
-  static constexpr int off_gm = off_wc + C;
-  static constexpr int off_lam = off_gm + N2;
-  static constexpr int nlam = MODE == 2 ? N2 * C / 2 + 1 : 0;
+  static constexpr int off_stw = NC * CS;
+  static constexpr int off_whi = off_stw + tf_stage_tw(LOGN2);
+  static constexpr int off_wlo = off_whi + HI;
+  static constexpr int off_g = off_wlo + 64;  // doubles: ghi[HI] glo[64] ihi[HI] ilo[64] → (2HI+128)/2 slots
+  static constexpr int off_lam = off_g + HI + 64;
+  static constexpr int nlam = MODE == 2 ? N / 2 + 1 : 0;
   static constexpr size_t bytes = (size_t)(off_lam + 2 * nlam) * 16;
 };
 
@@ -98,42 +102,50 @@ __global__ void __launch_bounds__(256, 2)
   const int cl = blockIdx.x / C, ncl = gridDim.x / C;
   const int Wi = (int)W, ldi = (int)ld;
   double2* const buf = tf_smem;
-  double2* const twl = tf_smem + LY::off_twl;
   double2* const stw = tf_smem + LY::off_stw;
-  double2* const wc = tf_smem + LY::off_wc;
-  double* const gm = reinterpret_cast<double*>(tf_smem + LY::off_gm);
-  double* const ig = gm + N2;
+  double2* const whi = tf_smem + LY::off_whi;
+  double2* const wlo = tf_smem + LY::off_wlo;
+  double* const ghi = reinterpret_cast<double*>(tf_smem + LY::off_g);
+  double* const glo = ghi + LY::HI;
+  double* const ihi = glo + 64;
+  double* const ilo = ihi + LY::HI;
   double2* const l1s = tf_smem + LY::off_lam;
   double2* const l2s = l1s + LY::nlam;
   // families {k2, N2−k2} owned by this rank: k2 = rank + C·i, k2 <= N2/2
   const int nfam = rank <= N2 / 2 ? (N2 / 2 - rank) / C + 1 : 0;
 
-  // ---- per-CTA tables, once: Γ_α slices and λ by cp.async, twiddles on chip (sincospi)
-  if (MODE != 1)
-    for (int q = tid; q < N2; q += NT) cp_async8(gm + q, gam + q * C + rank);
-  if (MODE != 0)
-    for (int q = tid; q < N2; q += NT) cp_async8(ig + q, igam + q * C + rank);
+  // ---- per-CTA tables, once: Γ_α two-level tables (exact host values: γ_{64i}, γ_i; N is a power
+  //      of two so N·(1/(Nγ_i)) is exact), λ by cp.async; twiddles on chip (sincospi)
+  for (int q = tid; q < LY::HI; q += NT) {
+    cp_async8(ghi + q, gam + q * LY::LO);
+    cp_async8(ihi + q, igam + q * LY::LO);
+  }
   if (MODE == 2)
     for (int q = tid; q < LY::nlam; q += NT) {
       cp_async16(l1s + q, lam1 + q);
       cp_async16(l2s + q, lam2 + q);
     }
   cp_async_commit();
-  const double sg = debug_sign ? -1.0 : 1.0;  // sign flip = negative-control debug hook
-  for (int q = tid; q < N2; q += NT) {
-    double2 w = expi_neg(q, N2);
-    w.y *= sg;
-    twl[q] = w;
+  for (int q = tid; q < LY::LO; q += NT) {
+    glo[q] = __ldg(gam + q);
+    ilo[q] = (double)N * __ldg(igam + q);
   }
-  if (tid < C) {
-    double2 w = expi_neg(tid, N);
+  const double sg = debug_sign ? -1.0 : 1.0;  // sign flip = negative-control debug hook
+  for (int q = tid; q < LY::HI; q += NT) {
+    double2 w = expi_neg(q * LY::LO, N);
     w.y *= sg;
-    wc[tid] = w;
+    whi[q] = w;
+  }
+  for (int q = tid; q < LY::LO; q += NT) {
+    double2 w = expi_neg(q, N);
+    w.y *= sg;
+    wlo[q] = w;
   }
   fill_stage_twiddles(stw, LOGN2, sg, tid, NT);
-  auto wN = [&](int j) { return cmul(wc[j & (C - 1)], twl[j / C]); };  // ω_N^j, j < N
+  auto wN = [&](int j) { return cmul(whi[j >> 6], wlo[j & 63]); };  // ω_N^j, j < N
   auto lam_s = [&](const double2* l, int k) { return k <= H ? l[k] : cconj(l[N - k]); };
   const double s = (MODE != 1 && vscale) ? *vscale : 1.0;
+  const TfScale sc{ghi, glo, C, rank, s};
 
   // ---- persistent loop over this cluster's tiles
   for (int tile = cl; tile < ntiles; tile += ncl) {
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(256, 2)
   __syncthreads();
 
   if (MODE == 0 || MODE == 2) {
-    local_fft<false, TF_SCALE, LOGN2, NC, NT>(buf, stw, gm, s);
+    local_fft<false, TF_SCALE, LOGN2, NC, NT>(buf, stw, sc);
     cluster_barrier<C>();
     // ---- radix-C stage across the cluster for the owned families, then separation / divide
     const int items = nfam * NC;
@@ -325,13 +337,13 @@ __global__ void __launch_bounds__(256, 2)
   }
   // ---- every T_r[k2] has arrived: local inverse FFT, then residue rows with 1/(N γ_t)
   cluster_barrier<C>();
-  local_fft<true, TF_PLAIN, LOGN2, NC, NT>(buf, stw, gm, 1.0);
+  local_fft<true, TF_PLAIN, LOGN2, NC, NT>(buf, stw, sc);
   for (int q = tid; q < N2 * NC; q += NT) {
     const int n = q / NC, c = q - n * NC;
     const int col = col0 + 2 * c;
     if (col >= Wi) continue;
     const int t = n * C + rank;
-    const double g = ig[n];
+    const double g = ihi[t >> 6] * ilo[t & 63];
     const double2 z = buf[c * CS + pd(n)];
     double2 val = make_double2(padA ? 0.0 : z.x * g, padB ? 0.0 : z.y * g);
     double2* dst = reinterpret_cast<double2*>(vout + (int64_t)t * W + col);
