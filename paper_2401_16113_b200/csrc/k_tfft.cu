@@ -33,6 +33,11 @@ namespace cg = cooperative_groups;
 
 #include "fft_tile.cuh"
 
+// threads per CTA of the time-FFT kernels (two CTAs per SM)
+#ifndef TF_NT
+#define TF_NT 256
+#endif
+
 namespace {
 
 // Hermitian separation of one packed pair: (Z_k, Z_{N−k}) → (X_a[k], X_b[k])
@@ -82,7 +87,7 @@ struct TfLayout {
 };
 
 template <int MODE, int C, int LOGN2, int NC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(TF_NT, 2)
     k_tfft(const double* __restrict__ vin, const double2* __restrict__ spin, double* __restrict__ vout,
            double2* __restrict__ spout, const double* __restrict__ vscale, int64_t W,
            const double* __restrict__ gam, const double* __restrict__ igam, int accumulate,
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(256, 2)
            const double* __restrict__ ey, double tau_shift, double tau, int64_t ld, int nx, int debug_sign,
            int ntiles) {
   using LY = TfLayout<MODE, C, LOGN2, NC>;
-  constexpr int NT = 256;
+  constexpr int NT = TF_NT;
   constexpr int X = 2 * NC;
   constexpr int N2 = LY::N2;
   constexpr int N = N2 * C;
@@ -376,7 +381,7 @@ TfftCfg tfft_cfg(int N) {
   f.X = 2 * NC;
   f.CS = tf_cs(f.logN2);
   f.smem = 0;
-  f.T = 256;
+  f.T = TF_NT;
   f.ok = N >= 2 && N <= 16384 && f.logN2 >= 1 && f.logN2 <= 11;
   return f;
 }
@@ -389,7 +394,7 @@ static cudaError_t launch_c(cnpint_ctx* c, const TfftCfg& f, const double* vin, 
   auto kern = k_tfft<MODE, C, LOGN2, NC>;
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(TF_NT);
   cfg.dynamicSmemBytes = LY::bytes;
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
