@@ -19,11 +19,25 @@ CNP_DEV double2 expi_neg(int num, int den) {
 // strided butterfly writes (stride R entries) and the per-column reads are conflict free.
 CNP_DEV int pd(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int tf_cs(int logN2) { return (1 << logN2) + ((1 << logN2) >> 3) + 1; }
+// Stage plan of a length-2^L local FFT: s stages of radix 2^{⌈L/s⌉} / 2^{⌊L/s⌋} (larger radices first),
+// s = ⌈L/4⌉ from L = 10 on (radix 16 where one work item per thread keeps it in registers: 16·8·8,
+// 16·16·8) and ⌈L/3⌉ below (8·8·8, 8·8·4, ...): few shared-memory passes, no radix-2 tail.
+__host__ __device__ constexpr int tf_nst(int L) { return L >= 10 ? (L + 3) / 4 : (L + 2) / 3; }
+__host__ __device__ constexpr int tf_lr(int L, int logNs) {  // radix (log) of the stage starting at logNs
+  int acc = 0;
+  const int s = tf_nst(L), rem = L % s;
+  for (int i = 0; i < s; ++i) {
+    const int r = rem == 0 ? L / s : (i < rem ? L / s + 1 : L / s);
+    if (acc == logNs) return r;
+    acc += r;
+  }
+  return 0;
+}
 // Per-stage twiddle table sizes: stage with NS > 1 and radix R stores ω_{NS R}^{r k} at [(r−1) NS + k].
 __host__ __device__ constexpr int tf_stage_tw(int logN2, int logNs = 0) {
   return logNs >= logN2 ? 0
-                        : ((logNs > 0 ? ((1 << (logN2 - logNs >= 3 ? 3 : logN2 - logNs)) - 1) << logNs : 0) +
-                           tf_stage_tw(logN2, logNs + (logN2 - logNs >= 3 ? 3 : logN2 - logNs)));
+                        : ((logNs > 0 ? ((1 << tf_lr(logN2, logNs)) - 1) << logNs : 0) +
+                           tf_stage_tw(logN2, logNs + tf_lr(logN2, logNs)));
 }
 
 template <bool INV>
@@ -48,6 +62,16 @@ CNP_DEV double2 tw8_3(double2 a) {  // a · e^{∓3iπ/4}
              : make_double2(TF_C8 * (a.y - a.x), -TF_C8 * (a.x + a.y));
 }
 
+// a · e^{∓2πi E/16} for odd E (forward −, inverse +)
+template <int E, bool INV>
+CNP_DEV double2 tw16s(double2 a) {
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+  constexpr double c = (E == 1 || E == 15) ? C1 : (E == 3 || E == 13) ? S1 : (E == 5 || E == 11) ? -S1 : -C1;
+  constexpr double sn = (E == 1 || E == 7) ? S1 : (E == 3 || E == 5) ? C1 : (E == 9 || E == 15) ? -S1 : -C1;
+  const double s = INV ? sn : -sn;  // e^{∓iθ} = cos θ ∓ i sin θ
+  return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+}
+
 // v[k] ← Σ_r v[r] e^{∓2πi r k / R}  (forward −, inverse +)
 template <int R, bool INV>
 CNP_DEV void dftR(double2* v) {
@@ -59,6 +83,23 @@ CNP_DEV void dftR(double2* v) {
     v[1] = csub(t, v[1]);
   } else if constexpr (R == 4) {
     dft4r<INV>(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 16) {
+    // four-step 4×4: A[r2][k1] = dft4_{r1}(v[4 r1 + r2]); A *= w16^{r2 k1}; out[k1 + 4 k2] = dft4_{r2}
+    double2 a[4][4];
+#pragma unroll
+    for (int r2 = 0; r2 < 4; ++r2) {
+      a[r2][0] = v[r2]; a[r2][1] = v[r2 + 4]; a[r2][2] = v[r2 + 8]; a[r2][3] = v[r2 + 12];
+      dft4r<INV>(a[r2][0], a[r2][1], a[r2][2], a[r2][3]);
+    }
+    a[1][1] = tw16s<1, INV>(a[1][1]); a[1][2] = tw8_1<INV>(a[1][2]); a[1][3] = tw16s<3, INV>(a[1][3]);
+    a[2][1] = tw8_1<INV>(a[2][1]); a[2][2] = cmul_mi<INV>(a[2][2]); a[2][3] = tw8_3<INV>(a[2][3]);
+    a[3][1] = tw16s<3, INV>(a[3][1]); a[3][2] = tw8_3<INV>(a[3][2]); a[3][3] = tw16s<9, INV>(a[3][3]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 b0 = a[0][k1], b1 = a[1][k1], b2 = a[2][k1], b3 = a[3][k1];
+      dft4r<INV>(b0, b1, b2, b3);
+      v[k1] = b0; v[k1 + 4] = b1; v[k1 + 8] = b2; v[k1 + 12] = b3;
+    }
   } else {
     double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
     double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
@@ -159,8 +200,7 @@ CNP_DEV void stage(double2* buf, const double2* stw, const TfScale& sc) {
 template <bool INV, int FIRST, int LOGN2, int NC, int NT, int LOGNS = 0>
 CNP_DEV void local_fft(double2* buf, const double2* stw, const TfScale& sc) {
   if constexpr (LOGNS < LOGN2) {
-    constexpr int REM = LOGN2 - LOGNS;
-    constexpr int LOGR = REM >= 3 ? 3 : REM;
+    constexpr int LOGR = tf_lr(LOGN2, LOGNS);
     stage<LOGR, INV, LOGNS == 0 ? FIRST : TF_PLAIN, LOGN2, NC, LOGNS, NT>(buf, stw, sc);
     local_fft<INV, FIRST, LOGN2, NC, NT, LOGNS + LOGR>(buf, stw + (LOGNS > 0 ? ((1 << LOGR) - 1) << LOGNS : 0), sc);
   }
@@ -170,7 +210,7 @@ CNP_DEV void local_fft(double2* buf, const double2* stw, const TfScale& sc) {
 CNP_DEV void fill_stage_twiddles(double2* stw, int logN2, double sg, int tid, int nt) {
   int off = 0;
   for (int logNs = 0; logNs < logN2;) {
-    const int lr = logN2 - logNs >= 3 ? 3 : logN2 - logNs;
+    const int lr = tf_lr(logN2, logNs);
     if (logNs > 0) {
       const int ns = 1 << logNs, cnt = ((1 << lr) - 1) << logNs;
       for (int q = tid; q < cnt; q += nt) {
