@@ -36,7 +36,9 @@ __global__ void flatcopy(const double2* in, double2* out, size_t n) {
     __stcs(out + i, __ldcs(in + i));
 }
 
+int main2();
 int main() {
+  main2();
   const long W = 4096, N = 4096;  // c2: 16.8 M doubles = 134 MB
   const size_t n = (size_t)W * N;
   double *a, *b;
@@ -72,5 +74,55 @@ int main() {
       printf("tile X=%3d R=%5d smem=%6zu KB: %.1f GB/s %s\n", X, R, smem / 1024,
              2.0 * n * 8 * 5 / (ms * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
     }
+  return 0;
+}
+
+// ---- K2 load-phase mimic: persistent CTAs, each "tile" = NC column pairs × R rows with row stride
+// RS (rows t = n·RS + rank), cp.async into padded columns, barrier; nothing computed or stored.
+__global__ void loadonly(const double* in, long W, int ntiles, int R, int RS, int NC, int CSs) {
+  const int rank = blockIdx.x % RS;
+  const int cl = blockIdx.x / RS, ncl = gridDim.x / RS;
+  for (int tile = cl; tile < ntiles; tile += ncl) {
+    const long col0 = (long)tile * 2 * NC;
+    for (int q = threadIdx.x; q < R * NC; q += blockDim.x) {
+      const int n = q / NC, c = q - n * NC;
+      cp16(sm + c * CSs + n + (n >> 3), in + (long)(n * RS + rank) * W + col0 + 2 * c);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
+}
+
+int main2() {
+  const long W = 4096, N = 4096;
+  const size_t n = (size_t)W * N;
+  double* a;
+  cudaMalloc(&a, n * 8);
+  cudaMemset(a, 0, n * 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms;
+  cudaFuncSetAttribute(loadonly, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  struct Cfg { int NC, RS, per_sm; };
+  Cfg cfgs[] = {{2, 2, 2}, {2, 2, 3}, {2, 1, 2}, {4, 2, 2}, {8, 8, 2}, {8, 8, 3}, {2, 2, 1}};
+  for (Cfg g : cfgs) {
+    const int R = (int)N / g.RS;
+    const int CSs = R + R / 8 + 1;
+    const size_t smem = (size_t)g.NC * CSs * 16;
+    const int ntiles = (int)(W / (2 * g.NC));
+    int grid = 148 * g.per_sm;
+    grid -= grid % g.RS;
+    for (int rep = 0; rep < 2; ++rep) loadonly<<<grid, 256, smem>>>(a, W, ntiles, R, g.RS, g.NC, CSs);
+    cudaEventRecord(e0);
+    for (int rep = 0; rep < 5; ++rep) loadonly<<<grid, 256, smem>>>(a, W, ntiles, R, g.RS, g.NC, CSs);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    printf("loadonly NC=%d rowstride=%d per_sm=%d smem=%zu KB: %.1f us, read %.1f GB/s %s\n", g.NC, g.RS, g.per_sm,
+           smem / 1024, ms * 1e3 / 5, n * 8.0 * 5 / (ms * 1e-3) / 1e9, err == cudaSuccess ? "" : cudaGetErrorString(err));
+  }
   return 0;
 }
