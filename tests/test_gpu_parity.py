@@ -38,6 +38,14 @@ SMALL = {
     "2d_small": synth.scaled(synth.C4, 15, 16, alpha=0.1),
     "2d_mid": synth.scaled(synth.C4, 31, 64, alpha=0.01),
     "c1": synth.C1,
+    # time-FFT cluster configurations (k_tfft.cu tfft_cfg): C = 1 (N <= 512), 2 (N2 = 512..2048), 8 (N >= 8192)
+    "1d_N1024_C2": synth.scaled(synth.C1, 21, 1024, alpha=0.01),
+    "1d_N2048_C2": synth.scaled(synth.C1, 13, 2048, alpha=0.02),
+    "1d_N4096_C2": synth.scaled(synth.C1, 65, 4096, alpha=0.01),
+    "1d_N8192_C8": synth.scaled(synth.C3, 37, 8192, alpha=0.01, T=5.0),
+    "1d_N16384_C8": synth.scaled(synth.C3, 9, 16384, alpha=0.1, T=5.0),
+    "2d_N1024_C2": synth.scaled(synth.C4, 15, 1024, alpha=0.01),
+    "2d_n63_N2048": synth.scaled(synth.C4, 63, 2048, alpha=0.01),
 }
 
 
@@ -115,7 +123,8 @@ def test_pinv_c1_all_16_vectors():
         assert rel(aao.apply_P(w, op, zg), v) < 1e-12
 
 
-@pytest.mark.parametrize("name", ["1d_small", "1d_price", "1d_ragged", "c1"])
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "1d_ragged", "c1", "1d_N1024_C2", "1d_N2048_C2",
+                                  "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8"])
 def test_stage_kernels(name):
     """K2, K3, K4 separately against the oracle's steps (a), (b), (c) (unnormalised DFT)."""
     w = SMALL[name]
@@ -135,10 +144,14 @@ def test_stage_kernels(name):
     s.shifted_solve(what, zhat)
     zh = torch.view_as_complex(zhat).cpu().numpy()[:, : w.n]
     assert rel(zh, zhat_o) < 1e-12
+    # K4 on the oracle's ẑ (so that K3's own rounding does not enter the K4 comparison)
     full = np.concatenate([zhat_o, np.conj(zhat_o[1:N - K + 1][::-1])])
     z_o = (np.fft.ifft(full, axis=0).real / g[:, None])
+    zin = s.empty_spec()
+    zin[:, : w.n, 0] = torch.from_numpy(np.ascontiguousarray(zhat_o.real)).to(zin.device)
+    zin[:, : w.n, 1] = torch.from_numpy(np.ascontiguousarray(zhat_o.imag)).to(zin.device)
     z = s.empty()
-    s.time_ifft(zhat, z)
+    s.time_ifft(zin, z)
     assert rel(s.to_host(z), z_o) < 1e-13
 
 
