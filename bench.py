@@ -272,7 +272,7 @@ def run_gpu(args, rank, world, local):
     # ---------------- end to end through the host-buffer C-ABI call (pinned host memory)
     bh = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
     bh.copy_(b[..., : w.m].cpu())
-    uh = torch.empty_like(bh)
+    uh = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
     bnp, unp = bh.numpy(), uh.numpy()
     s.gmres_host(bnp, w.tol, w.restart, u=unp)
     torch.cuda.synchronize()

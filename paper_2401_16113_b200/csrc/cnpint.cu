@@ -728,23 +728,28 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
 }
 
 // ------------------------------------------------------------------------------ host variants
-static cnpint_status h2d_vec(cnpint_ctx* c, const double* h, double* d) {
-  CK(cudaMemcpy2DAsync(d, c->ld * sizeof(double), h, c->nx * sizeof(double), c->nx * sizeof(double),
-                       (size_t)c->N * c->ny, cudaMemcpyHostToDevice, c->stream));
+// Host ↔ device: one contiguous copy of the packed host array into / out of a device staging vector,
+// and an on-device repack to / from the padded layout (a pitched 2D DMA copy of short rows is much
+// slower over PCIe than one linear transfer).
+static cnpint_status h2d_vec(cnpint_ctx* c, const double* h, double* d, double* stage) {
+  const size_t rows = (size_t)c->N * c->ny;
+  CK(cudaMemcpyAsync(stage, h, rows * c->nx * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(launch_repack(c, stage, d, 0));
   return CNPINT_OK;
 }
-static cnpint_status d2h_vec(cnpint_ctx* c, const double* d, double* h) {
-  CK(cudaMemcpy2DAsync(h, c->nx * sizeof(double), d, c->ld * sizeof(double), c->nx * sizeof(double),
-                       (size_t)c->N * c->ny, cudaMemcpyDeviceToHost, c->stream));
+static cnpint_status d2h_vec(cnpint_ctx* c, const double* d, double* h, double* stage) {
+  const size_t rows = (size_t)c->N * c->ny;
+  CK(launch_repack(c, d, stage, 1));
+  CK(cudaMemcpyAsync(h, stage, rows * c->nx * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   return CNPINT_OK;
 }
 
 cnpint_status cnpint_apply_Pinv_host(cnpint_ctx* c, const double* h_v, double* h_z) {
   if (!c || !h_v || !h_z) return CNPINT_EINVAL;
   cnpint_status st;
-  if ((st = h2d_vec(c, h_v, c->d_io1))) return st;
+  if ((st = h2d_vec(c, h_v, c->d_io1, c->d_io3))) return st;
   if ((st = pinv_dev(c, c->d_io1, nullptr, c->d_io2, 0))) return st;
-  if ((st = d2h_vec(c, c->d_io2, h_z))) return st;
+  if ((st = d2h_vec(c, c->d_io2, h_z, c->d_io3))) return st;
   CK(cudaStreamSynchronize(c->stream));
   return CNPINT_OK;
 }
@@ -752,9 +757,9 @@ cnpint_status cnpint_apply_Pinv_host(cnpint_ctx* c, const double* h_v, double* h
 cnpint_status cnpint_apply_A_host(cnpint_ctx* c, const double* h_u, double* h_y) {
   if (!c || !h_u || !h_y) return CNPINT_EINVAL;
   cnpint_status st;
-  if ((st = h2d_vec(c, h_u, c->d_io1))) return st;
+  if ((st = h2d_vec(c, h_u, c->d_io1, c->d_io3))) return st;
   CK(launch_matvec(c, c->d_io1, c->d_io2, 0, nullptr, nullptr));
-  if ((st = d2h_vec(c, c->d_io2, h_y))) return st;
+  if ((st = d2h_vec(c, c->d_io2, h_y, c->d_io3))) return st;
   CK(cudaStreamSynchronize(c->stream));
   return CNPINT_OK;
 }
@@ -765,11 +770,11 @@ cnpint_status cnpint_gmres_host(cnpint_ctx* c, const double* h_b, double* h_u, d
   // GMRES uses tmp1/tmp2 (1D) or tmp1-3 + io1 (2D) internally; b and u live in io2 / io3.
   double* db = c->d_io2;
   double* du = c->d_io3;
-  cnpint_status st = h2d_vec(c, h_b, db);
+  cnpint_status st = h2d_vec(c, h_b, db, c->d_io1);
   if (st) return st;
   st = cnpint_gmres(c, db, du, tol, restart, maxit, rep);
   if (st != CNPINT_OK && st != CNPINT_ENOCONV) return st;
-  cnpint_status st2 = d2h_vec(c, du, h_u);
+  cnpint_status st2 = d2h_vec(c, du, h_u, c->d_io1);
   if (st2) return st2;
   CK(cudaStreamSynchronize(c->stream));
   return st;

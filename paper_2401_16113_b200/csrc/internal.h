@@ -96,6 +96,9 @@ struct cnpint_ctx {
 // ------------------------------------------------------------------ kernel launchers (return cudaError_t)
 cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStream_t s);
 
+// host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed
+cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
+
 // y = 𝓜u (mode 0), y = P_α u (mode 1), y = b − 𝓜u (mode 2, b given); optional Σ y² partials
 cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part);
 

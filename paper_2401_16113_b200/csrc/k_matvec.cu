@@ -37,6 +37,26 @@ cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStr
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- host-layout repack (host API)
+// dir 0: packed [rows][nx] → padded [rows][ld] (padding written as 0); dir 1: padded → packed.
+__global__ void __launch_bounds__(256) k_repack(const double* __restrict__ src, double* __restrict__ dst, size_t rows,
+                                                int nx, int64_t ld, int dir) {
+  for (size_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    if (dir == 0) {
+      for (int x = threadIdx.x; x < ld; x += blockDim.x) dst[r * ld + x] = x < nx ? src[r * nx + x] : 0.0;
+    } else {
+      for (int x = threadIdx.x; x < nx; x += blockDim.x) dst[r * nx + x] = src[r * ld + x];
+    }
+  }
+}
+
+cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir) {
+  const size_t rows = (size_t)c->N * c->ny;
+  const unsigned grid = (unsigned)(rows < 65535 * 4 ? rows : 65535 * 4);
+  k_repack<<<grid, 256, 0, c->stream>>>(src, dst, rows, c->nx, c->ld, dir);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------ block-level sum helper
 template <int NT>
 CNP_DEV void block_partial(double v, double* part) {
