@@ -438,6 +438,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_part = (double*)(w + L.part);
   c->d_scal = (double*)(w + L.scal);
   c->d_status = (int*)(w + L.status);
+  c->d_counter = (unsigned*)(w + L.status + 32);
   // tables: build a host image of the table region [0, tables_end), upload, zero the rest
   cnpint_status st = CNPINT_OK;
   {
@@ -622,14 +623,12 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   int its = 0, cycles = 0, converged = 0;
   double est = 1.0, relres_true = 1.0;
   cnpint_status result = CNPINT_OK;
-  const int mvblocks = matvec_partial_blocks(c);
   CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
   CK(cudaMemsetAsync(c->d_scal, 0, 16 * sizeof(double), c->stream));
   // ||b||: first basis vector is b itself (x0 = 0 ⇒ r0 = b)
   double* b_nc = const_cast<double*>(d_b);
   V[0] = b_nc;
-  CK(launch_dots(c, &V[0], 1, d_b, c->d_part));
-  CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
+  CK(launch_dots(c, &V[0], 1, d_b, c->d_part, c->d_scal + 2));
   CK(launch_small(c, 0, 0, 1));
   CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -652,20 +651,16 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
       const int nv = j + 1;
       if (nv <= CNP_MAX_DOT) {
-        CK(launch_dots(c, V.data(), nv, w, c->d_part));
-        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, nv, c->d_c1));
-        CK(launch_update(c, V.data(), nv, c->d_c1, 0, w, w, 1, 0, c->d_part));
-        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, nv, c->d_c2));
-        CK(launch_update(c, V.data(), nv, c->d_c2, 0, w, w, 0, 1, c->d_part));
-        CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
+        CK(launch_dots(c, V.data(), nv, w, c->d_part, c->d_c1));
+        CK(launch_update(c, V.data(), nv, c->d_c1, 0, w, w, 1, 0, c->d_part, c->d_c2));
+        CK(launch_update(c, V.data(), nv, c->d_c2, 0, w, w, 0, 1, c->d_part, c->d_scal + 2));
       } else {
         // groups of CNP_MAX_DOT: dots, update (no fusion), dots, update, norm
         for (int pass = 0; pass < 2; ++pass) {
           double* cd = pass == 0 ? c->d_c1 : c->d_c2;
           for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
             int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
-            CK(launch_dots(c, V.data() + g0, ng, w, c->d_part));
-            CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, ng, cd + g0));
+            CK(launch_dots(c, V.data() + g0, ng, w, c->d_part, cd + g0));
           }
           for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
             int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
@@ -673,10 +668,10 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
             double* saved = c->d_scl;
             c->d_scl = saved + g0;
             const bool last = pass == 1 && g0 + ng == nv;
-            cudaError_t e = launch_update(c, V.data() + g0, ng, cd + g0, 0, w, w, 0, last ? 1 : 0, c->d_part);
+            cudaError_t e = launch_update(c, V.data() + g0, ng, cd + g0, 0, w, w, 0, last ? 1 : 0, c->d_part,
+                                          last ? c->d_scal + 2 : nullptr);
             c->d_scl = saved;
             CK(e);
-            if (last) CK(launch_reduce_n(c, c->d_part, CNP_RED_BLOCKS, CNP_MAX_DOT + 1, 1, c->d_scal + 2));
           }
         }
       }
@@ -697,12 +692,11 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     CK(launch_small(c, 2, jdone, 0));
     for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
       int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
-      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, d_u, d_u, 0, 0, c->d_part));
+      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, d_u, d_u, 0, 0, c->d_part, nullptr));
     }
     // true residual into the workspace slot of Ṽ_0 (b is never overwritten)
     V[0] = c->d_V;
-    CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part));
-    CK(launch_reduce_n(c, c->d_part, mvblocks, 1, 1, c->d_scal + 2));
+    CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part, c->d_scal + 2));
     CK(launch_small(c, 0, 0, 0));
     CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

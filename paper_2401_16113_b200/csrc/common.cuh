@@ -40,6 +40,51 @@ CNP_DEV double warp_sum(double v) {
   return v;
 }
 
+// Deterministic grid-level fold.  Every block has written its partial sums part[b*stride + col]
+// (col < ncols); the last block to arrive (atomic ticket) adds them up in block order — lane l sums
+// b = l, l+32, ... in order, then a fixed shuffle tree — and writes out[col], so the result does not
+// depend on which block finishes last (bitwise reproducible).  Partials are read with ld.global.cg
+// (L2) since other blocks wrote them.  The counter is reset for the next launch.
+CNP_DEV void grid_fold(const double* part, int nparts, int stride, int ncols, double* out, unsigned* counter) {
+  __shared__ bool amlast;
+  __shared__ double red[32][10];
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) amlast = atomicAdd(counter, 1u) == (unsigned)(nparts - 1);
+  __syncthreads();
+  if (!amlast) return;
+  __threadfence();
+  // every thread sums a fixed strided subset of the partials for all columns (independent L2 loads),
+  // then warp trees and a fixed-order sum over warps
+  const int nthr = blockDim.x * blockDim.y, lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  double acc[10];
+#pragma unroll
+  for (int col = 0; col < 10; ++col) acc[col] = 0.0;
+  for (int b = tid; b < nparts; b += nthr) {
+    const double* pb = part + (size_t)b * stride;
+#pragma unroll
+    for (int col = 0; col < 10; ++col)
+      if (col < ncols) acc[col] += __ldcg(pb + col);
+  }
+#pragma unroll
+  for (int col = 0; col < 10; ++col) {
+    if (col < ncols) {
+      double v = acc[col];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp][col] = v;
+    }
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += red[w][tid];
+    out[tid] = v;
+  }
+  if (tid == 0) *counter = 0u;
+}
+
 // Padded shared-memory index for complex FFT buffers: one pad entry every 16 elements breaks the
 // power-of-two strides of the Stockham stages into bank-conflict-free patterns.
 CNP_DEV int padi(int i) { return i + (i >> 4); }

@@ -86,6 +86,7 @@ struct cnpint_ctx {
   double* d_coef;      // [restart_max+1] combination coefficients
   double* d_scal;      // [8] misc scalars: 0 = ||b||, 1 = est, 2 = beta^2, 3 = nonfinite flag
   int* d_status;       // device status word (bit 0: singular pivot)
+  unsigned* d_counter; // grid_fold ticket counter (zero between launches)
   double* h_pinned;    // pinned host scalars [8]
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
@@ -100,7 +101,8 @@ cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStr
 cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
 
 // y = 𝓜u (mode 0), y = P_α u (mode 1), y = b − 𝓜u (mode 2, b given); optional Σ y² partials
-cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part);
+cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part,
+                          double* out = nullptr);
 
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat);
@@ -122,10 +124,11 @@ cudaError_t launch_dst_y(cnpint_ctx* c, const double* in, double* out, int inver
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 
 // GMRES helpers
-cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w, double* part);
+// partial sums into part; if out != nullptr the last block folds them (deterministically) into out
+cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w, double* part, double* out);
 cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int accumulate_sq);
 cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,
-                          double* w, double* wout, int want_dots, int want_norm, double* part);
+                          double* w, double* wout, int want_dots, int want_norm, double* part, double* out);
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg);
 
 // profiler hooks (cnpint.cu); no-ops unless cnpint_profile_enable(ctx, 1)

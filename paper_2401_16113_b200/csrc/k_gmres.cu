@@ -37,7 +37,8 @@ CNP_DEV void block_reduce_write(double (&acc)[NV], double* part, int stride) {
 // partial dots: part[b][i] = Σ Ṽ_i·w over block b's elements (grid-stride over double2)
 template <int NV>
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double* __restrict__ w, size_t n2,
-                                                           double* __restrict__ part, int stride) {
+                                                           double* __restrict__ part, int stride,
+                                                           double* __restrict__ out, unsigned* counter) {
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
@@ -51,6 +52,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double*
     }
   }
   block_reduce_write<NV>(acc, part, stride);
+  if (out) grid_fold(part, gridDim.x, stride, NV, out, counter);
 }
 
 // w_out = w − Σ_i coef_i Ṽ_i with coef_i = cd[i]·s_i² (MODE 0) or coef_i = cd[i] (MODE 1, combine,
@@ -59,7 +61,7 @@ template <int NV, int MODE, bool DOTS, bool NORM>
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const double* __restrict__ cd,
                                                              const double* __restrict__ scl, const double* w,
                                                              double* wout, size_t n2, double* __restrict__ part,
-                                                             int stride) {
+                                                             int stride, double* __restrict__ out, unsigned* counter) {
   double coef[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? cd[i] * scl[i] * scl[i] : cd[i];
@@ -85,8 +87,13 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
     }
     if constexpr (NORM) acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
   }
-  if constexpr (DOTS) block_reduce_write<NV>(acc, part, stride);
-  else if constexpr (NORM) block_reduce_write<1>(acc, part, stride);
+  if constexpr (DOTS) {
+    block_reduce_write<NV>(acc, part, stride);
+    if (out) grid_fold(part, gridDim.x, stride, NV, out, counter);
+  } else if constexpr (NORM) {
+    block_reduce_write<1>(acc, part, stride);
+    if (out) grid_fold(part, gridDim.x, stride, 1, out, counter);
+  }
 }
 
 // out[i] (+)= Σ_b part[b*stride + i], one block per column, fixed order
@@ -163,23 +170,24 @@ __global__ void k_backsolve(int k, int ldh, const double* H, const double* g, co
 static size_t n2_of(const cnpint_ctx* c) { return (size_t)c->vec / 2; }
 
 template <int NV>
-static void dots_nv(cnpint_ctx* c, const VPtrs& V, const double* w, double* part) {
-  k_dots<NV><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, w, n2_of(c), part, CNP_MAX_DOT + 1);
+static void dots_nv(cnpint_ctx* c, const VPtrs& V, const double* w, double* part, double* out) {
+  k_dots<NV><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, w, n2_of(c), part, CNP_MAX_DOT + 1, out,
+                                                                c->d_counter);
 }
 
-cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* w, double* part) {
+cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* w, double* part, double* out) {
   VPtrs V;
   for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
   cnp_prof_begin(c, KID_DOTS);
   switch (nv) {
-    case 1: dots_nv<1>(c, V, w, part); break;
-    case 2: dots_nv<2>(c, V, w, part); break;
-    case 3: dots_nv<3>(c, V, w, part); break;
-    case 4: dots_nv<4>(c, V, w, part); break;
-    case 5: dots_nv<5>(c, V, w, part); break;
-    case 6: dots_nv<6>(c, V, w, part); break;
-    case 7: dots_nv<7>(c, V, w, part); break;
-    case 8: dots_nv<8>(c, V, w, part); break;
+    case 1: dots_nv<1>(c, V, w, part, out); break;
+    case 2: dots_nv<2>(c, V, w, part, out); break;
+    case 3: dots_nv<3>(c, V, w, part, out); break;
+    case 4: dots_nv<4>(c, V, w, part, out); break;
+    case 5: dots_nv<5>(c, V, w, part, out); break;
+    case 6: dots_nv<6>(c, V, w, part, out); break;
+    case 7: dots_nv<7>(c, V, w, part, out); break;
+    case 8: dots_nv<8>(c, V, w, part, out); break;
     default: return cudaErrorInvalidValue;
   }
   cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c) * (nv + 1));
@@ -198,35 +206,36 @@ cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* 
 }
 
 template <int NV, int MODE, bool DOTS, bool NORM>
-static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w, double* wout, double* part) {
-  k_update<NV, MODE, DOTS, NORM><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, cd, c->d_scl, w, wout,
-                                                                                   n2_of(c), part, CNP_MAX_DOT + 1);
+static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w, double* wout, double* part,
+                double* out) {
+  k_update<NV, MODE, DOTS, NORM><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
+      V, cd, c->d_scl, w, wout, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
 }
 
 template <int NV>
 static void upd_sel(cnpint_ctx* c, const VPtrs& V, const double* cd, int mode, const double* w, double* wout,
-                    int dots, int norm, double* part) {
-  if (mode == 1) upd<NV, 1, false, false>(c, V, cd, w, wout, part);
-  else if (dots) upd<NV, 0, true, false>(c, V, cd, w, wout, part);
-  else if (norm) upd<NV, 0, false, true>(c, V, cd, w, wout, part);
-  else upd<NV, 0, false, false>(c, V, cd, w, wout, part);
+                    int dots, int norm, double* part, double* out) {
+  if (mode == 1) upd<NV, 1, false, false>(c, V, cd, w, wout, part, nullptr);
+  else if (dots) upd<NV, 0, true, false>(c, V, cd, w, wout, part, out);
+  else if (norm) upd<NV, 0, false, true>(c, V, cd, w, wout, part, out);
+  else upd<NV, 0, false, false>(c, V, cd, w, wout, part, nullptr);
 }
 
 // coefmode 0: w_out = w − Σ cd_i s_i² Ṽ_i.  coefmode 1: w_out = w + Σ cd_i Ṽ_i (w may be null).
 cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double* cd, int coefmode, double* w,
-                          double* wout, int want_dots, int want_norm, double* part) {
+                          double* wout, int want_dots, int want_norm, double* part, double* out) {
   VPtrs V;
   for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
   cnp_prof_begin(c, KID_UPDATE);
   switch (nv) {
-    case 1: upd_sel<1>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 2: upd_sel<2>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 3: upd_sel<3>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 4: upd_sel<4>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 5: upd_sel<5>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 6: upd_sel<6>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 7: upd_sel<7>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
-    case 8: upd_sel<8>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part); break;
+    case 1: upd_sel<1>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 2: upd_sel<2>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 3: upd_sel<3>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 4: upd_sel<4>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 5: upd_sel<5>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 6: upd_sel<6>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 7: upd_sel<7>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
+    case 8: upd_sel<8>(c, V, cd, coefmode, w, wout, want_dots, want_norm, part, out); break;
     default: return cudaErrorInvalidValue;
   }
   cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (w ? 2 : 1)));

@@ -59,7 +59,7 @@ cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir
 
 // ------------------------------------------------------------------------ block-level sum helper
 template <int NT>
-CNP_DEV void block_partial(double v, double* part) {
+CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsigned* counter = nullptr) {
   __shared__ double red[NT / 32];
   v = warp_sum(v);
   int w = threadIdx.x / 32 + threadIdx.y * (blockDim.x / 32);
@@ -70,6 +70,7 @@ CNP_DEV void block_partial(double v, double* part) {
     for (int i = 0; i < NT / 32; ++i) s += red[i];
     part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (size_t)blockIdx.z)] = s;
   }
+  if (out) grid_fold(part, gridDim.x * gridDim.y * gridDim.z, 1, 1, out, counter);
 }
 
 // ------------------------------------------------------------------------------- K1 1D
@@ -79,7 +80,8 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   const double* __restrict__ b, const double* __restrict__ lo,
                                                   const double* __restrict__ di, const double* __restrict__ up,
                                                   int N, int64_t ld, double htau, double alpha, int tchunk,
-                                                  double* __restrict__ part) {
+                                                  double* __restrict__ part, double* __restrict__ out,
+                                                  unsigned* counter) {
   const int lane = threadIdx.x & 31;
   const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
   const bool active = 2 * gx < ld;
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
     if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     pv = cv; pl = cl; pr = cr;
   }
-  if (NORM) block_partial<128>(acc, part);
+  if (NORM) block_partial<128>(acc, part, out, counter);
 }
 
 // ------------------------------------------------------------------------------- K1 2D
@@ -146,7 +148,8 @@ template <int MODE, bool NORM>
 __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
                                                   double htau, double alpha, double cxs, double cxu, double cys,
-                                                  double cyu, double cdiag, int tchunk, double* __restrict__ part) {
+                                                  double cyu, double cdiag, int tchunk, double* __restrict__ part,
+                                                  double* __restrict__ out, unsigned* counter) {
   __shared__ double2 S[2][10][32];
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
@@ -216,12 +219,13 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
     pv = cv; ph = ch; pl = cl; pr = cr;
     buf ^= 1;
   }
-  if (NORM) block_partial<256>(acc, part);
+  if (NORM) block_partial<256>(acc, part, out, counter);
 }
 
 // ----------------------------------------------------------------------------------- launcher
 template <int MODE, bool NORM>
-static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part) {
+static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part,
+                              double* out) {
   const double htau = 0.5 * c->tau;
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
@@ -229,14 +233,14 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec1d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau,
-                                                         c->alpha, tchunk, part);
+                                                         c->alpha, tchunk, part, out, c->d_counter);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec2d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
                                                          c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
-                                                         part);
+                                                         part, out, c->d_counter);
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));
   return cudaGetLastError();
@@ -250,11 +254,12 @@ int matvec_partial_blocks(const cnpint_ctx* c) {
   return (int)(((c->ld + 63) / 64) * ((c->ny + 7) / 8) * ((c->N + 15) / 16));
 }
 
-cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part) {
+cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part,
+                          double* out) {
   switch (mode) {
-    case 0: return run_matvec<0, false>(c, u, y, nullptr, nullptr);
-    case 1: return run_matvec<1, false>(c, u, y, nullptr, nullptr);
-    case 2: return part ? run_matvec<2, true>(c, u, y, b, part) : run_matvec<2, false>(c, u, y, b, nullptr);
+    case 0: return run_matvec<0, false>(c, u, y, nullptr, nullptr, nullptr);
+    case 1: return run_matvec<1, false>(c, u, y, nullptr, nullptr, nullptr);
+    case 2: return part ? run_matvec<2, true>(c, u, y, b, part, out) : run_matvec<2, false>(c, u, y, b, nullptr, nullptr);
     default: return cudaErrorInvalidValue;
   }
 }
