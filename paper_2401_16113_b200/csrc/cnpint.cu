@@ -623,16 +623,18 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   int its = 0, cycles = 0, converged = 0;
   double est = 1.0, relres_true = 1.0;
   cnpint_status result = CNPINT_OK;
-  CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
+  // u needs no zero fill: the first cycle end writes u = Σ y_j z_j (b = 0 is handled below)
   CK(cudaMemsetAsync(c->d_scal, 0, 16 * sizeof(double), c->stream));
   // ||b||: first basis vector is b itself (x0 = 0 ⇒ r0 = b)
   double* b_nc = const_cast<double*>(d_b);
   V[0] = b_nc;
-  CK(launch_dots(c, &V[0], 1, d_b, c->d_part, c->d_scal + 2));
+  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));
   CK(launch_small(c, 0, 0, 1));
   CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
+    CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     if (rep) { rep->iterations = 0; rep->restarts = 0; rep->converged = 1; rep->relres_est = 0; rep->relres_true = 0; }
     return CNPINT_OK;
   }
@@ -692,17 +694,24 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     CK(launch_small(c, 2, jdone, 0));
     for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
       int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
-      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, d_u, d_u, 0, 0, c->d_part, nullptr));
+      const bool fresh = cycles == 0 && g0 == 0;  // u = Σ y_j z_j (no read of an initial zero u)
+      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part, nullptr));
     }
-    // true residual into the workspace slot of Ṽ_0 (b is never overwritten)
+    // true residual ‖b − 𝓜u‖: when the estimate says converged only its norm is needed (mode 3, no
+    // store); otherwise r is written into the workspace slot of Ṽ_0 for the next cycle (b is kept)
     V[0] = c->d_V;
-    CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part, c->d_scal + 2));
+    const bool likely_done = est <= tol;
+    CK(launch_matvec(c, d_u, V[0], likely_done ? 3 : 2, d_b, c->d_part, c->d_scal + 2));
     CK(launch_small(c, 0, 0, 0));
     CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     relres_true = h[4];
     ++cycles;
     if (relres_true <= tol) { converged = 1; break; }
+    if (likely_done) {  // estimate and true residual disagree: form r for the restart after all
+      CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part, c->d_scal + 2));
+      CK(launch_small(c, 0, 0, 0));
+    }
     if (its >= maxit) { result = CNPINT_ENOCONV; break; }
     if (!std::isfinite(relres_true)) { seterr(c, "gmres: residual not finite"); result = CNPINT_EBREAKDOWN; break; }
   }

@@ -100,7 +100,8 @@ cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStr
 // host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed
 cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
 
-// y = 𝓜u (mode 0), y = P_α u (mode 1), y = b − 𝓜u (mode 2, b given); optional Σ y² partials
+// y = 𝓜u (mode 0), y = P_α u (mode 1), y = b − 𝓜u (mode 2, b given), mode 3 = mode 2 without storing y;
+// optional Σ y² partials (folded into out when given)
 cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part,
                           double* out = nullptr);
 
@@ -124,6 +125,7 @@ cudaError_t launch_dst_y(cnpint_ctx* c, const double* in, double* out, int inver
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 
 // GMRES helpers
+cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* out);  // out = Σ w²
 // partial sums into part; if out != nullptr the last block folds them (deterministically) into out
 cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w, double* part, double* out);
 cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int accumulate_sq);

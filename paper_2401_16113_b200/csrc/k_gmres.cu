@@ -55,6 +55,20 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double*
   if (out) grid_fold(part, gridDim.x, stride, NV, out, counter);
 }
 
+// Σ w² (one read of w), folded into out
+__global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restrict__ w, size_t n2,
+                                                            double* __restrict__ part, int stride,
+                                                            double* __restrict__ out, unsigned* counter) {
+  double acc[1] = {0.0};
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+    const double2 x = ldg_cs2(w2 + e);
+    acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
+  }
+  block_reduce_write<1>(acc, part, stride);
+  grid_fold(part, gridDim.x, stride, 1, out, counter);
+}
+
 // w_out = w − Σ_i coef_i Ṽ_i with coef_i = cd[i]·s_i² (MODE 0) or coef_i = cd[i] (MODE 1, combine,
 // w may be null), optionally fused partial dots with Ṽ (DOTS) or Σ w_out² (NORM).
 template <int NV, int MODE, bool DOTS, bool NORM>
@@ -191,6 +205,13 @@ cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* 
     default: return cudaErrorInvalidValue;
   }
   cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c) * (nv + 1));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* out) {
+  cnp_prof_begin(c, KID_DOTS);
+  k_norm2<<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
+  cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c));
   return cudaGetLastError();
 }
 

@@ -74,7 +74,8 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
 }
 
 // ------------------------------------------------------------------------------- K1 1D
-// MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  NORM: per-block Σ y².
+// MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  MODE 3: as 2 without storing y (norm
+// only).  NORM: per-block Σ y².
 template <int MODE, bool NORM>
 __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, const double* __restrict__ lo,
@@ -127,13 +128,13 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
     if (lane == 31) sr = hasR ? cr + pr : 0.0;
     double y0 = d0 - htau * fma(lo0, sl, fma(di0, s0, up0 * s1));
     double y1 = d1 - htau * fma(lo1, s0, fma(di1, s1, up1 * sr));
-    if (MODE == 2) {
+    if (MODE >= 2) {
       double2 bv = make_double2(0.0, 0.0);
       if (active) bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * ld + x0));
       y0 = bv.x - y0;
       y1 = bv.y - y1;
     }
-    if (active) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
+    if (active && MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
     if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     pv = cv; pl = cl; pr = cr;
   }
@@ -207,13 +208,13 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
     double y1 = (cv.y - pv.y) - htau * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
     if (x0 >= nx) y0 = 0.0;
     if (x0 + 1 >= nx) y1 = 0.0;
-    if (MODE == 2 && act) {
+    if (MODE >= 2 && act) {
       double2 bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * slice + off));
       y0 = bv.x - y0;
       y1 = bv.y - y1;
     }
     if (act) {
-      stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
+      if (MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
       if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     }
     pv = cv; ph = ch; pl = cl; pr = cr;
@@ -242,7 +243,7 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
                                                          c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
                                                          part, out, c->d_counter);
   }
-  cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));
+  cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
   return cudaGetLastError();
 }
 
@@ -260,6 +261,7 @@ cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, c
     case 0: return run_matvec<0, false>(c, u, y, nullptr, nullptr, nullptr);
     case 1: return run_matvec<1, false>(c, u, y, nullptr, nullptr, nullptr);
     case 2: return part ? run_matvec<2, true>(c, u, y, b, part, out) : run_matvec<2, false>(c, u, y, b, nullptr, nullptr);
+    case 3: return run_matvec<3, true>(c, u, y, b, part, out);
     default: return cudaErrorInvalidValue;
   }
 }
