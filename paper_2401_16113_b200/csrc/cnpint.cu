@@ -148,8 +148,8 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
     std::memset(&tmp, 0, sizeof(tmp));
     tmp.dim = op->dim; tmp.N = N; tmp.ld = ld; tmp.ny = ny;
     size_t mv = (size_t)matvec_partial_blocks(&tmp);
-    size_t rows = CNP_RED_BLOCKS * (CNP_MAX_DOT + 1);
-    L.part = take((rows > mv ? rows : mv) * 8);
+    size_t blocks = mv > CNP_RED_BLOCKS ? mv : CNP_RED_BLOCKS;
+    L.part = take(blocks * (CNP_MAX_DOT + 1) * 8);
   }
   L.scal = take(16 * 8);
   L.status = take(64);
@@ -650,13 +650,14 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       if (st != CNPINT_OK) return st;
       // w = 𝓜 z_j, written straight into the slot of Ṽ_{j+1}
       double* w = V[j + 1];
-      CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
       const int nv = j + 1;
       if (nv <= CNP_MAX_DOT) {
-        CK(launch_dots(c, V.data(), nv, w, c->d_part, c->d_c1));
+        // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw)
+        CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
         CK(launch_update(c, V.data(), nv, c->d_c1, 0, w, w, 1, 0, c->d_part, c->d_c2));
         CK(launch_update(c, V.data(), nv, c->d_c2, 0, w, w, 0, 1, c->d_part, c->d_scal + 2));
       } else {
+        CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
         // groups of CNP_MAX_DOT: dots, update (no fusion), dots, update, norm
         for (int pass = 0; pass < 2; ++pass) {
           double* cd = pass == 0 ? c->d_c1 : c->d_c2;

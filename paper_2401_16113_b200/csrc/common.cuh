@@ -40,6 +40,28 @@ CNP_DEV double warp_sum(double v) {
   return v;
 }
 
+// Block reduction of NV per-thread accumulators (any block shape, ≤ 32 warps): fixed warp trees and a
+// fixed-order sum over warps; writes part[block_linear * stride + i], i < NV.
+template <int NV>
+CNP_DEV void block_reduce_nv(double (&acc)[NV], double* part, int stride) {
+  __shared__ double red[32][NV];
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = (blockDim.x * blockDim.y) >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double v = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][i] = v;
+  }
+  __syncthreads();
+  if (tid < NV) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += red[w][tid];
+    part[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (size_t)blockIdx.z)) * stride + tid] = v;
+  }
+}
+
 // Deterministic grid-level fold.  Every block has written its partial sums part[b*stride + col]
 // (col < ncols); the last block to arrive (atomic ticket) adds them up in block order — lane l sums
 // b = l, l+32, ... in order, then a fixed shuffle tree — and writes out[col], so the result does not

@@ -97,6 +97,12 @@ struct cnpint_ctx {
 // ------------------------------------------------------------------ kernel launchers (return cudaError_t)
 cudaError_t launch_stream_copy(const double* src, double* dst, size_t n, cudaStream_t s);
 
+struct DotPtrs {
+  const double* p[CNP_MAX_DOT];
+};
+// y = 𝓜u fused with the first CGS pass: out[i] = Ṽ_iᵀ y, i < nv <= CNP_MAX_DOT (deterministic fold)
+cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
+                               double* out);
 // host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed
 cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
 

@@ -76,13 +76,16 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
 // ------------------------------------------------------------------------------- K1 1D
 // MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  MODE 3: as 2 without storing y (norm
 // only).  NORM: per-block Σ y².
-template <int MODE, bool NORM>
+template <int MODE, bool NORM, int NVD = 0>
 __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, const double* __restrict__ lo,
                                                   const double* __restrict__ di, const double* __restrict__ up,
                                                   int N, int64_t ld, double htau, double alpha, int tchunk,
                                                   double* __restrict__ part, double* __restrict__ out,
-                                                  unsigned* counter) {
+                                                  unsigned* counter, DotPtrs vd = DotPtrs{}) {
+  double dacc[NVD > 0 ? NVD : 1];
+#pragma unroll
+  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
   const bool active = 2 * gx < ld;
@@ -135,22 +138,37 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
       y1 = bv.y - y1;
     }
     if (active && MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
+    if (NVD > 0 && active) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+#pragma unroll
+      for (int i = 0; i < NVD; ++i) {
+        const double2 v = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * ld + x0));
+        dacc[i] = fma(v.x, y0, fma(v.y, y1, dacc[i]));
+      }
+    }
     if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     pv = cv; pl = cl; pr = cr;
   }
   if (NORM) block_partial<128>(acc, part, out, counter);
+  if constexpr (NVD > 0) {
+    block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
+    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+  }
 }
 
 // ------------------------------------------------------------------------------- K1 2D
 // Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread walks a
 // chunk of t.  y-neighbours of s = u_t + u_{t-1} are exchanged through a double-buffered shared
 // row array; the edge warps also carry the halo rows y0-1 and y0+8.
-template <int MODE, bool NORM>
+template <int MODE, bool NORM, int NVD = 0>
 __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
                                                   double htau, double alpha, double cxs, double cxu, double cys,
                                                   double cyu, double cdiag, int tchunk, double* __restrict__ part,
-                                                  double* __restrict__ out, unsigned* counter) {
+                                                  double* __restrict__ out, unsigned* counter,
+                                                  DotPtrs vd = DotPtrs{}) {
+  double dacc[NVD > 0 ? NVD : 1];
+#pragma unroll
+  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
   __shared__ double2 S[2][10][32];
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
@@ -215,12 +233,23 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
     }
     if (act) {
       if (MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
+      if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+#pragma unroll
+        for (int i = 0; i < NVD; ++i) {
+          const double2 v = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * slice + off));
+          dacc[i] = fma(v.x, y0, fma(v.y, y1, dacc[i]));
+        }
+      }
       if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     }
     pv = cv; ph = ch; pl = cl; pr = cr;
     buf ^= 1;
   }
   if (NORM) block_partial<256>(acc, part, out, counter);
+  if constexpr (NVD > 0) {
+    block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
+    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+  }
 }
 
 // ----------------------------------------------------------------------------------- launcher
@@ -245,6 +274,47 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
   return cudaGetLastError();
+}
+
+template <int NVD>
+static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, const DotPtrs& vd, double* part,
+                                   double* out) {
+  const double htau = 0.5 * c->tau;
+  cnp_prof_begin(c, KID_MATVEC);
+  if (c->dim == 1) {
+    const int tchunk = c->N >= 4096 ? 32 : 16;
+    dim3 block(128);
+    dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
+    k_matvec1d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N, c->ld,
+                                                            htau, c->alpha, tchunk, part, out, c->d_counter, vd);
+  } else {
+    const int tchunk = 16;
+    dim3 block(32, 8);
+    dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
+    k_matvec2d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
+                                                            c->alpha, c->xs, c->xu, c->ys, c->yu,
+                                                            c->xd + c->yd + c->shift, tchunk, part, out,
+                                                            c->d_counter, vd);
+  }
+  cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
+                               double* out) {
+  DotPtrs vd{};
+  for (int i = 0; i < nv && i < CNP_MAX_DOT; ++i) vd.p[i] = V[i];
+  switch (nv) {
+    case 1: return run_matvec_dots<1>(c, u, y, vd, part, out);
+    case 2: return run_matvec_dots<2>(c, u, y, vd, part, out);
+    case 3: return run_matvec_dots<3>(c, u, y, vd, part, out);
+    case 4: return run_matvec_dots<4>(c, u, y, vd, part, out);
+    case 5: return run_matvec_dots<5>(c, u, y, vd, part, out);
+    case 6: return run_matvec_dots<6>(c, u, y, vd, part, out);
+    case 7: return run_matvec_dots<7>(c, u, y, vd, part, out);
+    case 8: return run_matvec_dots<8>(c, u, y, vd, part, out);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 int matvec_partial_blocks(const cnpint_ctx* c) {
