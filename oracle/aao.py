@@ -9,6 +9,10 @@ Plain definitions written out:
   PAPER.md:198-203 (Eq. 2.2) 𝓜 = B1 ⊗ I − B2 ⊗ Ã, B1 = tridiag(−1,1,0), B2 = ½ tridiag(1,1,0).
   PAPER.md:244-266 (Eq. 3.1) P_α = C1^(α) ⊗ I − C2^(α) ⊗ Ã.
   PAPER.md:125-128 (Eq. 2.1) CN step (I − τ/2 A) u^{k+1} = (I + τ/2 A) u^k + τ f^{k+½}.
+  PAPER.md:1020-1036 (Eq. 5.8) time-dependent 𝓛(t) = d(t)𝓛: 𝓜 = B1 ⊗ I − (D̃B2) ⊗ Ã with
+                           D̃ = diag(d(t_{k+½})), i.e. row t of the block form uses Q1, Q2 with
+                           Ã → d(t_{t+½})Ã; the preconditioner replaces C2^(α) by d̄·C2^(α),
+                           d̄ = mean_k d(t_{k+½}), i.e. Ã → d̄Ã.
 Vectors are arrays of shape (N, m) (1D) or (N, n, n) (2D, [t][y][x]).
 """
 from __future__ import annotations
@@ -25,6 +29,18 @@ def tau_of(w) -> float:
     return w.T / w.N
 
 
+def d_half(w) -> np.ndarray:
+    """D̃ = diag(d(t_{½}), …, d(t_{N−½})); all ones for constant 𝓛."""
+    tau = tau_of(w)
+    return np.exp(-w.dt_rate * (np.arange(w.N) + 0.5) * tau)
+
+
+def tau_prec(w) -> float:
+    """τ of the preconditioner's Ã: d̄τ with d̄ = (1/N) Σ_k d(t_{k+½}); τ if 𝓛 is
+    constant."""
+    return tau_of(w) * float(np.mean(d_half(w))) if w.dt_rate else tau_of(w)
+
+
 def Q1(op, tau, z):
     """Q1 z = z − ½ τ L_h z."""
     return z - 0.5 * tau * apply_L(op, z)
@@ -36,18 +52,29 @@ def Q2(op, tau, z):
 
 
 def apply_M(w, op, u: np.ndarray) -> np.ndarray:
-    """𝓜u by the block form of PAPER.md:337-343: y_0 = Q1u_0, y_t = Q1u_t − Q2u_{t−1}."""
+    """𝓜u by the block form of PAPER.md:337-343: y_0 = Q1u_0, y_t = Q1u_t − Q2u_{t−1}; with
+    𝓛(t) = d(t)𝓛 row t uses Ã → d(t_{t+½})Ã (the t-th row of D̃B2)."""
     tau = tau_of(w)
-    y = Q1(op, tau, u)
-    y[1:] -= Q2(op, tau, u[:-1])
+    if not w.dt_rate:
+        y = Q1(op, tau, u)
+        y[1:] -= Q2(op, tau, u[:-1])
+        return y
+    d = d_half(w)
+    y = np.empty_like(u)
+    for t in range(w.N):
+        y[t] = Q1(op, tau * d[t], u[t])
+        if t:
+            y[t] -= Q2(op, tau * d[t], u[t - 1])
     return y
 
 
 def apply_P(w, op, z: np.ndarray, alpha: float | None = None) -> np.ndarray:
-    """P_α z by the block form of PAPER.md:344-350: as 𝓜 plus (P z)_0 −= α Q2 z_{N−1}."""
+    """P_α z by the block form of PAPER.md:344-350: rows Q1z_t − Q2z_{t−1} and the corner
+    (P z)_0 −= α Q2 z_{N−1}; Ã is d̄τL_h for a time-dependent 𝓛."""
     alpha = w.alpha if alpha is None else alpha
-    tau = tau_of(w)
-    y = apply_M(w, op, z)
+    tau = tau_prec(w)
+    y = Q1(op, tau, z)
+    y[1:] -= Q2(op, tau, z[:-1])
     y[0] -= alpha * Q2(op, tau, z[-1])
     return y
 
@@ -89,13 +116,17 @@ class Q1Solver:
 
 def solve_sequential(w, op, b: np.ndarray) -> np.ndarray:
     """The exact AaO solution by CN time stepping:
-    Q1 u_t = b_t + Q2 u_{t−1}, u_{−1} := 0 (u⁰ enters through ξ in b_0)."""
+    Q1 u_t = b_t + Q2 u_{t−1}, u_{−1} := 0 (u⁰ enters through ξ in b_0); for 𝓛(t) = d(t)𝓛 step t
+    uses d(t_{t+½})τ (Eq. 5.8)."""
     tau = tau_of(w)
-    solve = Q1Solver(op, tau)
+    d = d_half(w)
+    solve = Q1Solver(op, tau) if not w.dt_rate else None
     u = np.empty_like(b)
     prev = np.zeros_like(b[0])
     for t in range(w.N):
-        u[t] = solve(b[t] + Q2(op, tau, prev))
+        tt = tau * d[t]
+        s = solve if solve is not None else Q1Solver(op, tt)
+        u[t] = s(b[t] + Q2(op, tt, prev))
         prev = u[t]
     return u
 
@@ -127,13 +158,13 @@ def C2(N, alpha):
 
 
 def dense_M(w, op) -> np.ndarray:
-    """𝓜 = B1 ⊗ I − B2 ⊗ Ã, Ã = τ L_h."""
+    """𝓜 = B1 ⊗ I − (D̃B2) ⊗ Ã, Ã = τ L_h (D̃ = I for constant 𝓛, Eq. 5.8)."""
     At = tau_of(w) * op.dense()
-    return np.kron(B1(w.N), np.eye(op.m)) - np.kron(B2(w.N), At)
+    return np.kron(B1(w.N), np.eye(op.m)) - np.kron(np.diag(d_half(w)) @ B2(w.N), At)
 
 
 def dense_P(w, op, alpha=None) -> np.ndarray:
-    """P_α = C1^(α) ⊗ I − C2^(α) ⊗ Ã (PAPER.md:264-266, Eq. 3.1)."""
+    """P_α = C1^(α) ⊗ I − (d̄C2^(α)) ⊗ Ã (Eq. 3.1; d̄ = 1 for constant 𝓛)."""
     alpha = w.alpha if alpha is None else alpha
-    At = tau_of(w) * op.dense()
+    At = tau_prec(w) * op.dense()
     return np.kron(C1(w.N, alpha), np.eye(op.m)) - np.kron(C2(w.N, alpha), At)

@@ -32,7 +32,7 @@ import math
 
 import numpy as np
 
-from .aao import Q1Solver, Q2, tau_of
+from .aao import Q1Solver, Q2, tau_prec
 from .problem import Operator1D
 
 
@@ -121,7 +121,7 @@ def shifted_solve(w, op, lam1: np.ndarray, lam2: np.ndarray, rhs: np.ndarray) ->
     1D: complex Thomas vectorised across k.  2D: fast diagonalisation with dense DST-I matrices
     (PAPER.md:315-316)."""
     rdt = np.longdouble if lam1.dtype == np.clongdouble else np.float64
-    tau = rdt(w.T) / rdt(w.N)
+    tau = rdt(w.T) / rdt(w.N) if not w.dt_rate else rdt(tau_prec(w))   # d̄τ for 𝓛(t) = d(t)𝓛
     K = lam1.size
     if isinstance(op, Operator1D):
         l1, l2 = lam1[:, None], lam2[:, None]
@@ -224,7 +224,7 @@ def pinv_sweep(w, op, v: np.ndarray, alpha: float | None = None, max_sweeps: int
     (Lemma 3.2), so it contracts at least by α.  Stops when the update of ζ
     is below 1e-15‖ζ‖ or stops shrinking (rounding level).  Returns (z, sweeps)."""
     alpha = w.alpha if alpha is None else alpha
-    tau = tau_of(w)
+    tau = tau_prec(w)
     solve = Q1Solver(op, tau)
     zeta = np.zeros_like(v[0])
     z = np.empty_like(v)

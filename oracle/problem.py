@@ -143,7 +143,22 @@ def u_exact(w, op, t: float) -> np.ndarray:
     return math.exp(-t) * np.outer(sx, sx)                  # [y][x]
 
 
+def d_of(w, t: float) -> float:
+    """Time factor of 𝓛(t) = d(t)𝓛: d(t) = exp(−dt_rate·t); 1 when dt_rate = 0."""
+    return math.exp(-w.dt_rate * t)
+
+
 def f_source(w, op, t: float) -> np.ndarray:
+    """f = ∂_t u − d(t)𝓛u for the manufactured u (continuous 𝓛; d ≡ 1 unless dt_rate ≠ 0)."""
+    return _minus_u(w, op, t) - d_of(w, t) * _L_exact(w, op, t)
+
+
+def _minus_u(w, op, t: float) -> np.ndarray:
+    return -u_exact(w, op, t)   # ∂_t u = −u for every manufactured u = e^{−t}φ(x)
+
+
+def _L_exact(w, op, t: float) -> np.ndarray:
+    """𝓛u of the manufactured solution (continuous operator, analytic derivatives)."""
     a, b = w.domain
     e = math.exp(-t)
     if w.kind == "logprice":
@@ -152,15 +167,13 @@ def f_source(w, op, t: float) -> np.ndarray:
         u = e * np.sin(k * (op.x - a))
         ux = e * k * np.cos(k * (op.x - a))
         uxx = -k * k * u
-        Lu = 0.5 * s2 * uxx + mu * ux - w.r * u
-        return -u - Lu
+        return 0.5 * s2 * uxx + mu * ux - w.r * u
     if w.kind == "price":
         S = op.x
         u = e * S * (b - S) / (b * b)
         uS = e * (b - 2 * S) / (b * b)
         uSS = -2.0 * e / (b * b)
-        Lu = 0.5 * w.sigma ** 2 * S * S * uSS + w.r * S * uS - w.r * u
-        return -u - Lu
+        return 0.5 * w.sigma ** 2 * S * S * uSS + w.r * S * uS - w.r * u
     k = math.pi / (b - a)
     (s1, s2) = w.sigma2
     m1, m2 = w.r - 0.5 * s1 * s1, w.r - 0.5 * s2 * s2
@@ -168,17 +181,17 @@ def f_source(w, op, t: float) -> np.ndarray:
     u = e * np.outer(sx, sx)                 # [y][x]
     ux = e * k * np.outer(sx, cx)            # derivative along x (fast axis)
     uy = e * k * np.outer(cx, sx)
-    Lu = 0.5 * s1 * s1 * (-k * k * u) + 0.5 * s2 * s2 * (-k * k * u) + m1 * ux + m2 * uy - w.r * u
-    return -u - Lu
+    return 0.5 * s1 * s1 * (-k * k * u) + 0.5 * s2 * s2 * (-k * k * u) + m1 * ux + m2 * uy - w.r * u
 
 
 def assemble_rhs(w, op) -> np.ndarray:
     """b = ξ + τf (Eq. 2.2; SURVEY.md §8(c) reading #7):
-    b_t = τ f(·, (t+½)τ) for t = 0..N−1 and b_0 += (I + ½Ã) u⁰ with Ã = τ L_h."""
+    b_t = τ f(·, (t+½)τ) for t = 0..N−1 and b_0 += (I + ½Ã) u⁰ with Ã = τ L_h; with 𝓛(t) = d(t)𝓛
+    the ξ block is (I + ½d(t_½)Ã)u⁰ (Eq. 5.8)."""
     N, tau = w.N, w.T / w.N
     b = np.stack([tau * f_source(w, op, (t + 0.5) * tau) for t in range(N)])
     u0 = u_exact(w, op, 0.0)
-    b[0] += u0 + 0.5 * tau * apply_L(op, u0)
+    b[0] += u0 + 0.5 * d_of(w, 0.5 * tau) * tau * apply_L(op, u0)
     return b
 
 

@@ -43,6 +43,9 @@ class Workload:
     rand_count: int = 4      # number of N(0,1) random vectors for P^-1 / A checks
     rand_seed: int = 1
     note: str = ""
+    # time-varying operator 𝓛(t) = d(t)𝓛 with d(t) = exp(−dt_rate·t) (Eq. 5.8;
+    # SURVEY.md §8(f) NEXT #1); 0 = the constant-coefficient method of BASELINE.json.
+    dt_rate: float = 0.0
 
     @property
     def m(self) -> int:
@@ -86,7 +89,13 @@ def c5(n: int, N: int) -> Workload:
 
 C5_SIZES = [(n, N) for n in (127, 255, 511) for N in (256, 1024)]
 
-WORKLOADS = {w.name: w for w in (C1, C2, C3, C4)}
+# SURVEY.md §8(f) NEXT #1 (not a BASELINE config): the c1 / c2 operator with 𝓛(t) = e^{−t/2}𝓛, the
+# shape of the paper's Set V variant (d(t) = e^{−rt}), strengthened so that d
+# varies by 40 % over the horizon.
+C1T = C1.with_(name="c1t", dt_rate=0.5, note="NEXT #1: c1 operator with d(t) = exp(-t/2)")
+C2T = C2.with_(name="c2t", dt_rate=0.5, note="NEXT #1: c2 operator with d(t) = exp(-t/2)")
+
+WORKLOADS = {w.name: w for w in (C1, C2, C3, C4, C1T, C2T)}
 for _n, _N in C5_SIZES:
     WORKLOADS[f"c5_n{_n}_N{_N}"] = c5(_n, _N)
 

@@ -503,3 +503,77 @@ def test_gmres_c1_converges_to_sequential_cn():
     assert 2 <= rep.iterations <= 5
     assert rel(u, useq) < 1e-8
     assert all(h2 <= h1 for h1, h2 in zip(rep.history, rep.history[1:]))     # monotone within a cycle
+
+
+# ------------------------------------------------------------------------------ NEXT #1: 𝓛(t) = d(t)𝓛
+# PAPER.md:1020-1036 (Eq. 5.8): 𝓜 = B1⊗I − (D̃B2)⊗Ã, ξ₀ = (I + ½d(t_½)Ã)u⁰; the preconditioner uses d̄C2.
+
+def _tv(n=15, N=8, rate=0.5, alpha=0.1):
+    return synth.C1T.with_(name="tv", n=n, N=N, dt_rate=rate, alpha=alpha)
+
+
+def test_tv_block_matvec_equals_dense_kronecker():
+    w = _tv()
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 5)[0]
+    Md = aao.dense_M(w, op)
+    assert rel(aao.apply_M(w, op, v).reshape(-1), Md @ v.reshape(-1)) < 1e-14
+    # the d-weighting sits on the rows (D̃B2, not B2D̃): row t uses d(t_{t+½}) for both u_t and u_{t−1}
+    d = aao.d_half(w)
+    tau = aao.tau_of(w)
+    At = tau * op.dense()
+    B2D = np.kron(np.diag(d) @ aao.B2(w.N), At)
+    assert rel(np.kron(aao.B1(w.N), np.eye(op.m)) - B2D, Md) == 0.0
+    assert rel(np.kron(aao.B2(w.N) @ np.diag(d), At), B2D) > 1e-3   # the other placement differs
+
+
+def test_tv_dbar_closed_form():
+    """d̄ = (1/N) Σ_k e^{−ρτ(k+½)} = e^{−ρτ/2}(1 − e^{−ρT}) / (N(1 − e^{−ρτ})) (geometric sum)."""
+    w = _tv(N=64)
+    rho, tau = w.dt_rate, w.T / w.N
+    closed = math.exp(-rho * tau / 2) * (1 - math.exp(-rho * w.T)) / (w.N * (1 - math.exp(-rho * tau)))
+    assert abs(aao.tau_prec(w) / tau - closed) < 1e-15
+    assert aao.tau_prec(w.with_(dt_rate=0.0)) == tau
+
+
+def test_tv_sequential_cn_solves_aao():
+    w = _tv(n=31, N=32)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    u = aao.solve_sequential(w, op, b)
+    assert rel(aao.apply_M(w, op, u), b) < 1e-13
+
+
+def test_tv_second_order_convergence():
+    """The time-dependent CN solution converges at second order to u = e^{−t}sin(…) (pins f = ∂_tu −
+    d(t)𝓛u, the midpoint sampling of D̃ and the ξ block)."""
+    errs = []
+    for n in (63, 127, 255):
+        w = synth.C1T.with_(name="tvc", n=n, N=n + 1)
+        op = problem.build_operator(w)
+        u = aao.solve_sequential(w, op, problem.assemble_rhs(w, op))
+        errs.append(float(np.abs(u - problem.exact_blocks(w, op)).max()))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert 3.5 < r1 < 4.5 and 3.5 < r2 < 4.5, errs
+
+
+def test_tv_pinv_roundtrip_and_dense():
+    w = _tv(n=15, N=16)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 7)[0]
+    z = precond.pinv_dft(w, op, v)
+    assert rel(aao.apply_P(w, op, z), v) < 1e-12
+    zd = np.linalg.solve(aao.dense_P(w, op), v.reshape(-1)).reshape(v.shape)
+    assert rel(z, zd) < 1e-12
+    zs, _ = precond.pinv_sweep(w, op, v)
+    assert rel(z, zs) < 1e-12
+
+
+def test_tv_gmres_converges_to_sequential_cn():
+    w = _tv(n=63, N=64, alpha=0.01).with_(restart=40, tol=1e-10)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    u, rep = gmres.gmres_right(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
+                               w.tol, w.restart)
+    assert rep.converged and rel(u, aao.solve_sequential(w, op, b)) < 1e-8
+    assert 3 <= rep.iterations <= 12, rep.iterations   # d̄ approximation: a few more than constant 𝓛
