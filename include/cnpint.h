@@ -160,6 +160,14 @@ cnpint_status cnpint_apply_A_host(cnpint_ctx* ctx, const double* h_u, double* h_
 cnpint_status cnpint_gmres_host(cnpint_ctx* ctx, const double* h_b, double* h_u, double tol, int restart,
                                 int maxit, cnpint_gmres_report* rep);
 
+/* Time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8).
+ * d_half: host array of the N values d(t_{t+½}), t = 0..N−1 (finite, > 0), copied; NULL restores the
+ * constant-coefficient method.  Afterwards 𝓜 = B1⊗I − (D̃B2)⊗Ã with D̃ = diag(d_half) in apply_A,
+ * gmres and the true residual, and the preconditioner uses d̄·C2^(α), d̄ = mean(d_half)
+ * (apply_P, apply_Pinv and the stage kernels).  The caller forms ξ₀ = (I + ½d(t_½)Ã)u⁰ in b.
+ * Synchronises; rebuilds the tables that depend on the preconditioner's τ. */
+cnpint_status cnpint_set_time_dependence(cnpint_ctx* ctx, const double* d_half);
+
 /* Synchronise the stream and report deferred device errors (CNPINT_ESINGULAR), clearing them. */
 cnpint_status cnpint_device_status(cnpint_ctx* ctx);
 

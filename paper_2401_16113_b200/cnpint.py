@@ -27,7 +27,7 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_apply_Pinv", "cnpint_time_fft", "cnpint_shifted_solve", "cnpint_time_ifft", "cnpint_gmres",
            "cnpint_apply_Pinv_host", "cnpint_apply_A_host", "cnpint_gmres_host", "cnpint_device_status",
            "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug", "cnpint_profile_enable",
-           "cnpint_profile_read", "cnpint_kernel_name"]
+           "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence"]
 
 
 class CnpintError(RuntimeError):
@@ -81,6 +81,7 @@ def load_library(path: str = LIB_PATH):
         "cnpint_profile_enable": (C.c_int, [vp, C.c_int]),
         "cnpint_profile_read": (C.c_int, [vp, C.c_int, dp, C.POINTER(C.c_int64), dp]),
         "cnpint_kernel_name": (C.c_char_p, [C.c_int]),
+        "cnpint_set_time_dependence": (C.c_int, [vp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -288,6 +289,18 @@ class Solver:
                 out[name.decode()] = (ms.value, n.value, by.value)
             kid += 1
         return out
+
+    def set_time_dependence(self, d_half: Optional[np.ndarray]):
+        """𝓛(t) = d(t)𝓛 with the N values d(t_{t+½}) (None: constant operator)."""
+        self._sync_stream()
+        if d_half is None:
+            self._check(self.lib.cnpint_set_time_dependence(self.h, None), "set_time_dependence")
+            return
+        d = np.ascontiguousarray(d_half, dtype=np.float64)
+        if d.shape != (self.N,):
+            raise CnpintError(EINVAL, f"d_half must have shape ({self.N},)")
+        self._check(self.lib.cnpint_set_time_dependence(self.h, d.ctypes.data_as(C.POINTER(C.c_double))),
+                    "set_time_dependence")
 
     def set_debug(self, flags: int):
         self._sync_stream()

@@ -73,7 +73,7 @@ bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 struct Layout {
   size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
-  size_t V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
+  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
   size_t total;
 };
 
@@ -153,6 +153,7 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   }
   L.scal = take(16 * 8);
   L.status = take(64);
+  L.dt = take((size_t)N * 8);  // d(t_{t+½}) of a time-dependent operator (cnpint_set_time_dependence)
   L.total = off;
   return L;
 }
@@ -238,7 +239,7 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
       typedef std::complex<long double> cld;
       const int Lt = t.L, st = t.tabstride;
       std::vector<double2> tab((size_t)(H + 1) * st, make_double2(0.0, 0.0));
-      const long double tau = (long double)c->T / (long double)N;
+      const long double tau = (long double)c->tau_p;  // preconditioner τ (d̄τ for 𝓛(t) = d(t)𝓛)
       const long double a = -tau * (long double)op->xs, cc = -tau * (long double)op->xu;
       std::vector<cld> inv(Lt), al(Lt), ga(Lt), ap(Lt), gp(Lt);
       auto d2 = [](cld z) { return make_double2((double)z.real(), (double)z.imag()); };
@@ -405,7 +406,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->toeplitz = op->dim == 2 ? 1 : op->toeplitz;
   c->ld = ld_of(op->nx); c->slice = (int64_t)c->ny * c->ld; c->vec = (int64_t)N * c->slice;
   c->spec_rows = c->H + 1; c->spec_elems = c->spec_rows * c->slice;
-  c->T = T; c->tau = T / N; c->alpha = alpha; c->lnalpha = std::log(alpha); c->a = std::exp(c->lnalpha / N);
+  c->T = T; c->tau = T / N; c->tau_p = T / N; c->d_dt = nullptr; c->alpha = alpha; c->lnalpha = std::log(alpha); c->a = std::exp(c->lnalpha / N);
   c->xs = op->xs; c->xd = op->xd; c->xu = op->xu; c->ys = op->ys; c->yd = op->yd; c->yu = op->yu;
   c->shift = op->dim == 2 ? op->shift : 0.0;
   c->restart_max = restart_max;
@@ -585,15 +586,45 @@ cnpint_status cnpint_stream_copy(const double* src, double* dst, size_t n, void*
   return e == cudaSuccess ? CNPINT_OK : CNPINT_ECUDA;
 }
 
+cnpint_status cnpint_set_time_dependence(cnpint_ctx* c, const double* d_half) {
+  if (!c) return CNPINT_EINVAL;
+  if (!d_half) {
+    c->tau_p = c->tau;
+    c->d_dt = nullptr;
+  } else {
+    long double sum = 0.0L;
+    for (int t = 0; t < c->N; ++t) {
+      if (!std::isfinite(d_half[t]) || !(d_half[t] > 0.0)) {
+        seterr(c, "set_time_dependence: d(t) must be finite and positive");
+        return CNPINT_EINVAL;
+      }
+      sum += (long double)d_half[t];
+    }
+    cnpint_operator op;
+    std::memset(&op, 0, sizeof(op));
+    op.dim = c->dim; op.nx = c->nx; op.ny = c->ny; op.toeplitz = c->toeplitz;
+    Layout L = layout(c->N, &op, c->restart_max);
+    double* dd = (double*)(c->ws + L.dt);
+    CK(cudaMemcpyAsync(dd, d_half, (size_t)c->N * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->d_dt = dd;
+    c->tau_p = (double)((long double)c->tau * (sum / (long double)c->N));  // τ·d̄
+  }
+  // the K3 chunk tables depend on the preconditioner's τ: rebuild them
+  return cnpint_set_debug(c, c->debug);
+}
+
 cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
   if (!c) return CNPINT_EINVAL;
   c->debug = flags;
   // rebuild the table region with the new flags (synchronous)
   cnpint_operator op;
   std::memset(&op, 0, sizeof(op));
-  op.dim = c->dim; op.nx = c->nx; op.ny = c->ny; op.toeplitz = 1;
+  op.dim = c->dim; op.nx = c->nx; op.ny = c->ny; op.toeplitz = c->toeplitz;
   op.xs = c->xs; op.xd = c->xd; op.xu = c->xu; op.ys = c->ys; op.yd = c->yd; op.yu = c->yu; op.shift = c->shift;
-  // only tw / λ tables depend on the flags; they sit between L.tw and L.spec
+  // the coefficient rows precede L.tw and are not re-uploaded: placeholders for variable rows
+  std::vector<double> dummy(c->dim == 1 && !c->toeplitz ? c->nx : 0, 0.0);
+  if (!dummy.empty()) { op.sub = dummy.data(); op.diag = dummy.data(); op.sup = dummy.data(); }
   Layout L = layout(c->N, &op, c->restart_max);
   std::vector<char> img(L.tables_end, 0);
   make_tables(c, &op, img, L);

@@ -36,6 +36,8 @@ struct cnpint_ctx {
   int dim, nx, ny, N, H, toeplitz;
   int64_t ld, slice, vec, spec_rows, spec_elems;
   double T, tau, alpha, a, lnalpha;
+  double tau_p;        // τ of the preconditioner's Ã: τ·d̄ for 𝓛(t) = d(t)𝓛, else τ
+  double* d_dt;        // [N] d(t_{t+½}) of a time-dependent operator (Eq. 5.8), null when constant
   double xs, xd, xu, ys, yd, yu, shift;
   int restart_max;
   cudaStream_t stream;

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   const double* __restrict__ di, const double* __restrict__ up,
                                                   int N, int64_t ld, double htau, double alpha, int tchunk,
                                                   double* __restrict__ part, double* __restrict__ out,
-                                                  unsigned* counter, DotPtrs vd = DotPtrs{}) {
+                                                  unsigned* counter, DotPtrs vd = DotPtrs{},
+                                                  const double* __restrict__ dt = nullptr) {
   double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
   for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
@@ -129,8 +130,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
     double sr = __shfl_down_sync(0xffffffffu, s0, 1);
     if (lane == 0) sl = hasL ? cl + pl : 0.0;
     if (lane == 31) sr = hasR ? cr + pr : 0.0;
-    double y0 = d0 - htau * fma(lo0, sl, fma(di0, s0, up0 * s1));
-    double y1 = d1 - htau * fma(lo1, s0, fma(di1, s1, up1 * sr));
+    const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
+    double y0 = d0 - ht * fma(lo0, sl, fma(di0, s0, up0 * s1));
+    double y1 = d1 - ht * fma(lo1, s0, fma(di1, s1, up1 * sr));
     if (MODE >= 2) {
       double2 bv = make_double2(0.0, 0.0);
       if (active) bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * ld + x0));
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
                                                   double htau, double alpha, double cxs, double cxu, double cys,
                                                   double cyu, double cdiag, int tchunk, double* __restrict__ part,
                                                   double* __restrict__ out, unsigned* counter,
-                                                  DotPtrs vd = DotPtrs{}) {
+                                                  DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr) {
   double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
   for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
@@ -222,8 +224,9 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
     double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
     if (lane == 0) sl = hasL ? cl + pl : 0.0;
     if (lane == 31) sr = hasR ? cr + pr : 0.0;
-    double y0 = (cv.x - pv.x) - htau * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
-    double y1 = (cv.y - pv.y) - htau * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
+    const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
+    double y0 = (cv.x - pv.x) - ht * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
+    double y1 = (cv.y - pv.y) - ht * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
     if (x0 >= nx) y0 = 0.0;
     if (x0 + 1 >= nx) y1 = 0.0;
     if (MODE >= 2 && act) {
@@ -256,21 +259,23 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
 template <int MODE, bool NORM>
 static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part,
                               double* out) {
-  const double htau = 0.5 * c->tau;
+  // 𝓜 (modes 0, 2, 3) weights row t by d(t_{t+½}); P_α (mode 1) uses d̄
+  const double htau = 0.5 * (MODE == 1 ? c->tau_p : c->tau);
+  const double* dt = MODE == 1 ? nullptr : c->d_dt;
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec1d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau,
-                                                         c->alpha, tchunk, part, out, c->d_counter);
+                                                         c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec2d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
                                                          c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
-                                                         part, out, c->d_counter);
+                                                         part, out, c->d_counter, DotPtrs{}, dt);
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
   return cudaGetLastError();
@@ -286,7 +291,8 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec1d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N, c->ld,
-                                                            htau, c->alpha, tchunk, part, out, c->d_counter, vd);
+                                                            htau, c->alpha, tchunk, part, out, c->d_counter, vd,
+                                                            c->d_dt);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
@@ -294,7 +300,7 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     k_matvec2d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
                                                             c->alpha, c->xs, c->xu, c->ys, c->yu,
                                                             c->xd + c->yd + c->shift, tchunk, part, out,
-                                                            c->d_counter, vd);
+                                                            c->d_counter, vd, c->d_dt);
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
   return cudaGetLastError();

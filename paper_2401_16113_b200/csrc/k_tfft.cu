@@ -419,7 +419,7 @@ static cudaError_t launch_c(cnpint_ctx* c, const TfftCfg& f, const double* vin, 
   cfg.gridDim = dim3(ncl * C);
   return cudaLaunchKernelEx(&cfg, kern, vin, spin, vout, spout, vscale, W, (const double*)c->d_gam,
                             (const double*)c->d_igam, accumulate, (const double2*)c->d_lam1, (const double2*)c->d_lam2,
-                            (const double*)c->d_ex, (const double*)c->d_ey, c->tau * c->shift, c->tau, (int64_t)c->ld,
+                            (const double*)c->d_ex, (const double*)c->d_ey, c->tau_p * c->shift, c->tau_p, (int64_t)c->ld,
                             c->nx, c->debug & 1, ntiles);
 }
 

@@ -211,7 +211,7 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
   cnp_prof_begin(c, kid);
   k_time_fft<MODE><<<grid, f.T, f.smem, c->stream>>>(vin, spin, vout, spout, vscale, c->N, f.logH, W, f.X, f.CS,
                                                     c->d_tw, c->d_gam, c->d_igam, accumulate, c->d_lam1, c->d_lam2,
-                                                    c->d_ex, c->d_ey, c->tau * c->shift, c->tau, c->ld);
+                                                    c->d_ex, c->d_ey, c->tau_p * c->shift, c->tau_p, c->ld);
   cnp_prof_end(c, kid, bytes);
   return cudaGetLastError();
 }

@@ -487,7 +487,7 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
                                t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
   k_tridiag<MODE, L><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
       what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS,
-      t.padsh, t.smask, t.tabstride, c->tau, c->d_status);
+      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status);
   return cudaGetLastError();
 }
 
@@ -501,7 +501,7 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
   cudaError_t e;
   if (t.small) {
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
-                                                            m, W, c->tau, K, c->d_status);
+                                                            m, W, c->tau_p, K, c->d_status);
     e = cudaGetLastError();
   } else if (!c->toeplitz) {
     e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, what, zhat)

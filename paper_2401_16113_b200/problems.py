@@ -44,8 +44,19 @@ def operator_spec(w) -> OperatorSpec:
     raise ValueError(w.kind)
 
 
+def d_time(w, t):
+    """d(t) of a time-dependent operator 𝓛(t) = d(t)𝓛: exp(−dt_rate·t)."""
+    return math.exp(-w.dt_rate * t)
+
+
+def d_half(w) -> np.ndarray:
+    """The N values d(t_{k+½}) handed to cnpint_set_time_dependence (D̃ of Eq. 5.8)."""
+    tau = w.T / w.N
+    return np.array([d_time(w, (k + 0.5) * tau) for k in range(w.N)])
+
+
 def _exact_and_source(w, x, t):
-    """(u(x, t), f(x, t)) of the manufactured solution, f = ∂_t u − 𝓛u (analytic 𝓛)."""
+    """(u(x, t), f(x, t)) of the manufactured solution, f = ∂_t u − d(t)𝓛u (analytic 𝓛)."""
     import torch
     lo_, hi_ = w.domain
     e = math.exp(-t)
@@ -55,14 +66,14 @@ def _exact_and_source(w, x, t):
         u = e * s
         mu = w.r - 0.5 * w.sigma ** 2
         Lu = (-0.5 * w.sigma ** 2 * k * k - w.r) * u + mu * k * e * c
-        return u, -u - Lu
+        return u, -u - d_time(w, t) * Lu
     if w.kind == "price":
         L = hi_
         u = e * x * (L - x) / (L * L)
         uS = e * (L - 2.0 * x) / (L * L)
         uSS = -2.0 * e / (L * L)
         Lu = 0.5 * w.sigma ** 2 * x * x * uSS + w.r * x * uS - w.r * u
-        return u, -u - Lu
+        return u, -u - d_time(w, t) * Lu
     k = math.pi / (hi_ - lo_)
     s, c = torch.sin(k * (x - lo_)), torch.cos(k * (x - lo_))
     s1, s2 = w.sigma2
@@ -70,7 +81,7 @@ def _exact_and_source(w, x, t):
     ux = e * s[:, None] * c[None, :] * k
     uy = e * c[:, None] * s[None, :] * k
     Lu = -(0.5 * (s1 * s1 + s2 * s2) * k * k + w.r) * u + (w.r - 0.5 * s1 * s1) * ux + (w.r - 0.5 * s2 * s2) * uy
-    return u, -u - Lu
+    return u, -u - d_time(w, t) * Lu
 
 
 def _apply_L_torch(spec: OperatorSpec, u):
@@ -99,19 +110,23 @@ def _apply_L_torch(spec: OperatorSpec, u):
 
 def rhs(w, solver):
     """b = ξ + τf as a zero-padded device vector in the solver's layout:
-    b_t = τ f(·, (t+½)τ), plus (I + ½τL_h) u⁰ in block 0.  Every manufactured solution here is
-    u = e^{−t}φ(x), so f(x, t) = e^{−t} f(x, 0) and the time dependence is one outer product."""
+    b_t = τ f(·, (t+½)τ), plus (I + ½d(t_½)τL_h) u⁰ in block 0 (d ≡ 1 unless 𝓛(t) = d(t)𝓛, Eq. 5.8).
+    Every manufactured solution here is u = e^{−t}φ(x), so f(x, t) = e^{−t}(−φ − d(t)𝓛φ) and the
+    time dependence is an outer product."""
     import torch
     spec = operator_spec(w)
     _, xs = grid(w)
     x = torch.as_tensor(xs, dtype=torch.float64, device=solver.device)
     tau = w.T / w.N
-    u0, f0 = _exact_and_source(w, x, 0.0)
-    et = torch.exp(-(torch.arange(w.N, dtype=torch.float64, device=solver.device) + 0.5) * tau)
+    phi, f0 = _exact_and_source(w.with_(dt_rate=0.0), x, 0.0)
+    Lphi = -phi - f0                                          # 𝓛φ (continuous operator)
+    th = (torch.arange(w.N, dtype=torch.float64, device=solver.device) + 0.5) * tau
+    et = torch.exp(-th)
+    dt = torch.exp(-w.dt_rate * th)
     b = solver.empty()
-    shape = (w.N,) + (1,) * f0.dim()
-    b[..., : w.n] = tau * et.reshape(shape) * f0
-    b[0, ..., : w.n] += u0 + 0.5 * tau * _apply_L_torch(spec, u0.clone())
+    shape = (w.N,) + (1,) * phi.dim()
+    b[..., : w.n] = tau * et.reshape(shape) * (-phi - dt.reshape(shape) * Lphi)
+    b[0, ..., : w.n] += phi + 0.5 * d_time(w, 0.5 * tau) * tau * _apply_L_torch(spec, phi.clone())
     return b
 
 
@@ -130,4 +145,7 @@ def exact(w, solver):
 
 def make_solver(w, restart_max: int = 0, alpha: float | None = None):
     from .cnpint import Solver
-    return Solver(w.N, w.T, w.alpha if alpha is None else alpha, operator_spec(w), restart_max)
+    s = Solver(w.N, w.T, w.alpha if alpha is None else alpha, operator_spec(w), restart_max)
+    if w.dt_rate:
+        s.set_time_dependence(d_half(w))
+    return s

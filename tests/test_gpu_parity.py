@@ -46,6 +46,10 @@ SMALL = {
     "1d_N16384_C8": synth.scaled(synth.C3, 9, 16384, alpha=0.1, T=5.0),
     "2d_N1024_C2": synth.scaled(synth.C4, 15, 1024, alpha=0.01),
     "2d_n63_N2048": synth.scaled(synth.C4, 63, 2048, alpha=0.01),
+    # NEXT #1: time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8)
+    "1d_tv": synth.scaled(synth.C1T, 63, 64, alpha=0.01),
+    "1d_tv_price": synth.scaled(synth.C3, 127, 128, alpha=0.01, dt_rate=0.3),
+    "2d_tv": synth.scaled(synth.C4, 15, 32, alpha=0.05, dt_rate=0.5),
 }
 
 
@@ -66,7 +70,7 @@ def test_operator_rows_match_oracle(name):
         assert rel(got, exp) < 1e-14
 
 
-@pytest.mark.parametrize("name", ["1d_small", "1d_price", "2d_small", "c1"])
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "2d_small", "c1", "1d_tv", "1d_tv_price", "2d_tv"])
 def test_rhs_matches_oracle(name):
     w = SMALL[name]
     s = solver_for(w)
@@ -367,3 +371,31 @@ def test_gmres_c5_mesh_independence():
         torch.cuda.empty_cache()
     assert max(its.values()) - min(its.values()) <= 1, its
     assert all(3 <= v <= 6 for v in its.values()), its
+
+
+# ------------------------------------------------------------------------------ NEXT #1 GMRES
+@pytest.mark.parametrize("name", ["1d_tv", "1d_tv_price", "2d_tv"])
+def test_gmres_time_dependent(name):
+    """𝓛(t) = d(t)𝓛 (Eq. 5.8) with the d̄ preconditioner: counts ±1 vs the oracle (≈ 6, cf. Table 4),
+    iterates 1e-9, final u = sequential CN (1e-8)."""
+    w = SMALL[name].with_(restart=40)
+    rep, orep = _gmres_case(w)
+    assert rep["iterations"] >= 4
+
+
+def test_time_dependent_full_c2t():
+    """c2 size with d(t) = e^{−t/2}: 𝓜 vs the oracle, P⁻¹ backward error, GMRES vs sequential CN."""
+    w = synth.C2T
+    op = problem.build_operator(w)
+    s = solver_for(w, restart_max=w.restart)
+    v = synth.random_vectors(w, 1)[0]
+    y = s.empty()
+    s.apply_A(s.to_device(v), y)
+    assert rel(s.to_host(y), aao.apply_M(w, op, v)) < 1e-12
+    z = s.empty()
+    s.apply_Pinv(s.to_device(v), z)
+    assert rel(aao.apply_P(w, op, s.to_host(z)), v) < 1e-12
+    b = problem.assemble_rhs(w, op)
+    u = s.empty()
+    rep = s.gmres(problems.rhs(w, s), u, w.tol, w.restart)
+    assert rep["converged"] and rel(s.to_host(u), aao.solve_sequential(w, op, b)) < 1e-8
