@@ -577,3 +577,53 @@ def test_tv_gmres_converges_to_sequential_cn():
                                w.tol, w.restart)
     assert rep.converged and rel(u, aao.solve_sequential(w, op, b)) < 1e-8
     assert 3 <= rep.iterations <= 12, rep.iterations   # d̄ approximation: a few more than constant 𝓛
+
+
+# ------------------------------------------------------------------------------ NEXT #2: P₁ (α = 1)
+# PAPER.md:324-328 (Remark 3.2): P₁ = C1^(1)⊗I − C2^(1)⊗Ã is the block circulant preconditioner; it is
+# singular exactly when Ã is, because λ1,1 = 0 (here k = 0) leaves −λ2,1Ã = −Ã.
+
+def test_P1_inverse_equals_dense_solve_and_roundtrip():
+    w = synth.scaled(synth.C1, 15, 16, alpha=1.0)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 3)[0]
+    z = precond.pinv_dft(w, op, v)
+    assert rel(aao.apply_P(w, op, z), v) < 1e-12
+    zd = np.linalg.solve(aao.dense_P(w, op), v.reshape(-1)).reshape(v.shape)
+    assert rel(z, zd) < 1e-12
+    # the λ pair at k = N/2 degenerates to (2, 0): that shifted system is 2 z = w (no spatial coupling)
+    l1, l2 = precond.lambdas(w.N, 1.0)
+    assert abs(l1[w.N // 2] - 2.0) < 1e-14 and abs(l2[w.N // 2]) < 1e-14 and abs(l1[0]) < 1e-14
+
+
+def test_P1_singular_iff_A_singular():
+    """Remark 3.2: with a singular Ã (zero row sums: reflecting ends), P₁ is singular while P_α (α < 1)
+    is not; with the Dirichlet operators of the workloads P₁ is invertible."""
+    m, N = 7, 4
+    lo = np.ones(m); up = np.ones(m); di = -2.0 * np.ones(m)
+    di[0] = di[-1] = -1.0                                   # reflecting ends: L·1 = 0
+    op = problem.Operator1D(lo=lo, di=di, up=up, x=np.arange(1, m + 1) * 0.1, h=0.1)
+    w = synth.scaled(synth.C1, m, N, alpha=1.0)
+    s1 = np.linalg.svd(aao.dense_P(w, op), compute_uv=False)
+    sa = np.linalg.svd(aao.dense_P(w.with_(alpha=0.5), op), compute_uv=False)
+    assert s1[-1] < 1e-12 * s1[0]
+    assert sa[-1] > 1e-3 * sa[0]
+    wd = synth.scaled(synth.C1, 15, 8, alpha=1.0)
+    sd = np.linalg.svd(aao.dense_P(wd, problem.build_operator(wd)), compute_uv=False)
+    assert sd[-1] > 1e-6 * sd[0]
+
+
+def test_P1_needs_more_gmres_iterations():
+    """The paper's comparison (Tables 1-4: P₁ 21-131 iterations vs P_α 4-6): on the c1 family the
+    oracle's right-preconditioned GMRES needs more iterations with P₁ than with P_0.01."""
+    w = synth.scaled(synth.C1, 63, 64, restart=50)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    its = {}
+    for a in (1.0, 0.01):
+        wa = w.with_(alpha=a)
+        u, rep = gmres.gmres_right(lambda x: aao.apply_M(wa, op, x), lambda x: precond.pinv_dft(wa, op, x), b,
+                                   1e-10, 50)
+        assert rep.converged and rel(u, aao.solve_sequential(wa, op, b)) < 1e-8
+        its[a] = rep.iterations
+    assert its[1.0] > its[0.01] + 2, its
