@@ -102,7 +102,11 @@ typedef struct {
 size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max);
 
 /* Create a handle.  N: time steps, power of two, 2 <= N <= 65536.  T > 0: horizon (τ = T/N).
- * alpha in (0, 1): the α of C1^(α), C2^(α) (α = 1 is P_1, out of scope).
+ * alpha in (0, 1]: the α of C1^(α), C2^(α).  α = 1 is the block circulant P_1 of
+ * the paper's comparison (NEXT #2): its k = N/2 shifted system degenerates to λ1 z = w, and P_1 is
+ * singular iff Ã is (Remark 3.2) — for Toeplitz / 2D operators create checks the
+ * closed-form spectrum and returns CNPINT_ESINGULAR; for variable rows a zero / non-finite pivot is
+ * reported by cnpint_device_status / cnpint_gmres.
  * d_workspace: device pointer, >= cnpint_workspace_bytes bytes, 256-B aligned.
  * cuda_stream: cudaStream_t (may be NULL = legacy default stream). */
 cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <algorithm>
 #include <complex>
 #include <cmath>
 #include <cstdarg>
@@ -220,12 +221,20 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
     long double th = 2.0L * PI * (long double)k / (long double)N;
     long double sh = sinl(0.5L * th);
     long double sn = sinl(th), cs = cosl(th);
+    if (2 * k == N) { sh = 1.0L; sn = 0.0L; cs = -1.0L; }  // exact at θ = π (λ2 = 0 when α = 1)
     if (c->debug & 2) sn = -sn;  // printed Eq. eigCx ordering (negative control)
     long double r1 = one_m_a + 2.0L * a * sh * sh, i1 = a * sn;        // 1 − a cos θ + i a sin θ
     long double r2 = 0.5L * (1.0L + a * cs), i2 = -0.5L * a * sn;      // ½(1 + a cos θ) − ½ i a sin θ
     long double den = r2 * r2 + i2 * i2;
     l1[k] = make_double2((double)r1, (double)i1);
     l2[k] = make_double2((double)r2, (double)i2);
+    if (den == 0.0L) {
+      // α = 1, k = N/2: λ2 = 0, the shifted system is λ1 z = w (no spatial coupling).  K3 recognises
+      // il2 = 0 and divides by λ1.
+      sk[k] = make_double2(0.0, 0.0);
+      il2[k] = make_double2(0.0, 0.0);
+      continue;
+    }
     sk[k] = make_double2((double)((r1 * r2 + i1 * i2) / den), (double)((i1 * r2 - r1 * i2) / den));
     il2[k] = make_double2((double)(r2 / den), (double)(-i2 / den));
   }
@@ -246,8 +255,10 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
       for (int k = 0; k <= H; ++k) {
         long double th = 2.0L * PI * (long double)k / (long double)N;
         long double sh = sinl(0.5L * th), sn = sinl(th), cs = cosl(th);
+        if (2 * k == N) { sh = 1.0L; sn = 0.0L; cs = -1.0L; }
         if (c->debug & 2) sn = -sn;
         const cld l1(one_m_a + 2.0L * a_ld * sh * sh, a_ld * sn), l2(0.5L * (1.0L + a_ld * cs), -0.5L * a_ld * sn);
+        if (std::norm(l2) == 0.0L) continue;  // diagonal-only system (α = 1, k = N/2): no table
         const cld b = l1 / l2 - cld(tau * (long double)op->xd, 0.0L);
         double2* tb = tab.data() + (size_t)k * st;
         for (int j = 1; j < Lt; ++j) {
@@ -387,10 +398,34 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   const char* msg = check_op(N, op, &uns);
   if (msg) return uns ? CNPINT_EUNSUPPORTED : CNPINT_EINVAL;
   if (!(T > 0.0) || !std::isfinite(T)) return CNPINT_EINVAL;
-  if (!(alpha > 0.0 && alpha < 1.0)) return CNPINT_EINVAL;
+  if (!(alpha > 0.0 && alpha <= 1.0)) return CNPINT_EINVAL;  // α = 1: P₁ (NEXT #2)
   if (restart_max < 0 || restart_max > 1000) return CNPINT_EINVAL;
   Layout L = layout(N, op, restart_max);
   if (!d_workspace || ws_bytes < L.total || ((uintptr_t)d_workspace & (ALIGN - 1))) return CNPINT_EINVAL;
+  if (alpha == 1.0 && (op->dim == 2 || op->toeplitz)) {
+    // P₁ is singular iff Ã is (Remark 3.2): λ1 = 0 at k = 0 leaves −λ2Ã.  Closed-form
+    // spectrum of the Toeplitz (Kronecker-sum) operator: μ = d + 2 sgn(s)√(su) cos(jπ/(n+1)).
+    auto eig = [](double s, double d, double u, int n, int j) {
+      const double r = s * u > 0.0 ? std::sqrt(s * u) * (s > 0.0 ? 1.0 : -1.0) : 0.0;
+      return d + 2.0 * r * std::cos(M_PI * j / (n + 1.0));
+    };
+    double mn = HUGE_VAL, mx = 0.0;
+    if (op->dim == 1) {
+      if (op->xs * op->xu > 0.0)
+        for (int j = 1; j <= op->nx; ++j) {
+          const double e = std::fabs(eig(op->xs, op->xd, op->xu, op->nx, j));
+          mn = std::min(mn, e); mx = std::max(mx, e);
+        }
+    } else {
+      for (int j = 1; j <= op->ny; ++j)
+        for (int i = 1; i <= op->nx; ++i) {
+          const double e = std::fabs(eig(op->xs, op->xd, op->xu, op->nx, i) + eig(op->ys, op->yd, op->yu, op->ny, j) +
+                                     op->shift);
+          mn = std::min(mn, e); mx = std::max(mx, e);
+        }
+    }
+    if (mx > 0.0 && mn <= 1e-13 * mx) return CNPINT_ESINGULAR;
+  }
   if (op->dim == 1 && !op->toeplitz) {
     for (int i = 0; i < op->nx; ++i)
       if (!std::isfinite(op->sub[i]) || !std::isfinite(op->diag[i]) || !std::isfinite(op->sup[i])) return CNPINT_EINVAL;

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(256)
     k_tridiag(const double2* __restrict__ what, double2* __restrict__ zhat, const double* __restrict__ lo,
               const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
               const double2* __restrict__ il2, const double2* __restrict__ tab, int m, int64_t W, int K, int G,
-              int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status) {
+              int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status,
+              const double2* __restrict__ lam1) {
   constexpr bool TOEP = MODE != MODE_VAR;
   constexpr bool FAST = MODE == MODE_FAST;
   constexpr int NCF = FAST ? 2 : 6;  // stored coefficients per merge
@@ -140,7 +141,13 @@ __global__ void __launch_bounds__(256)
   cp_async_wait<0>();
   __syncthreads();
   Seg sg;
-  if (act) {
+  // α = 1, k = N/2: λ2 = 0 (il2 = 0 from the host tables) — the system is λ1 z = w; uniform per system
+  const bool diag_only = act && il.x == 0.0 && il.y == 0.0;
+  if (diag_only) {
+    const double2 r = crecip(lam1[k]);
+    for (int i = p; i < m; i += P) D[sidx(i)] = cmul(D[sidx(i)], r);
+  }
+  if (act && !diag_only) {
     double2 dl[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) dl[j] = (j < len) ? cmul(D[sidx(i0 + j)], il) : make_double2(0.0, 0.0);
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(256)
   // ---------------- tree up: 5 warp levels
   double2* cw = coefw + warp * 31 * NCF;
   const double2* TT = T + L1S;  // fast-tree table
-  if (act) {
+  if (act && !diag_only) {
 #pragma unroll
     for (int lv = 1; lv <= 5; ++lv) {
       const int sft = 1 << (lv - 1);
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(256)
     xe = cmul(csub(cmul(t.fb, t.gd), cmul(t.ga, t.fd)), id);
   };
   if (G == 1) {
-    if (act && lane == 0) root(sg);
+    if (act && !diag_only && lane == 0) root(sg);
   } else {
     // ---------------- cross-warp levels (warp 0 of the system, lanes 0..G−1)
     if (lane == 0) {
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(256)
       if (!FAST) { r[0] = sg.fa; r[1] = sg.fb; r[2] = sg.fc; r[4] = sg.ga; r[5] = sg.gb; r[6] = sg.gc; }
     }
     named_sync(1 + g, 32 * G);
-    if (wg == 0 && act) {
+    if (wg == 0 && act && !diag_only) {
       Seg t = sg;
       if (lane < G) {
         const double2* r = segr + (g * G + lane) * 8;
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(256)
       xe = bnd[warp * 2 + 1];
     }
   }
-  if (act) {
+  if (act && !diag_only) {
     // ---------------- tree down: 5 warp levels
 #pragma unroll
     for (int lv = 5; lv >= 1; --lv) {
@@ -403,13 +410,20 @@ __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __res
                                 const double* __restrict__ lo, const double* __restrict__ di,
                                 const double* __restrict__ up, const double2* __restrict__ sk,
                                 const double2* __restrict__ il2, int m, int64_t W, double tau, int K,
-                                int* __restrict__ status) {
+                                int* __restrict__ status, const double2* __restrict__ lam1) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   const double2 s = sk[k], il = il2[k];
   double2 cp[64], dp[64];
   const double2* src = what + (int64_t)k * W;
+  double2* dst = zhat + (int64_t)k * W;
   bool ok = true;
+  if (il.x == 0.0 && il.y == 0.0) {  // α = 1, k = N/2: λ1 z = w
+    const double2 r = crecip(lam1[k]);
+    for (int i = 0; i < m; ++i) dst[i] = cmul(src[i], r);
+    for (int i = m; i < W; ++i) dst[i] = make_double2(0.0, 0.0);
+    return;
+  }
   for (int i = 0; i < m; ++i) {
     const double a = -tau * lo[i], c = -tau * up[i];
     const double2 b = make_double2(s.x - tau * di[i], s.y);
@@ -420,7 +434,6 @@ __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __res
     cp[i] = cscale(inv, c);
     dp[i] = (i == 0) ? cmul(d, inv) : cmul(crfms(d, a, dp[i - 1]), inv);
   }
-  double2* dst = zhat + (int64_t)k * W;
   double2 x = dp[m - 1];
   dst[m - 1] = x;
   for (int i = m - 2; i >= 0; --i) {
@@ -487,7 +500,7 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
                                t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
   k_tridiag<MODE, L><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
       what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS,
-      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status);
+      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1);
   return cudaGetLastError();
 }
 
@@ -501,7 +514,7 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
   cudaError_t e;
   if (t.small) {
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
-                                                            m, W, c->tau_p, K, c->d_status);
+                                                            m, W, c->tau_p, K, c->d_status, c->d_lam1);
     e = cudaGetLastError();
   } else if (!c->toeplitz) {
     e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, what, zhat)

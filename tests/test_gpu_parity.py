@@ -319,7 +319,7 @@ def test_invalid_arguments():
     with pytest.raises(CnpintError):
         Solver(24, 1.0, 0.1, spec)            # N not a power of two -> EUNSUPPORTED (workspace 0)
     with pytest.raises(CnpintError):
-        Solver(16, 1.0, 1.0, spec)            # alpha = 1 (P_1) out of scope
+        Solver(16, 1.0, 1.5, spec)            # alpha > 1
     with pytest.raises(CnpintError):
         Solver(16, -1.0, 0.1, spec)
     s = solver_for(w)
@@ -399,3 +399,51 @@ def test_time_dependent_full_c2t():
     u = s.empty()
     rep = s.gmres(problems.rhs(w, s), u, w.tol, w.restart)
     assert rep["converged"] and rel(s.to_host(u), aao.solve_sequential(w, op, b)) < 1e-8
+
+
+# ------------------------------------------------------------------------------ NEXT #2: P₁ (α = 1)
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "2d_small", "c1", "1d_N4096_C2"])
+def test_pinv_P1(name):
+    """α = 1 (the paper's block circulant P₁): the k = N/2 system degenerates to λ1 z = w."""
+    w = SMALL[name].with_(alpha=1.0)
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    for v in synth.random_vectors(w, 2, 31):
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12, name
+        assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+    assert s.device_status() == 0
+
+
+def test_gmres_P1_vs_P_alpha():
+    """The paper's comparison (Tables 1-4): with P₁ GMRES needs several times the iterations of P_α; the
+    GPU counts agree with the oracle's (±1) and both reach sequential CN."""
+    w = synth.scaled(synth.C1, 63, 64, restart=50)
+    its = {}
+    for a in (1.0, 0.01):
+        rep, orep = _gmres_case(w.with_(alpha=a), check_iterates=False)
+        its[a] = rep["iterations"]
+    assert its[1.0] > its[0.01] + 2, its
+
+
+def test_P1_singular_operator_rejected():
+    """Remark 3.2: P₁ is singular iff Ã is — a Toeplitz operator with an eigenvalue 0 is refused at
+    create with α = 1 (CNPINT_ESINGULAR) and accepted with α < 1."""
+    import math
+    from paper_2401_16113_b200.cnpint import ESINGULAR
+    m = 31
+    d = -2.0 * math.cos(math.pi / (m + 1))
+    spec = OperatorSpec(dim=1, nx=m, toeplitz=True, xs=1.0, xd=d, xu=1.0)
+    with pytest.raises(CnpintError) as ei:
+        Solver(16, 1.0, 1.0, spec)
+    assert ei.value.status == ESINGULAR
+    Solver(16, 1.0, 0.5, spec)
+    # 2D: shift chosen so that μ_11 = 0
+    n = 15
+    e1 = -2.0 + 2.0 * math.cos(math.pi / (n + 1))
+    spec2 = OperatorSpec(dim=2, nx=n, ny=n, xs=1.0, xd=-2.0, xu=1.0, ys=1.0, yd=-2.0, yu=1.0, shift=-2 * e1)
+    with pytest.raises(CnpintError) as ei:
+        Solver(16, 1.0, 1.0, spec2)
+    assert ei.value.status == ESINGULAR
