@@ -18,7 +18,8 @@ aao       𝓜u, P_α z by the block formulas (§3.2), sequential CN, dense 𝓜
 precond   λ tables (Eq. eigCx, FFT-consistent reading), DFT-matrix P_α⁻¹ (Eq. 3.2 + Remark 3.1),
           full-spectrum variant, 2D dense-DST fast diagonalisation, FFT-free fixed-point sweep,
           dense solve
-gmres     restarted right-preconditioned GMRES (MGS + Givens), §5 / PAPER.md:795
+gmres     restarted right-preconditioned GMRES (MGS + Givens), §5 / PAPER.md:795; left-preconditioned
+          GMRES (§4) and the Theorem 4.5 rate bound
 spectrum  dense eigenvalues of P_α⁻¹𝓜 and the closed forms of Lemma 3.1 / Theorem 3.1
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in

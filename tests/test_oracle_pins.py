@@ -627,3 +627,147 @@ def test_P1_needs_more_gmres_iterations():
         assert rep.converged and rel(u, aao.solve_sequential(wa, op, b)) < 1e-8
         its[a] = rep.iterations
     assert its[1.0] > its[0.01] + 2, its
+
+
+# ------------------------------------------------------------------ NEXT #4: left GMRES + Theorem 4.5
+# PAPER.md:576-590 (§4, Eq. sss2x) left-preconditioned GMRES, residual r_k = P⁻¹(b − 𝓜u^(k));
+# PAPER.md:663-718 (Eqs. 4.9, 4.11, 4.12) field-of-values bound; Theorem 4.5.
+
+def heat_workload(n, N, delta=0.25):
+    """Symmetric negative definite 1D operator (the hypothesis of Theorem 4.5): the
+    log-price Black–Scholes operator with r = σ²/2 has no convection term, L = (σ²/2)∂xx − r.
+    α = δ√(τ/T) = δ/√N."""
+    w = synth.scaled(synth.C1, n, N)
+    return w.with_(r=0.5 * w.sigma ** 2, alpha=delta / math.sqrt(N))
+
+
+def test_heat_workload_is_symmetric_nsd():
+    w = heat_workload(15, 16)
+    L = problem.build_operator(w).dense()
+    assert np.array_equal(L, L.T)
+    assert np.linalg.eigvalsh(L).max() < 0
+
+
+def test_gmres_left_identity_and_exact_preconditioner_one_iteration():
+    b = np.random.default_rng(0).standard_normal((4, 5))
+    u, rep = gmres.gmres_left(lambda x: x, lambda x: x, b, 1e-12, 10)
+    assert rep.iterations == 1 and rep.converged and rel(u, b) < 1e-14
+    w = small1d(15, 16)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    u, rep = gmres.gmres_left(lambda x: aao.apply_M(w, op, x), lambda x: aao.solve_sequential(w, op, x),
+                              b, 1e-12, 10)
+    assert rep.iterations == 1 and rep.converged
+    assert rel(u, aao.solve_sequential(w, op, b)) < 1e-12
+
+
+def test_gmres_left_minimal_residual_property_brute_force():
+    """Eq. sss2x: ‖r_k‖ = min_{x ∈ K_k(B, r0)} ‖r0 − Bx‖, B = P⁻¹𝓜, r0 = P⁻¹b — the Givens history
+    and the k-th iterate against numpy lstsq on an explicit Krylov basis (built from (B − I)^i r0,
+    which spans the same space and stays well conditioned when B ≈ I)."""
+    w = small1d(9, 8, 0.3)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    A = lambda x: aao.apply_M(w, op, x)
+    P = lambda x: precond.pinv_dft(w, op, x)
+    Bf = lambda x: P(A(x.reshape(b.shape))).reshape(-1)
+    r0 = P(b).reshape(-1)
+    for k in (1, 2, 3):
+        u, rep = gmres.gmres_left(A, P, b, 1e-15, 20, maxit=k)
+        K = [r0]
+        for _ in range(k - 1):
+            K.append(Bf(K[-1]) - K[-1])
+        Q, _ = np.linalg.qr(np.array(K).T)
+        BQ = np.array([Bf(Q[:, i]) for i in range(k)]).T
+        y, *_ = np.linalg.lstsq(BQ, r0, rcond=None)
+        rmin = np.linalg.norm(r0 - BQ @ y) / np.linalg.norm(r0)
+        assert abs(rep.history[k - 1] - rmin) <= 1e-9 * max(rmin, 1e-6)
+        assert rel(u, (Q @ y).reshape(b.shape)) < 1e-8
+        assert abs(rep.relres_prec - rmin) <= 1e-9 * max(rmin, 1e-6)
+
+
+def test_gmres_left_and_right_agree_with_dense_solve():
+    for w in (small1d(15, 16, 0.05), small1d(15, 16, 0.05, kind="price"), small2d(7, 8, 0.05)):
+        op = problem.build_operator(w)
+        b = problem.assemble_rhs(w, op)
+        A = lambda x: aao.apply_M(w, op, x)
+        P = lambda x: precond.pinv_dft(w, op, x)
+        ud = np.linalg.solve(aao.dense_M(w, op), b.reshape(-1)).reshape(b.shape)
+        ul, repl = gmres.gmres_left(A, P, b, 1e-11, 30)
+        ur, repr_ = gmres.gmres_right(A, P, b, 1e-11, 30)
+        assert repl.converged and repr_.converged
+        assert rel(ul, ud) < 1e-8 and rel(ur, ud) < 1e-8
+        assert abs(repl.iterations - repr_.iterations) <= 1
+        # relres_true is the unpreconditioned residual of the returned iterate
+        assert abs(repl.relres_true - np.linalg.norm(b - A(ul)) / np.linalg.norm(b)) < 1e-14
+
+
+def test_rate_bound_values():
+    """Theorem 4.5's rate [1 − (1 − 2δ)²]^{1/2} = 2√(δ(1 − δ)) (reading R27: the printed 2√δ(1 − δ)
+    is the algebra slip; SPEC.md:372's "δ = ¼ → 0.75" is that printed value): δ = ¼ → √3/2,
+    δ → 0 → 0, δ ≥ ½ violates the hypothesis."""
+    N, T = 64, 1.0
+    tau = T / N
+    d, rate = gmres.rate_bound(0.25 * math.sqrt(tau / T), tau, T)
+    assert abs(d - 0.25) < 1e-15 and abs(rate - math.sqrt(3) / 2) < 1e-15
+    assert abs(gmres.printed_rate(0.25) - 0.75) < 1e-15
+    for delta in (1e-8, 0.01, 0.1, 0.3, 0.49):
+        d, rate = gmres.rate_bound(delta / math.sqrt(N), tau, T)
+        exact = 2 * math.sqrt(delta * (1 - delta))
+        assert abs(rate - exact) <= 1e-15 / delta * exact     # 1 − (1 − 2δ)² cancels at small δ
+        assert gmres.printed_rate(delta) < rate                 # the printed value is stricter
+    assert gmres.rate_bound(1e-8 / 8, tau, T)[1] < 3e-4
+    for bad in (0.5, 0.7, 1.0 * math.sqrt(N)):
+        with pytest.raises(ValueError):
+            gmres.rate_bound(bad / math.sqrt(N), tau, T)
+    r = math.sqrt(3) / 2
+    chk = gmres.rate_bound_check([0.8, 0.7, 0.6], 0.25 / 8, tau, T)
+    assert chk["holds"] and abs(chk["worst"] - 0.7 / r ** 2) < 1e-14 and not chk["holds_printed"]
+    assert not gmres.rate_bound_check([0.8, 0.76], 0.25 / 8, tau, T)["holds"]   # 0.76 > 0.75
+
+
+def test_theorem_4_5_bound_chain_dense():
+    """SPEC.md:374 example: symmetric 1D heat, N = m = 32, α = ¼√(τ/T), full GMRES → the bound holds.
+    Checked link by link against dense matrices: ‖𝓜⁻¹𝓡‖ ≤ √N, Eq. 4.11
+    (‖P⁻¹𝓜 − I‖ ≤ α‖𝓜⁻¹𝓡‖/(1 − α‖𝓜⁻¹𝓡‖) and λ_min(H(P⁻¹𝓜)) > 0), the field-of-values bound Eq. 4.9
+    / 4.12 per step, and Theorem 4.5's [2√δ(1−δ)]^k on the GMRES history."""
+    w = heat_workload(31, 32)
+    op = problem.build_operator(w)
+    M = aao.dense_M(w, op)
+    P = aao.dense_P(w, op)
+    R = (M - P) / w.alpha                                  # P_α = 𝓜 − α𝓡
+    mr = np.linalg.norm(np.linalg.solve(M, R), 2)
+    assert mr <= math.sqrt(w.N) * (1 + 1e-12)
+    B = np.linalg.solve(P, M)
+    E = np.linalg.norm(B - np.eye(B.shape[0]), 2)
+    assert E <= w.alpha * mr / (1 - w.alpha * mr) * (1 + 1e-9)
+    Hs = 0.5 * (B + B.T)
+    nu = np.linalg.eigvalsh(Hs).min()
+    assert nu >= 1 - E - 1e-12 and nu > 0
+    fov_rate = math.sqrt(1 - (nu / np.linalg.norm(B, 2)) ** 2)           # Eq. 4.9
+    eq412 = math.sqrt(1 - (1 - 2 * w.alpha * mr) ** 2)                     # Eq. 4.12
+    assert fov_rate <= eq412 * (1 + 1e-9)
+    b = problem.assemble_rhs(w, op)
+    u, rep = gmres.gmres_left(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
+                              1e-13, 60)
+    assert rep.converged and rep.restarts == 0
+    for k, h in enumerate(rep.history, start=1):
+        assert h <= fov_rate ** k * (1 + 1e-9)
+    chk = gmres.rate_bound_check(rep.history, w.alpha, 1.0 / w.N, 1.0)
+    assert chk["holds"] and abs(chk["delta"] - 0.25) < 1e-14 and abs(chk["bound_rate"] - math.sqrt(3) / 2) < 1e-14
+
+
+def test_theorem_4_5_mesh_independent_counts():
+    """'mesh-independent linear convergence rate': with α = δ√(τ/T) the left GMRES
+    iteration count to 1e-10 stays flat under simultaneous refinement of space and time."""
+    its = []
+    for n, N in ((15, 16), (63, 64), (255, 256)):
+        w = heat_workload(n, N)
+        op = problem.build_operator(w)
+        b = problem.assemble_rhs(w, op)
+        u, rep = gmres.gmres_left(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
+                                  1e-10, 40)
+        assert rep.converged and rep.restarts == 0
+        assert gmres.rate_bound_check(rep.history, w.alpha, 1.0 / N, 1.0)["holds"]
+        its.append(rep.iterations)
+    assert max(its) - min(its) <= 1, its
