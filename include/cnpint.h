@@ -94,6 +94,8 @@ typedef struct {
   double seconds;      /* host wall time inside the call */
   double* history;     /* caller host array (may be NULL): estimate after every inner step */
   int history_cap;     /* capacity of history */
+  double relres_prec;  /* cnpint_gmres_left: ||P_α⁻¹(b − 𝓜u)|| / ||P_α⁻¹b|| at the last cycle end
+                        * (the residual of PAPER.md:578-579); cnpint_gmres: not written */
 } cnpint_gmres_report;
 
 /* Bytes of device workspace for a handle with these sizes (0 on invalid arguments).
@@ -156,6 +158,20 @@ cnpint_status cnpint_time_ifft(cnpint_ctx* ctx, const double* d_zhat, double* d_
  * maxit = j <= restart returns the j-th GMRES iterate) or an error.  rep may be NULL. */
 cnpint_status cnpint_gmres(cnpint_ctx* ctx, const double* d_b, double* d_u, double tol, int restart,
                            int maxit, cnpint_gmres_report* rep);
+
+/* Left-preconditioned restarted GMRES(restart) on P_α⁻¹𝓜u = P_α⁻¹b, zero initial guess: the
+ * variant the paper's convergence analysis is stated for (§4; Theorem 4.5,
+ * PAPER.md:771-784).  r_0 = P_α⁻¹b; each inner step forms
+ * w = P_α⁻¹(𝓜 v_j) (K1 then the P_α⁻¹ kernels, the basis scale folded into the Γ-scaling) and
+ * orthogonalises it with the same CGS2 kernels as cnpint_gmres; the cycle end is u += V y (no
+ * P_α⁻¹), then r = P_α⁻¹(b − 𝓜u) starts the next cycle.
+ * history[k−1] = Givens estimate of ||r_k|| / ||r_0||, r_k = P_α⁻¹(b − 𝓜u^(k)) (R28).
+ * Converged iff ||P_α⁻¹(b − 𝓜u)|| / ||P_α⁻¹b|| <= tol at a cycle end (rep->relres_prec);
+ * rep->relres_true is the unpreconditioned ||b − 𝓜u|| / ||b||.  Arguments, workspace, errors and
+ * the maxit semantics as cnpint_gmres (the first preconditioned direction slot serves as the
+ * 𝓜v_j temporary). */
+cnpint_status cnpint_gmres_left(cnpint_ctx* ctx, const double* d_b, double* d_u, double tol, int restart,
+                                int maxit, cnpint_gmres_report* rep);
 
 /* Host-buffer variants (end-to-end: H2D copy of the input, the device computation, D2H copy of
  * the result, all on the handle's stream; synchronises).  Host layout: packed (see top). */

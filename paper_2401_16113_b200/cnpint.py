@@ -27,7 +27,7 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_apply_Pinv", "cnpint_time_fft", "cnpint_shifted_solve", "cnpint_time_ifft", "cnpint_gmres",
            "cnpint_apply_Pinv_host", "cnpint_apply_A_host", "cnpint_gmres_host", "cnpint_device_status",
            "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug", "cnpint_profile_enable",
-           "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence"]
+           "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence", "cnpint_gmres_left"]
 
 
 class CnpintError(RuntimeError):
@@ -46,7 +46,7 @@ class Operator(C.Structure):
 class GmresReport(C.Structure):
     _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("converged", C.c_int),
                 ("relres_est", C.c_double), ("relres_true", C.c_double), ("seconds", C.c_double),
-                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int), ("relres_prec", C.c_double)]
 
 
 _lib = None
@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
         "cnpint_time_fft": (C.c_int, [vp, vp, vp]), "cnpint_shifted_solve": (C.c_int, [vp, vp, vp]),
         "cnpint_time_ifft": (C.c_int, [vp, vp, vp]),
         "cnpint_gmres": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(GmresReport)]),
+        "cnpint_gmres_left": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(GmresReport)]),
         "cnpint_apply_Pinv_host": (C.c_int, [vp, dp, dp]), "cnpint_apply_A_host": (C.c_int, [vp, dp, dp]),
         "cnpint_gmres_host": (C.c_int, [vp, dp, dp, C.c_double, C.c_int, C.c_int, C.POINTER(GmresReport)]),
         "cnpint_device_status": (C.c_int, [vp]), "cnpint_launch_count": (i64, [vp]),
@@ -222,17 +223,25 @@ class Solver:
         self._sync_stream()
         self._check(self.lib.cnpint_time_ifft(self.h, C.c_void_p(_ptr(zhat)), C.c_void_p(_ptr(z))), "time_ifft")
 
-    def gmres(self, b, u, tol: float, restart: int, maxit: int = 1000, history_cap: int = 1000):
+    def gmres(self, b, u, tol: float, restart: int, maxit: int = 1000, history_cap: int = 1000,
+              side: str = "right"):
+        """cnpint_gmres (side="right", the paper's §5 solver) or cnpint_gmres_left (side="left", the
+        §4 / Theorem 4.5 setting; the report adds relres_prec = ||P⁻¹(b − 𝓜u)||/||P⁻¹b||)."""
+        if side not in ("right", "left"):
+            raise ValueError(f"side must be 'right' or 'left', got {side!r}")
         self._sync_stream()
         hist = (C.c_double * history_cap)()
-        rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, C.cast(hist, C.POINTER(C.c_double)), history_cap)
-        st = self.lib.cnpint_gmres(self.h, C.c_void_p(_ptr(b)), C.c_void_p(_ptr(u)), tol, restart, maxit,
-                                   C.byref(rep))
+        rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, C.cast(hist, C.POINTER(C.c_double)), history_cap, float("nan"))
+        fn = self.lib.cnpint_gmres if side == "right" else self.lib.cnpint_gmres_left
+        st = fn(self.h, C.c_void_p(_ptr(b)), C.c_void_p(_ptr(u)), tol, restart, maxit, C.byref(rep))
         if st not in (OK, ENOCONV):
-            self._check(st, "gmres")
-        return {"status": STATUS[st], "iterations": rep.iterations, "restarts": rep.restarts,
-                "converged": bool(rep.converged), "relres_est": rep.relres_est, "relres_true": rep.relres_true,
-                "seconds": rep.seconds, "history": [hist[i] for i in range(min(rep.iterations, history_cap))]}
+            self._check(st, "gmres" if side == "right" else "gmres_left")
+        out = {"status": STATUS[st], "iterations": rep.iterations, "restarts": rep.restarts,
+               "converged": bool(rep.converged), "relres_est": rep.relres_est, "relres_true": rep.relres_true,
+               "seconds": rep.seconds, "history": [hist[i] for i in range(min(rep.iterations, history_cap))]}
+        if side == "left":
+            out["relres_prec"] = rep.relres_prec
+        return out
 
     # host-buffer (end-to-end) variants: packed numpy arrays
     def apply_Pinv_host(self, v: np.ndarray, z: Optional[np.ndarray] = None) -> np.ndarray:
@@ -255,7 +264,7 @@ class Solver:
         b = np.ascontiguousarray(b, dtype=np.float64)
         u = np.empty_like(b) if u is None else u
         self._sync_stream()
-        rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, None, 0)
+        rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, None, 0, float("nan"))
         st = self.lib.cnpint_gmres_host(self.h, b.ctypes.data_as(C.POINTER(C.c_double)),
                                         u.ctypes.data_as(C.POINTER(C.c_double)), tol, restart, maxit, C.byref(rep))
         if st not in (OK, ENOCONV):

@@ -671,8 +671,7 @@ cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
 }
 
 // ------------------------------------------------------------------------------ GMRES
-cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
-                           cnpint_gmres_report* rep) {
+static cnpint_status gmres_args(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit) {
   if (!c) return CNPINT_EINVAL;
   if (check_vec(c, d_b, "b") || check_vec(c, d_u, "u")) return CNPINT_EINVAL;
   if (d_b == d_u) { seterr(c, "gmres: u aliases b"); return CNPINT_EINVAL; }
@@ -681,6 +680,43 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     seterr(c, "gmres: need 0 < tol < 1, 1 <= restart <= restart_max, maxit >= 1");
     return CNPINT_EINVAL;
   }
+  return CNPINT_OK;
+}
+
+// CGS2 of w (already in its basis slot) against Ṽ_0..Ṽ_{nv−1}: c1 = Ṽᵀw (unless the producer fused
+// it: have_c1), w −= Ṽ(s²c1) with c2 = Ṽᵀw fused, w −= Ṽ(s²c2) with ||w||² fused into scal[2].
+// More than CNP_MAX_DOT vectors: groups of CNP_MAX_DOT (dots, update, dots, update, norm).
+static cnpint_status cgs2(cnpint_ctx* c, double* const* V, int nv, double* w, bool have_c1) {
+  if (nv <= CNP_MAX_DOT) {
+    if (!have_c1) CK(launch_dots(c, V, nv, w, c->d_part, c->d_c1));
+    CK(launch_update(c, V, nv, c->d_c1, 0, w, w, 1, 0, c->d_part, c->d_c2));
+    CK(launch_update(c, V, nv, c->d_c2, 0, w, w, 0, 1, c->d_part, c->d_scal + 2));
+    return CNPINT_OK;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    double* cd = pass == 0 ? c->d_c1 : c->d_c2;
+    for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
+      int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
+      CK(launch_dots(c, V + g0, ng, w, c->d_part, cd + g0));
+    }
+    for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
+      int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
+      // coefficients cd[g0..] with scales scl[g0..]: shift the scale pointer via a temporary swap
+      double* saved = c->d_scl;
+      c->d_scl = saved + g0;
+      const bool last = pass == 1 && g0 + ng == nv;
+      cudaError_t e = launch_update(c, V + g0, ng, cd + g0, 0, w, w, 0, last ? 1 : 0, c->d_part,
+                                    last ? c->d_scal + 2 : nullptr);
+      c->d_scl = saved;
+      CK(e);
+    }
+  }
+  return CNPINT_OK;
+}
+
+cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
+                           cnpint_gmres_report* rep) {
+  if (cnpint_status a = gmres_args(c, d_b, d_u, tol, restart, maxit)) return a;
   auto t0 = std::chrono::steady_clock::now();
   const int64_t vec = c->vec;
   double* h = c->h_pinned;
@@ -720,30 +756,10 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       if (nv <= CNP_MAX_DOT) {
         // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw)
         CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
-        CK(launch_update(c, V.data(), nv, c->d_c1, 0, w, w, 1, 0, c->d_part, c->d_c2));
-        CK(launch_update(c, V.data(), nv, c->d_c2, 0, w, w, 0, 1, c->d_part, c->d_scal + 2));
       } else {
         CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
-        // groups of CNP_MAX_DOT: dots, update (no fusion), dots, update, norm
-        for (int pass = 0; pass < 2; ++pass) {
-          double* cd = pass == 0 ? c->d_c1 : c->d_c2;
-          for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
-            int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
-            CK(launch_dots(c, V.data() + g0, ng, w, c->d_part, cd + g0));
-          }
-          for (int g0 = 0; g0 < nv; g0 += CNP_MAX_DOT) {
-            int ng = nv - g0 < CNP_MAX_DOT ? nv - g0 : CNP_MAX_DOT;
-            // coefficients cd[g0..] with scales scl[g0..]: shift the scale pointer via a temporary swap
-            double* saved = c->d_scl;
-            c->d_scl = saved + g0;
-            const bool last = pass == 1 && g0 + ng == nv;
-            cudaError_t e = launch_update(c, V.data() + g0, ng, cd + g0, 0, w, w, 0, last ? 1 : 0, c->d_part,
-                                          last ? c->d_scal + 2 : nullptr);
-            c->d_scl = saved;
-            CK(e);
-          }
-        }
       }
+      if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
       CK(launch_small(c, 1, j, 0));
       CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
@@ -794,6 +810,104 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   }
   if (dst != CNPINT_OK) return dst;
   if (result == CNPINT_ENOCONV) seterr(c, "gmres: maxit reached (relres %.3e > tol %.3e)", relres_true, tol);
+  return result;
+}
+
+// Left preconditioning (NEXT #4).  scal[0] = ||P⁻¹b|| (the r_0 norm the estimates
+// are relative to), scal[6] = ||b − 𝓜u||² of the last cycle end, scal[7] = ||b||².
+cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
+                                cnpint_gmres_report* rep) {
+  if (cnpint_status a = gmres_args(c, d_b, d_u, tol, restart, maxit)) return a;
+  auto t0 = std::chrono::steady_clock::now();
+  const int64_t vec = c->vec;
+  double* h = c->h_pinned;
+  std::vector<double*> V(restart + 1);
+  for (int i = 0; i <= restart; ++i) V[i] = c->d_V + (size_t)i * vec;
+  double* tmp = c->d_Z;  // 𝓜v_j and b − 𝓜u (the preconditioned-direction slots are unused here)
+  int its = 0, cycles = 0, converged = 0;
+  double est = 1.0, relres_true = 1.0, relres_prec = 1.0;
+  cnpint_status result = CNPINT_OK;
+  CK(cudaMemsetAsync(c->d_scal, 0, 16 * sizeof(double), c->stream));
+  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 7));
+  // r_0 = P⁻¹b (x0 = 0), β = ||r_0||
+  if (cnpint_status st = pinv_dev(c, d_b, nullptr, V[0], 0)) return st;
+  CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
+  CK(launch_small(c, 0, 0, 1));
+  CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const double bnorm = std::sqrt(h[7]);
+  if (h[7] == 0.0) {  // b = 0 ⇒ u = 0
+    CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (rep) {
+      rep->iterations = 0; rep->restarts = 0; rep->converged = 1;
+      rep->relres_est = 0; rep->relres_true = 0; rep->relres_prec = 0;
+    }
+    return CNPINT_OK;
+  }
+  if (!std::isfinite(h[0]) || !std::isfinite(bnorm) || h[0] == 0.0) {
+    if (cnpint_status dst = cnpint_device_status(c)) return dst;
+    seterr(c, "gmres_left: ||P^-1 b|| = %g (b != 0)", h[0]);
+    return CNPINT_EBREAKDOWN;
+  }
+  while (true) {
+    int jdone = 0;
+    bool stop_inner = false;
+    for (int j = 0; j < restart && !stop_inner; ++j) {
+      // w = P⁻¹(𝓜 v_j), v_j = s_j Ṽ_j: 𝓜Ṽ_j, then s_j folded into the Γ-scaling of P⁻¹
+      CK(launch_matvec(c, V[j], tmp, 0, nullptr, nullptr));
+      double* w = V[j + 1];
+      if (cnpint_status st = pinv_dev(c, tmp, c->d_scl + j, w, 0)) return st;
+      if (cnpint_status cs = cgs2(c, V.data(), j + 1, w, false)) return cs;
+      CK(launch_small(c, 1, j, 0));
+      CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      ++its;
+      jdone = j + 1;
+      est = h[1];
+      if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
+      if (h[3] != 0.0) {
+        seterr(c, "gmres_left: non-finite scalar in the Arnoldi process");
+        return CNPINT_EBREAKDOWN;
+      }
+      if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
+    }
+    // cycle end: y = H⁻¹g, u += V y = Σ (y_i s_i) Ṽ_i  (no P⁻¹ with left preconditioning)
+    CK(launch_small(c, 2, jdone, 0));
+    for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
+      int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
+      const bool fresh = cycles == 0 && g0 == 0;
+      CK(launch_update(c, V.data() + g0, ng, c->d_coef + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part,
+                       nullptr));
+    }
+    // b − 𝓜u (its norm²: the unpreconditioned residual), r = P⁻¹(b − 𝓜u) → Ṽ_0 of the next cycle
+    CK(launch_matvec(c, d_u, tmp, 2, d_b, c->d_part, c->d_scal + 6));
+    if (cnpint_status st = pinv_dev(c, tmp, nullptr, V[0], 0)) return st;
+    CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
+    CK(launch_small(c, 0, 0, 0));
+    CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    relres_prec = h[4];
+    relres_true = std::sqrt(h[6]) / bnorm;
+    ++cycles;
+    if (relres_prec <= tol) { converged = 1; break; }
+    if (its >= maxit) { result = CNPINT_ENOCONV; break; }
+    if (!std::isfinite(relres_prec)) { seterr(c, "gmres_left: residual not finite"); result = CNPINT_EBREAKDOWN; break; }
+  }
+  cnpint_status dst = cnpint_device_status(c);
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->iterations = its;
+    rep->restarts = cycles - 1;
+    rep->converged = converged;
+    rep->relres_est = est;
+    rep->relres_true = relres_true;
+    rep->relres_prec = relres_prec;
+    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+  }
+  if (dst != CNPINT_OK) return dst;
+  if (result == CNPINT_ENOCONV)
+    seterr(c, "gmres_left: maxit reached (preconditioned relres %.3e > tol %.3e)", relres_prec, tol);
   return result;
 }
 

@@ -95,6 +95,17 @@ C5_SIZES = [(n, N) for n in (127, 255, 511) for N in (256, 1024)]
 C1T = C1.with_(name="c1t", dt_rate=0.5, note="NEXT #1: c1 operator with d(t) = exp(-t/2)")
 C2T = C2.with_(name="c2t", dt_rate=0.5, note="NEXT #1: c2 operator with d(t) = exp(-t/2)")
 
+def heat(n: int, N: int, delta: float = 0.25, T: float = 1.0) -> Workload:
+    """SURVEY.md §8(f) NEXT #4 (Theorem 4.5; SPEC.md:374's "symmetric 1D heat"):
+    the c1 log-price operator with r = σ²/2, which removes the convection term so L = (σ²/2)∂xx − r is
+    symmetric negative definite (the theorem's hypothesis), and Theorem 4.5's
+    α = δ√(τ/T) with τ = T/N.  Parameters only."""
+    tau = T / N
+    return C1.with_(name=f"heat_n{n}_N{N}_d{delta}", n=n, N=N, T=T, r=0.5 * C1.sigma ** 2,
+                    alpha=delta * math.sqrt(tau / T), restart=40,
+                    note="NEXT #4: symmetric heat-type operator, alpha = delta*sqrt(tau/T)")
+
+
 WORKLOADS = {w.name: w for w in (C1, C2, C3, C4, C1T, C2T)}
 for _n, _N in C5_SIZES:
     WORKLOADS[f"c5_n{_n}_N{_N}"] = c5(_n, _N)

@@ -75,3 +75,27 @@ def test_product_path_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", txt, re.M), f
                 assert "oracle/" not in txt.replace("``oracle/``", ""), f
+
+
+def test_theorem_4_5_host_check_matches_oracle():
+    """paper_2401_16113_b200.theory (host logic of NEXT #4) against the oracle's rate_bound_check on
+    seeded histories, δ ∈ (0, ½), and the δ ≥ ½ refusal."""
+    import math
+    import numpy as np
+    from oracle import gmres as og
+    from paper_2401_16113_b200 import theory
+    rng = np.random.default_rng(7)
+    for N in (16, 256, 4096):
+        for delta in (0.01, 0.25, 0.45):
+            a = theory.alpha_for_delta(delta, N)
+            d, r = theory.theorem_4_5_rate(a, N)
+            do, ro = og.rate_bound(a, 1.0 / N, 1.0)
+            assert abs(d - do) < 1e-14 and abs(r - ro) < 1e-14 * max(1.0, 1e-2 / delta)
+            for _ in range(5):
+                hist = list(np.cumprod(rng.uniform(0.3, 1.0, 6)) * r ** 0.5)
+                c1, c2 = theory.rate_bound_check(hist, a, N), og.rate_bound_check(hist, a, 1.0 / N, 1.0)
+                assert c1["holds"] == c2["holds"] and c1["holds_printed"] == c2["holds_printed"]
+                assert abs(c1["worst"] - c2["worst"]) <= 1e-12 * c2["worst"]
+    import pytest
+    with pytest.raises(ValueError):
+        theory.theorem_4_5_rate(0.5 / math.sqrt(64), 64)

@@ -447,3 +447,102 @@ def test_P1_singular_operator_rejected():
     with pytest.raises(CnpintError) as ei:
         Solver(16, 1.0, 1.0, spec2)
     assert ei.value.status == ESINGULAR
+
+
+# ------------------------------------------------------------------------------ NEXT #4: left GMRES
+# PAPER.md:576-590 (§4) left-preconditioned GMRES on P⁻¹𝓜u = P⁻¹b; Theorem 4.5.
+def _gmres_left_case(w, check_iterates=True):
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    s = solver_for(w, restart_max=w.restart)
+    bd = problems.rhs(w, s)
+    u = s.empty()
+    rep = s.gmres(bd, u, w.tol, w.restart, side="left")
+    A = lambda x: aao.apply_M(w, op, x)
+    P = lambda x: precond.pinv_dft(w, op, x)
+    uo, orep = ogmres.gmres_left(A, P, b, w.tol, w.restart)
+    assert rep["converged"] and rep["relres_prec"] <= w.tol, rep
+    assert abs(rep["iterations"] - orep.iterations) <= 1, (rep["iterations"], orep.iterations)
+    ug = s.to_host(u)
+    assert rel(ug, aao.solve_sequential(w, op, b)) < 1e-8
+    assert abs(rep["relres_true"] - np.linalg.norm(b - A(ug)) / np.linalg.norm(b)) < 1e-9
+    # the Givens history ‖r_k‖/‖r_0‖ agrees with the oracle's while it is well above rounding
+    for hg, ho in zip(rep["history"], orep.history):
+        if ho > 1e-8:
+            assert abs(hg - ho) <= 1e-6 * ho, (rep["history"], orep.history)
+    if check_iterates:
+        for j in range(1, min(rep["iterations"], orep.iterations) + 1):
+            uj = s.empty()
+            s.gmres(bd, uj, w.tol, w.restart, maxit=j, side="left")
+            uoj, _ = ogmres.gmres_left(A, P, b, w.tol, w.restart, maxit=j)
+            assert rel(s.to_host(uj), uoj) < 1e-9, j
+    return rep, orep
+
+
+@pytest.mark.parametrize("name", ["1d_small", "1d_price", "2d_small", "1d_tv", "c1"])
+def test_gmres_left_vs_oracle(name):
+    w = SMALL[name].with_(restart=40)
+    _gmres_left_case(w, check_iterates=name != "c1")
+
+
+def test_gmres_left_restart_cycles_and_zero_rhs():
+    w = synth.scaled(synth.C1, 63, 64, alpha=0.5, restart=2)
+    op = problem.build_operator(w)
+    s = solver_for(w, restart_max=2)
+    u = s.empty()
+    rep = s.gmres(problems.rhs(w, s), u, 1e-10, 2, maxit=200, side="left")
+    assert rep["converged"] and rep["restarts"] >= 1 and rep["relres_prec"] <= 1e-10
+    assert rel(s.to_host(u), aao.solve_sequential(w, op, problem.assemble_rhs(w, op))) < 1e-8
+    z = s.empty()
+    rep0 = s.gmres(s.empty(), z, 1e-10, 2, side="left")
+    assert rep0["iterations"] == 0 and float(z.abs().max()) == 0.0
+    with pytest.raises(ValueError):
+        s.gmres(s.empty(), z, 1e-10, 2, side="middle")
+
+
+def test_gmres_left_full_c2():
+    """c2 size (m = 4095, N = 4096, α = 0.01): left GMRES reaches sequential CN; its count is the right
+    solver's ±1."""
+    w = synth.C2
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    s = solver_for(w, restart_max=w.restart)
+    bd = problems.rhs(w, s)
+    ul, ur = s.empty(), s.empty()
+    repl = s.gmres(bd, ul, w.tol, w.restart, side="left")
+    repr_ = s.gmres(bd, ur, w.tol, w.restart)
+    assert repl["converged"] and abs(repl["iterations"] - repr_["iterations"]) <= 1
+    assert rel(s.to_host(ul), aao.solve_sequential(w, op, b)) < 1e-8
+
+
+@pytest.mark.parametrize("delta", [0.1, 0.25, 0.45])
+def test_theorem_4_5_on_gpu_meshes(delta):
+    """Theorem 4.5 on GPU-scale meshes: symmetric heat operator, α = δ√(τ/T), N ∈ {256, 1024, 4096,
+    16384} with m = min(N − 1, 4095) (the 1D Toeplitz limit).  Every left-GMRES residual ratio stays under the proved bound (2√(δ(1−δ)))^k
+    (reading R27), the iteration count does not grow under refinement, and at the smallest mesh the history
+    matches the oracle's."""
+    from paper_2401_16113_b200 import theory
+    its = {}
+    for N in (256, 1024, 4096, 16384):
+        w = synth.heat(min(N - 1, 4095), N, delta).with_(tol=1e-12)
+        s = solver_for(w, restart_max=w.restart)
+        u = s.empty()
+        # seeded N(0,1) rhs: every spatial mode excited (the manufactured rhs is nearly one eigenmode)
+        bh = synth.random_vectors(w, 1, 5)[0]
+        rep = s.gmres(s.to_device(bh), u, w.tol, w.restart, side="left")
+        assert rep["converged"] and rep["restarts"] == 0, (N, rep)
+        chk = theory.rate_bound_check(rep["history"], w.alpha, N, w.T)
+        assert chk["holds"] and abs(chk["delta"] - delta) < 1e-12, (N, chk, rep["history"])
+        its[N] = rep["iterations"]
+        if N == 256:
+            op = problem.build_operator(w)
+            _, orep = ogmres.gmres_left(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x),
+                                        bh, w.tol, w.restart)
+            assert abs(orep.iterations - rep["iterations"]) <= 1
+            for hg, ho in zip(rep["history"], orep.history):
+                if ho > 1e-9:
+                    assert abs(hg - ho) <= 1e-6 * ho
+        del s, u
+        torch.cuda.empty_cache()
+    # mesh independent: refinement never increases the count (α = δ/√N shrinks, so it can decrease)
+    assert all(its[N] <= its[256] for N in its) and max(its.values()) <= 8, its

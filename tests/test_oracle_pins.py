@@ -634,11 +634,9 @@ def test_P1_needs_more_gmres_iterations():
 # PAPER.md:663-718 (Eqs. 4.9, 4.11, 4.12) field-of-values bound; Theorem 4.5.
 
 def heat_workload(n, N, delta=0.25):
-    """Symmetric negative definite 1D operator (the hypothesis of Theorem 4.5): the
-    log-price Black–Scholes operator with r = σ²/2 has no convection term, L = (σ²/2)∂xx − r.
-    α = δ√(τ/T) = δ/√N."""
-    w = synth.scaled(synth.C1, n, N)
-    return w.with_(r=0.5 * w.sigma ** 2, alpha=delta / math.sqrt(N))
+    """Symmetric negative definite 1D operator (the hypothesis of Theorem 4.5), with
+    α = δ√(τ/T) = δ/√N: synth.heat (c1 operator with r = σ²/2)."""
+    return synth.heat(n, N, delta)
 
 
 def test_heat_workload_is_symmetric_nsd():
@@ -759,15 +757,16 @@ def test_theorem_4_5_bound_chain_dense():
 
 def test_theorem_4_5_mesh_independent_counts():
     """'mesh-independent linear convergence rate': with α = δ√(τ/T) the left GMRES
-    iteration count to 1e-10 stays flat under simultaneous refinement of space and time."""
+    iteration count to 1e-10 does not grow under simultaneous refinement of space and time."""
     its = []
     for n, N in ((15, 16), (63, 64), (255, 256)):
         w = heat_workload(n, N)
         op = problem.build_operator(w)
-        b = problem.assemble_rhs(w, op)
+        b = synth.random_vectors(w, 1, 5)[0]     # every spatial mode excited (the manufactured rhs is
+        #                                          close to one eigenmode and converges in 2 steps)
         u, rep = gmres.gmres_left(lambda x: aao.apply_M(w, op, x), lambda x: precond.pinv_dft(w, op, x), b,
                                   1e-10, 40)
         assert rep.converged and rep.restarts == 0
         assert gmres.rate_bound_check(rep.history, w.alpha, 1.0 / N, 1.0)["holds"]
         its.append(rep.iterations)
-    assert max(its) - min(its) <= 1, its
+    assert its == sorted(its, reverse=True) and max(its) <= 8, its     # refinement never adds iterations
