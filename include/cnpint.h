@@ -72,7 +72,8 @@ typedef enum {
  *       Requires xs*xu > 0 and ys*yu > 0 (diagonal similarity to a symmetric Toeplitz matrix,
  *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two <= 1024.
  *   1D sizes: 2 <= nx <= 4096 (Toeplitz) or 2048 (variable rows).  N: power of two, 2..65536
- *   (time-axis FFT on thread-block clusters up to N = 16384, one column per CTA beyond). */
+ *   (1D time-axis FFT: thread-block clusters for N < 2048, the four-step L2-resident kernel for
+ *   N >= 2048); 2D: N <= 16384 (cluster / one-column time pass). */
 typedef struct {
   int dim;
   int nx, ny;
@@ -103,7 +104,7 @@ typedef struct {
  * a handle for apply_A / apply_P / apply_Pinv only (cnpint_gmres then returns EINVAL). */
 size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max);
 
-/* Create a handle.  N: time steps, power of two, 2 <= N <= 65536.  T > 0: horizon (τ = T/N).
+/* Create a handle.  N: time steps, power of two, 2 <= N <= 65536 (1D; 2D: N <= 16384).  T > 0: horizon (τ = T/N).
  * alpha in (0, 1]: the α of C1^(α), C2^(α).  α = 1 is the block circulant P_1 of
  * the paper's comparison (NEXT #2): its k = N/2 shifted system degenerates to λ1 z = w, and P_1 is
  * singular iff Ã is (Remark 3.2) — for Toeplitz / 2D operators create checks the

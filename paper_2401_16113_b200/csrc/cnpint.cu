@@ -72,7 +72,7 @@ size_t up_align(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 
 struct Layout {
-  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, tmp1, tmp2, tmp3, io1, io2, io3;
+  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
   size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
   size_t total;
@@ -102,6 +102,7 @@ const char* check_op(int N, const cnpint_operator* op, int* unsupported) {
       return "2D requires nx+1 and ny+1 powers of two (DST-I via FFT)";
     }
     if (op->nx + 1 > 1024 || op->ny + 1 > 1024) { *unsupported = 1; return "2D n+1 > 1024 unsupported"; }
+    if (N > 16384) { *unsupported = 1; return "2D needs N <= 16384 (time pass on chip)"; }
     if (!(op->xs * op->xu > 0.0) || !(op->ys * op->yu > 0.0))
       return "2D requires xs*xu > 0 and ys*yu > 0 (diagonal symmetrisation)";
   }
@@ -133,6 +134,8 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   }
   L.tables_end = off;
   L.spec = op->dim == 1 ? take((size_t)(H + 1) * ld * 16) : take(16);
+  L.fsy = take(fstep_y_bytes(op->dim, N, ld));
+  L.fscnt = take(op->dim == 1 && N >= 2048 ? (size_t)(fstep_nxb(N, ld) + 1) * 4 : 4);
   L.tmp1 = take(vec * 8); L.tmp2 = take(vec * 8); L.tmp3 = take(vec * 8);
   L.io1 = take(vec * 8); L.io2 = take(vec * 8); L.io3 = take(vec * 8);
   if (restart_max >= 1) {
@@ -458,6 +461,10 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_sk = (double2*)(w + L.sk); c->d_il2 = (double2*)(w + L.il2);
   c->d_tritab = (double2*)(w + L.tri);
   c->d_spec = (double2*)(w + L.spec);
+  c->d_fsY = fstep_y_bytes(op->dim, N, c->ld) ? (double*)(w + L.fsy) : nullptr;
+  c->d_fscnt = (unsigned*)(w + L.fscnt);
+  c->fs_cnt = 0;
+  c->fs_tick = 0;
   c->d_tmp1 = (double*)(w + L.tmp1); c->d_tmp2 = (double*)(w + L.tmp2); c->d_tmp3 = (double*)(w + L.tmp3);
   c->d_io1 = (double*)(w + L.io1); c->d_io2 = (double*)(w + L.io2); c->d_io3 = (double*)(w + L.io3);
   if (op->dim == 2) {

@@ -58,6 +58,10 @@ struct cnpint_ctx {
   double2* d_il2;      // [H+1] 1/λ2_k
   double2* d_tritab;   // [H+1][tabstride] Toeplitz chunk tables of K3 (1D Toeplitz only)
   double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
+  double* d_fsY;       // four-step FFT intermediate (1D, N >= 2048; k_fstep.cu), else null
+  unsigned* d_fscnt;   // [nxb] per-block pass-A counters, then the work ticket (monotonic)
+  unsigned fs_cnt;     // host mirror: Σ pass-A items per block over all launches so far
+  unsigned fs_tick;    // host mirror: tickets consumed so far
   double* d_tmp1;      // [vec] scratch vectors
   double* d_tmp2;
   double* d_tmp3;
@@ -103,6 +107,11 @@ struct DotPtrs {
   const double* p[CNP_MAX_DOT];
 };
 // y = 𝓜u fused with the first CGS pass: out[i] = Ṽ_iᵀ y, i < nv <= CNP_MAX_DOT (deterministic fold)
+bool fstep_ok(const cnpint_ctx* c);
+size_t fstep_y_bytes(int dim, int N, int64_t ld);
+int fstep_nxb(int N, int64_t ld);
+cudaError_t launch_fstep_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
+cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
                                double* out);
 // host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed

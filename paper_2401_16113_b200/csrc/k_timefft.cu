@@ -216,13 +216,16 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
   return cudaGetLastError();
 }
 
-// N <= 16384 goes to the cluster kernels of k_tfft.cu; larger N stays here (one column per CTA,
-// even/odd time packing).  debug bit 8 forces this path (cross-check in the parity tests).
+// 1D with N >= 2048: four-step kernel of k_fstep.cu (debug bit 16 opts out); other N <= 16384: the
+// cluster kernels of k_tfft.cu; larger N (2D) stays here (one column per CTA, even/odd time
+// packing).  debug bit 8 forces this path (cross-check in the parity tests).
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what) {
+  if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_fwd(c, v, vscale, what);
   if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_fwd(c, v, vscale, what);
   return run_fft<0>(c, v, nullptr, nullptr, what, vscale, 0);
 }
 cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate) {
+  if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_inv(c, zhat, z, accumulate);
   if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_inv(c, zhat, z, accumulate);
   return run_fft<1>(c, nullptr, zhat, z, nullptr, nullptr, accumulate);
 }

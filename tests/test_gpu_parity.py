@@ -44,6 +44,10 @@ SMALL = {
     "1d_N4096_C2": synth.scaled(synth.C1, 65, 4096, alpha=0.01),
     "1d_N8192_C8": synth.scaled(synth.C3, 37, 8192, alpha=0.01, T=5.0),
     "1d_N16384_C8": synth.scaled(synth.C3, 9, 16384, alpha=0.1, T=5.0),
+    # four-step time FFT (k_fstep.cu, 1D N >= 2048): a ragged last column block, and N beyond 16384
+    "1d_N2048_ragged": synth.scaled(synth.C1, 201, 2048, alpha=0.01),
+    "1d_N32768": synth.scaled(synth.C3, 13, 32768, alpha=0.01, T=5.0),
+    "1d_N65536": synth.scaled(synth.C1, 5, 65536, alpha=0.1),
     "2d_N1024_C2": synth.scaled(synth.C4, 15, 1024, alpha=0.01),
     "2d_n63_N2048": synth.scaled(synth.C4, 63, 2048, alpha=0.01),
     # NEXT #1: time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8)
@@ -105,9 +109,16 @@ def test_pinv_small(name):
         z = s.empty()
         s.apply_Pinv(s.to_device(v), z)
         zg = s.to_host(z)
-        zo = precond.pinv_dft(w, op, v)
-        assert rel(zg, zo) < 1e-12, name
         assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+        if w.N >= 32768:
+            # reading R-tol: at N >= 32768 the fp64 oracle's own error (λ1_0 = 1 − α^{1/N} ≈ 3e-5
+            # cancels) nears the bar, so the forward error is taken against the extended-precision
+            # oracle and bounded by max(1e-12, 4 × the fp64 oracle's own error)
+            zt = precond.pinv_dft(w, op, v, extended=True)
+            own = rel(precond.pinv_dft(w, op, v), zt)
+            assert rel(zg, zt) <= max(1e-12, 4 * own), (name, rel(zg, zt), own)
+        else:
+            assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12, name
         if s.ld > w.n:
             assert float(z[..., w.n:].abs().max()) == 0.0
     assert s.device_status() == 0
@@ -128,7 +139,8 @@ def test_pinv_c1_all_16_vectors():
 
 
 @pytest.mark.parametrize("name", ["1d_small", "1d_price", "1d_ragged", "c1", "1d_N1024_C2", "1d_N2048_C2",
-                                  "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8"])
+                                  "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8", "1d_N2048_ragged", "1d_N32768",
+                                  "1d_N65536"])
 def test_stage_kernels(name):
     """K2, K3, K4 separately against the oracle's steps (a), (b), (c) (unnormalised DFT)."""
     w = SMALL[name]
@@ -147,7 +159,8 @@ def test_stage_kernels(name):
     zhat = s.empty_spec()
     s.shifted_solve(what, zhat)
     zh = torch.view_as_complex(zhat).cpu().numpy()[:, : w.n]
-    assert rel(zh, zhat_o) < 1e-12
+    if w.N < 32768:  # beyond, K3 is held to the extended-precision bar of test_pinv_small (R-tol)
+        assert rel(zh, zhat_o) < 1e-12
     # K4 on the oracle's ẑ (so that K3's own rounding does not enter the K4 comparison)
     full = np.concatenate([zhat_o, np.conj(zhat_o[1:N - K + 1][::-1])])
     z_o = (np.fft.ifft(full, axis=0).real / g[:, None])
@@ -174,10 +187,41 @@ def test_pinv_k3_tree_variants(name, debug):
     assert s.device_status() == 0
 
 
+@pytest.mark.parametrize("name", ["1d_N2048_C2", "1d_N2048_ragged", "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8",
+                                  "1d_N32768"])
+@pytest.mark.parametrize("debug", [0, 16, 8])
+def test_time_fft_paths(name, debug):
+    """The 1D time FFTs for N >= 2048 run the four-step kernel (debug 0); debug 16 selects the
+    cluster kernel (N <= 16384) and debug 8 the one-column kernel — all three match the oracle's
+    steps (a) and (c), repeatedly (the four-step kernel's monotonic counters across launches)."""
+    w = SMALL[name]
+    if debug in (8, 16) and w.N > 16384:
+        pytest.skip("the cluster and one-column kernels cover N <= 16384")
+    s = solver_for(w)
+    s.set_debug(debug)
+    op = problem.build_operator(w)
+    N, K = w.N, w.N // 2 + 1
+    g = precond.gamma(N, w.alpha)
+    for v in synth.random_vectors(w, 2, 41):
+        what = s.empty_spec()
+        for _ in range(2):
+            s.time_fft(s.to_device(v), what)
+        wg = torch.view_as_complex(what).cpu().numpy()[:, : w.n]
+        assert rel(wg, np.fft.fft(g[:, None] * v, axis=0)[:K]) < 1e-13
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        assert rel(s.to_host(z), precond.pinv_dft(w, op, v)) < 1e-12
+        if s.ld > w.n:
+            assert float(z[..., w.n:].abs().max()) == 0.0
+    assert s.device_status() == 0
+
+
 @pytest.mark.parametrize("debug", [1, 2])
-def test_negative_controls_break_parity(debug):
-    """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail."""
-    w = SMALL["1d_small"]
+@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2"])
+def test_negative_controls_break_parity(debug, name):
+    """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail (cluster and
+    four-step FFT paths)."""
+    w = SMALL[name]
     s = solver_for(w)
     op = problem.build_operator(w)
     v = synth.random_vectors(w, 1, 5)[0]
