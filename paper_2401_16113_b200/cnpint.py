@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcnpint.so")
+# CNPINT_LIB: an alternative in-tree build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("CNPINT_LIB") or os.path.join(_HERE, "libcnpint.so")
 
 STATUS = {0: "CNPINT_OK", -1: "CNPINT_EINVAL", -2: "CNPINT_EUNSUPPORTED", -3: "CNPINT_ECUDA",
           -4: "CNPINT_ESINGULAR", -5: "CNPINT_ENOCONV", -6: "CNPINT_EBREAKDOWN"}

@@ -28,11 +28,9 @@
 
 #include "fft_tile.cuh"
 
-#ifndef FS_NT
-#define FS_NT 128
-#endif
-#ifndef FS_MINB
-#define FS_MINB 4
+#define FS_NT 256
+#ifndef FS_MINB6
+#define FS_MINB6 3
 #endif
 
 namespace {
@@ -49,25 +47,63 @@ CNP_DEV unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 CNP_DEV void discard_l2(const void* p) { asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory"); }
+template <bool INV>
+CNP_DEV double2 twm(double2 a, double2 w) {  // a·w (forward) or a·conj(w) (inverse)
+  return INV ? cmul_conj(a, w) : cmul(a, w);
+}
 
-// compile-time geometry.  t1 items hold NC pair columns × N2 rows; family items hold NF = NC/2 pair
-// columns × 2 members × N1 rows (the same shared-memory footprint when N1 = N2).
+// Register FFT of length L = R1·R2 over one column, two threads roles (Cooley–Tukey, n = n2 + R2 n1,
+// k = k1 + R1 k2):  step 1 — thread n2 holds x[n2 + R2 n1] (n1 < R1), R1-point DFT in registers,
+// twiddle ω_L^{n2 k1}, write A[k1][n2] to the column's exchange area; step 2 — thread k1 reads
+// A[k1][·], R2-point DFT → X[k1 + R1 k2] (k2 < R2).  One shared-memory round trip per pass
+// (the Stockham version of fft_tile.cuh makes one per radix stage).
+template <int LOGL>
+struct RF {
+  static constexpr int L = 1 << LOGL;
+  static constexpr int R1 = LOGL >= 8 ? 16 : LOGL >= 6 ? 8 : 4;
+  static constexpr int R2 = L / R1;
+  static constexpr int SK = R2 + 1;          // exchange layout A[k1][n2] at k1·SK + n2
+  static constexpr int G1 = R1 + 1;          // gather layout x[n2 + R2 n1] at n2·G1 + n1
+  static constexpr int S1 = R1 * SK, S2 = R2 * G1;
+  static constexpr int SC = (S1 > S2 ? S1 : S2) | 1;  // odd per-column stride: lanes = columns, conflict free
+};
+
+template <int LOGL, bool INV>
+CNP_DEV void rf_step1(double2 (&v)[RF<LOGL>::R1], double2* col, const double2* twL, int n2) {
+  using F = RF<LOGL>;
+  dftR<F::R1, INV>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < F::R1; ++k1) v[k1] = twm<INV>(v[k1], twL[n2 * k1]);
+#pragma unroll
+  for (int k1 = 0; k1 < F::R1; ++k1) col[k1 * F::SK + n2] = v[k1];
+}
+template <int LOGL, bool INV>
+CNP_DEV void rf_step2(double2 (&u)[RF<LOGL>::R2], const double2* col, int k1) {
+  using F = RF<LOGL>;
+#pragma unroll
+  for (int n2 = 0; n2 < F::R2; ++n2) u[n2] = col[k1 * F::SK + n2];
+  dftR<F::R2, INV>(u);
+}
+
+// compile-time geometry: blocks of NC pair columns; t1 items hold NC columns, family items NC
+// columns = 2 members × NF pairs (half of the block's pairs)
 template <int LOG1, int LOG2>
 struct FsGeo {
   static constexpr int N1 = 1 << LOG1, N2 = 1 << LOG2, N = N1 * N2, H = N / 2;
   static constexpr int MX = LOG1 > LOG2 ? LOG1 : LOG2;
-  static constexpr int NC = MX <= 6 ? 32 : MX == 7 ? 16 : 8;
+  static constexpr int NC = MX <= 6 ? 32 : 16;
   static constexpr int NF = NC / 2;
-  static constexpr int CS1 = tf_cs(LOG1), CS2 = tf_cs(LOG2);
-  static constexpr int dataA = NC * CS2, dataB = 2 * NF * CS1;
-  static constexpr int data = dataA > dataB ? dataA : dataB;
-  static constexpr int off_stw1 = data;
-  static constexpr int off_stw2 = off_stw1 + tf_stage_tw(LOG1);
-  static constexpr int off_tw = off_stw2 + tf_stage_tw(LOG2);           // per-item twiddles [2·max(N1,N2)]
+  static constexpr int SCM = RF<LOG1>::SC > RF<LOG2>::SC ? RF<LOG1>::SC : RF<LOG2>::SC;
+  static constexpr int off_tw1 = NC * SCM;           // ω_{N1}^j, j < N1
+  static constexpr int off_tw2 = off_tw1 + N1;       // ω_{N2}^j
+  static constexpr int off_twn = off_tw2 + N2;       // per-item ω_N table [2·max(N1, N2)]
   static constexpr int NTW = 2 * (N1 > N2 ? N1 : N2);
   static constexpr int HI = N / 64;
-  static constexpr int off_g = off_tw + NTW;                            // doubles ghi[HI], glo[64]
+  static constexpr int off_g = off_twn + NTW;        // doubles ghi[HI], glo[64]
   static constexpr size_t bytes = (size_t)(off_g + (HI + 64) / 2 + 1) * 16;
+  static constexpr int MINB = MX <= 6 ? FS_MINB6 : 2;
+  static_assert(NC * (RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2) <= FS_NT, "threads");
+  static_assert(NC * (RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2) <= FS_NT, "threads");
 };
 
 }  // namespace
@@ -96,46 +132,61 @@ CNP_DEV void fs_item(const FsSched& S, unsigned T, int& isB, int& xb, int& idx) 
   }
 }
 
+CNP_DEV void fs_wait(const unsigned* cnt, unsigned target) {
+  if (threadIdx.x == 0)
+    while ((int)(ld_acquire(cnt) - target) < 0) __nanosleep(32);
+  __syncthreads();
+}
+CNP_DEV void fs_signal(unsigned* cnt) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // cumulative over the CTA's stores ordered before it by the barrier
+    atomicAdd(cnt, 1u);
+  }
+}
+
 // Item kinds.  MODE 0: A items (isB = 0) are t1 items, B items are family items.  MODE 1: A items are
 // family items, B items are t1 items.  Family item index = 2·k2 + h (h: which half of the block's
-// pair columns).
+// pair columns).  Threads: tid = col + NC·j, j = the role index of the register FFT.  Inputs go
+// straight from global memory (HBM for the input vector / spectrum, L2 for Y) into the step-1
+// registers; the only shared-memory traffic is the exchange of the register FFT.
 template <int MODE, int LOG1, int LOG2>
-__global__ void __launch_bounds__(FS_NT, FS_MINB)
+__global__ void __launch_bounds__(FS_NT, FsGeo<LOG1, LOG2>::MINB)
     k_fstep(const double* __restrict__ vin, const double2* __restrict__ spin, double* __restrict__ vout,
             double2* __restrict__ spout, double2* __restrict__ Y, const double* __restrict__ vscale, int W, int nx,
             const double* __restrict__ gtab, int accumulate, int debug_sign, FsSched S, unsigned* cnt,
             unsigned* ticket, unsigned tick_base, unsigned cnt_target, int no_discard) {
   using G = FsGeo<LOG1, LOG2>;
+  using F1 = RF<LOG1>;  // family items: length N1
+  using F2 = RF<LOG2>;  // t1 items: length N2
   constexpr int NT = FS_NT;
   constexpr int N1 = G::N1, N2 = G::N2, N = G::N, H = G::H, NC = G::NC, NF = G::NF;
-  constexpr int CS1 = G::CS1, CS2 = G::CS2;
   constexpr int X = 2 * NC;  // real columns per block
-  static_assert(NT % NC == 0, "pair column per thread must be fixed");
   const int tid = threadIdx.x;
+  const int col = tid % NC, j = tid / NC;
   double2* const buf = tf_smem;
-  double2* const stw1 = tf_smem + G::off_stw1;
-  double2* const stw2 = tf_smem + G::off_stw2;
-  double2* const tws = tf_smem + G::off_tw;
+  double2* const tw1 = tf_smem + G::off_tw1;
+  double2* const tw2 = tf_smem + G::off_tw2;
+  double2* const twn = tf_smem + G::off_twn;
   double* const ghi = reinterpret_cast<double*>(tf_smem + G::off_g);
   double* const glo = ghi + G::HI;
-  __shared__ unsigned s_ticket;
+  __shared__ unsigned s_tk[2];  // ticket of item i in s_tk[i & 1]
 
-  // ---- per-CTA tables once: stage twiddles of both lengths, Γ_α (MODE 0) or 1/(NΓ_α) (MODE 1) as
-  //      two-level tables g_t = ghi[t >> 6]·glo[t & 63] (glo of MODE 1 carries the factor N back)
+  // ---- per-CTA tables once: ω_{N1}, ω_{N2}; Γ_α (MODE 0) or 1/(NΓ_α) (MODE 1) as two-level tables
+  //      g_t = ghi[t >> 6]·glo[t & 63] (glo of MODE 1 carries the factor N back)
   const double sg = debug_sign ? -1.0 : 1.0;
-  fill_stage_twiddles(stw1, LOG1, sg, tid, NT);
-  fill_stage_twiddles(stw2, LOG2, sg, tid, NT);
+  for (int q = tid; q < N1; q += NT) { double2 w = expi_neg(q, N1); w.y *= sg; tw1[q] = w; }
+  for (int q = tid; q < N2; q += NT) { double2 w = expi_neg(q, N2); w.y *= sg; tw2[q] = w; }
   for (int q = tid; q < G::HI; q += NT) ghi[q] = __ldg(gtab + q * 64);
   for (int q = tid; q < 64; q += NT) glo[q] = MODE == 0 ? __ldg(gtab + q) : (double)N * __ldg(gtab + q);
   const double s = (MODE == 0 && vscale) ? *vscale : 1.0;
-  if (tid == 0) s_ticket = atomicAdd(ticket, 1u) - tick_base;
+  if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u) - tick_base;
 
-  for (;;) {
-    __syncthreads();  // previous item done with buf / tws; s_ticket published
-    const unsigned T = s_ticket;
+  for (int it = 0;; ++it) {
+    __syncthreads();  // previous item done with buf / twn; s_tk[it & 1] published
+    const unsigned T = s_tk[it & 1];
     if (T >= S.total) break;
-    // the next ticket is requested now and published at the end of this item (its latency hides
-    // behind this item's work)
+    // the next ticket is requested now and published in the other slot at the end of this item
     unsigned nxt = 0;
     if (tid == 0) nxt = atomicAdd(ticket, 1u);
     int isB, xb, idx;
@@ -144,63 +195,61 @@ __global__ void __launch_bounds__(FS_NT, FS_MINB)
     double2* const Yb = Y + (size_t)xb * N * NC;  // block's Y: [t1][k2][c], c < NC
 
     if ((MODE == 0 && !isB) || (MODE == 1 && isB)) {
-      // ================= t1 items: MODE 0 pass A (rows t1 + N1 t2 → Y), MODE 1 pass B' (Y → rows)
+      // ================= t1 items (length N2): MODE 0 pass A, MODE 1 pass B'
+      double2* const cb = buf + col * F2::SC;
       const int t1 = idx;
-      const int cpair = tid % NC;  // fixed across the loops below
-      const int mycol = col0 + 2 * cpair;
+      const int mycol = col0 + 2 * col;
       const bool padA = mycol >= nx, padB = mycol + 1 >= nx, colok = mycol < W;
-      if (MODE == 0) {
-        for (int q = tid; q < N2 * NC; q += NT) {
-          const int t2 = q / NC, c = q - t2 * NC;
-          const int col = col0 + 2 * c;
-          double2* dst = buf + c * CS2 + pd(t2);
-          if (col < W) cp_async16(dst, vin + (int64_t)(t1 + N1 * t2) * W + col);
-          else *dst = make_double2(0.0, 0.0);
-        }
+      if (MODE == 0)
         for (int q = tid; q < N2; q += NT) {  // ω_N^{t1 k2}
           double2 w = expi_neg((t1 * q) & (N - 1), N);
           w.y *= sg;
-          tws[q] = w;
+          twn[q] = w;
         }
-      } else {
-        if (tid == 0) {
-          while ((int)(ld_acquire(cnt + xb) - cnt_target) < 0) __nanosleep(32);
+      else
+        fs_wait(cnt + xb, cnt_target);
+      if (j < F2::R2) {
+        const int n2 = j;
+        double2 v[F2::R1];
+        if (MODE == 0) {
+#pragma unroll
+          for (int n1 = 0; n1 < F2::R1; ++n1) {
+            const int t = t1 + N1 * (n2 + F2::R2 * n1);
+            v[n1] = colok ? __ldcs(reinterpret_cast<const double2*>(vin + (int64_t)t * W + mycol))
+                          : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int n1 = 0; n1 < F2::R1; ++n1) {
+            const int t = t1 + N1 * (n2 + F2::R2 * n1);
+            v[n1] = cscale(v[n1], ghi[t >> 6] * glo[t & 63] * s);
+          }
+        } else {
+#pragma unroll
+          for (int n1 = 0; n1 < F2::R1; ++n1) v[n1] = __ldcg(Yb + ((size_t)t1 * N2 + n2 + F2::R2 * n1) * NC + col);
         }
-        __syncthreads();
-        const double2* src = Yb + (size_t)t1 * N2 * NC;
-        for (int q = tid; q < N2 * NC; q += NT) {
-          const int k2 = q / NC, c = q - k2 * NC;
-          cp_async16(buf + c * CS2 + pd(k2), src + q);
-        }
+        rf_step1<LOG2, MODE == 1>(v, cb, tw2, n2);
       }
-      cp_async_commit();
-      cp_async_wait<0>();
       __syncthreads();
-      if (MODE == 0) {
-        local_fft<false, TF_SCALE, LOG2, NC, NT>(buf, stw2, TfScale{ghi, glo, N1, t1, s});
-        double2* dst = Yb + (size_t)t1 * N2 * NC;
-        for (int q = tid; q < N2 * NC; q += NT) {
-          const int k2 = q / NC, c = q - k2 * NC;
-          dst[q] = cmul(buf[c * CS2 + pd(k2)], tws[k2]);
-        }
-        __syncthreads();
-        if (tid == 0) {
-          __threadfence();  // cumulative: orders the CTA's Y stores (bar.sync) before the count
-          atomicAdd(cnt + xb, 1u);
-        }
-      } else {
-        if (!no_discard) {
-          const char* src = reinterpret_cast<const char*>(Yb + (size_t)t1 * N2 * NC);
-          for (int q = tid; q < N2 * NC * 16 / 128; q += NT) discard_l2(src + q * 128);
-        }
-        local_fft<true, TF_PLAIN, LOG2, NC, NT>(buf, stw2, TfScale{nullptr, nullptr, 1, 0, 1.0});
-        if (colok) {
-          for (int q = tid; q < N2 * NC; q += NT) {
-            const int t2 = q / NC;  // q % NC == cpair
-            const int t = t1 + N1 * t2;
+      if (MODE == 1 && !no_discard) {  // this t1's Y rows: N2·NC·16 B, contiguous
+        const char* src = reinterpret_cast<const char*>(Yb + (size_t)t1 * N2 * NC);
+        for (int q = tid; q < N2 * NC * 16 / 128; q += NT) discard_l2(src + q * 128);
+      }
+      if (j < F2::R1) {
+        const int k1 = j;
+        double2 u[F2::R2];
+        rf_step2<LOG2, MODE == 1>(u, cb, k1);
+        if (MODE == 0) {
+#pragma unroll
+          for (int k2 = 0; k2 < F2::R2; ++k2) {
+            const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
+            Yb[((size_t)t1 * N2 + kk) * NC + col] = cmul(u[k2], twn[kk]);
+          }
+        } else if (colok) {
+#pragma unroll
+          for (int k2 = 0; k2 < F2::R2; ++k2) {
+            const int t = t1 + N1 * (k1 + F2::R1 * k2);
             const double g = ghi[t >> 6] * glo[t & 63];
-            const double2 z = buf[cpair * CS2 + pd(t2)];
-            double2 val = make_double2(padA ? 0.0 : z.x * g, padB ? 0.0 : z.y * g);
+            double2 val = make_double2(padA ? 0.0 : u[k2].x * g, padB ? 0.0 : u[k2].y * g);
             double2* dst = reinterpret_cast<double2*>(vout + (int64_t)t * W + mycol);
             if (accumulate) {
               const double2 o = *dst;
@@ -211,62 +260,64 @@ __global__ void __launch_bounds__(FS_NT, FS_MINB)
           }
         }
       }
+      if (MODE == 0) fs_signal(cnt + xb);
     } else {
-      // ================= family items {k2, N2 − k2} × half block h: MODE 0 pass B (Y → spectrum
-      //                   rows), MODE 1 pass A' (spectrum rows → Y).  Columns: pairs h·NF + c, c < NF.
+      // ================= family items {k2, N2 − k2} × half block h (length N1): MODE 0 pass B,
+      //                   MODE 1 pass A'.  Column col = m·NF + p: member m, pair h·NF + p.
       const int k2 = idx >> 1, h = idx & 1;
       const int k2m = (N2 - k2) & (N2 - 1);
       const bool two = k2m != k2;
-      const int cpair = tid % NF;
-      const int gpair = h * NF + cpair;  // pair index within the block
-      const int mycol = col0 + 2 * gpair;
+      const int m = col / NF, p = col - m * NF;
+      const int km = m ? k2m : k2;
+      const bool active = m == 0 || two;
+      const int gp = h * NF + p;
+      const int mycol = col0 + 2 * gp;
       const bool padA = mycol >= nx, padB = mycol + 1 >= nx, colok = mycol < W;
-      // spectrum rows of the family: member 0 k = k2 + N2 k1 <= H (n0 rows), member 1 k = k2m + N2 k1 <= H
-      const int n0 = (H - k2) / N2 + 1;
-      const int n1 = two ? (H - k2m) / N2 + 1 : 0;
+      double2* const fb = buf + col * F1::SC;
       if (MODE == 0) {
-        if (tid == 0) {
-          while ((int)(ld_acquire(cnt + xb) - cnt_target) < 0) __nanosleep(32);
+        fs_wait(cnt + xb, cnt_target);
+        if (j < F1::R2) {
+          const int n2 = j;
+          double2 v[F1::R1];
+#pragma unroll
+          for (int n1 = 0; n1 < F1::R1; ++n1)
+            v[n1] = active ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp) : make_double2(0.0, 0.0);
+          rf_step1<LOG1, false>(v, fb, tw1, n2);
         }
         __syncthreads();
-        for (int q = tid; q < N1 * NF; q += NT) {
-          const int t1 = q / NF, c = q - t1 * NF;
-          cp_async16(buf + c * CS1 + pd(t1), Yb + ((size_t)t1 * N2 + k2) * NC + h * NF + c);
-          if (two) cp_async16(buf + (NF + c) * CS1 + pd(t1), Yb + ((size_t)t1 * N2 + k2m) * NC + h * NF + c);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-        if (!no_discard) {  // NF·16 B per (t1, member) row
+        if (!no_discard) {  // rows (t1, km): NF·16 B = NF/8 lines at each of N1 rows, 2 members
           constexpr int LPR = NF * 16 / 128;
-          for (int q = tid; q < N1 * LPR * 2; q += NT) {
-            const int m = q / (N1 * LPR), r = q - m * N1 * LPR;
+          for (int q = tid; q < 2 * N1 * LPR; q += NT) {
+            const int mm = q / (N1 * LPR), r = q - mm * N1 * LPR;
             const int t1 = r / LPR, l = r - t1 * LPR;
-            if (m == 1 && !two) continue;
-            const char* p = reinterpret_cast<const char*>(Yb + ((size_t)t1 * N2 + (m ? k2m : k2)) * NC + h * NF);
-            discard_l2(p + l * 128);
+            if (mm == 1 && !two) continue;
+            const char* a = reinterpret_cast<const char*>(Yb + ((size_t)t1 * N2 + (mm ? k2m : k2)) * NC + h * NF);
+            discard_l2(a + l * 128);
           }
         }
-        local_fft<false, TF_PLAIN, LOG1, 2 * NF, NT>(buf, stw1, TfScale{nullptr, nullptr, 1, 0, 1.0});
-        if (colok) {
-          for (int q = tid; q < (n0 + n1) * NF; q += NT) {
-            const int r = q / NF;  // q % NF == cpair
-            double2 zk, zm;
-            int k;
-            if (r < n0) {
-              const int k1 = r;
-              k = k2 + N2 * k1;
-              zk = buf[cpair * CS1 + pd(k1)];
-              zm = k2 == 0 ? buf[cpair * CS1 + pd((N1 - k1) & (N1 - 1))]
-                           : buf[((two ? NF : 0) + cpair) * CS1 + pd(N1 - 1 - k1)];
-            } else {
-              const int k1 = r - n0;
-              k = k2m + N2 * k1;
-              zk = buf[(NF + cpair) * CS1 + pd(k1)];
-              zm = buf[cpair * CS1 + pd(N1 - 1 - k1)];
-            }
+        double2 u[F1::R2];
+        if (j < F1::R1) rf_step2<LOG1, false>(u, fb, j);
+        __syncthreads();  // every thread has read its exchange row: the areas now take X
+        if (j < F1::R1) {
+#pragma unroll
+          for (int k2i = 0; k2i < F1::R2; ++k2i) fb[j * F1::SK + k2i] = u[k2i];  // X[k1 + R1 k2] at k1·SK + k2
+        }
+        __syncthreads();
+        if (j < F1::R1 && active && colok) {
+          const int k1 = j;
+#pragma unroll
+          for (int k2i = 0; k2i < F1::R2; ++k2i) {
+            const int ko = k1 + F1::R1 * k2i;  // outer frequency: spectrum row km + N2·ko
+            const int k = km + N2 * ko;
+            if (k > H) continue;
+            int pcol, pko;
+            if (m == 1) { pcol = col - NF; pko = N1 - 1 - ko; }
+            else if (k2 == 0) { pcol = col; pko = (N1 - ko) & (N1 - 1); }
+            else if (!two) { pcol = col; pko = N1 - 1 - ko; }
+            else { pcol = col + NF; pko = N1 - 1 - ko; }
+            const double2 zm = buf[pcol * F1::SC + (pko % F1::R1) * F1::SK + pko / F1::R1];
             double2 xa, xbv;
-            fs_separate(zk, zm, xa, xbv);
+            fs_separate(u[k2i], zm, xa, xbv);
             if (padA) xa = make_double2(0.0, 0.0);
             if (padB) xbv = make_double2(0.0, 0.0);
             double2* o = spout + (int64_t)k * W + mycol;
@@ -275,15 +326,19 @@ __global__ void __launch_bounds__(FS_NT, FS_MINB)
           }
         }
       } else {
-        // gather Z_k for both members from the stored rows min(k, N − k)
-        for (int q = tid; q < (n0 + n1) * NF; q += NT) {
-          const int r = q / NF;
+        // gather Z for both members from the stored rows min(k, N − k) into the step-1 layout
+        // x[n2 + R2 n1] at n2·G1 + n1
+        const int n0 = (H - k2) / N2 + 1;
+        const int n1r = two ? (H - k2m) / N2 + 1 : 0;
+        for (int q = tid; q < (n0 + n1r) * NF; q += NT) {
+          const int r = q / NF, pp = q - r * NF;
           const bool m1 = r >= n0;
-          const int k1 = m1 ? r - n0 : r;
-          const int k = (m1 ? k2m : k2) + N2 * k1;
+          const int k1o = m1 ? r - n0 : r;
+          const int k = (m1 ? k2m : k2) + N2 * k1o;
+          const int gcol = col0 + 2 * (h * NF + pp);
           double2 xa = make_double2(0.0, 0.0), xbv = xa;
-          if (colok) {
-            const double2* src = spin + (int64_t)k * W + mycol;
+          if (gcol < W) {
+            const double2* src = spin + (int64_t)k * W + gcol;
             xa = ldg_cs2(src);
             xbv = ldg_cs2(src + 1);
           }
@@ -294,40 +349,46 @@ __global__ void __launch_bounds__(FS_NT, FS_MINB)
             zk = fs_pack(xa, xbv);
             zp = fs_pack(cconj(xa), cconj(xbv));
           }
-          // Z_k at its own member position; Z_{N−k} = conj-packed at the partner's position
-          buf[((m1 ? NF : 0) + cpair) * CS1 + pd(k1)] = zk;
-          int pm, pk1;
-          if (m1) { pm = 0; pk1 = N1 - 1 - k1; }
-          else if (k2 == 0) { pm = 0; pk1 = (N1 - k1) & (N1 - 1); }
-          else if (!two) { pm = 0; pk1 = N1 - 1 - k1; }
-          else { pm = 1; pk1 = N1 - 1 - k1; }
-          buf[(pm * NF + cpair) * CS1 + pd(pk1)] = zp;
+          int pm, pk;
+          if (m1) { pm = 0; pk = N1 - 1 - k1o; }
+          else if (k2 == 0) { pm = 0; pk = (N1 - k1o) & (N1 - 1); }
+          else if (!two) { pm = 0; pk = N1 - 1 - k1o; }
+          else { pm = 1; pk = N1 - 1 - k1o; }
+          buf[((m1 ? NF : 0) + pp) * F1::SC + (k1o % F1::R2) * F1::G1 + k1o / F1::R2] = zk;
+          buf[(pm * NF + pp) * F1::SC + (pk % F1::R2) * F1::G1 + pk / F1::R2] = zp;
         }
-        for (int q = tid; q < N1; q += NT) {  // conj ω_N^{k2 t1}, conj ω_N^{k2m t1}
+        for (int q = tid; q < N1; q += NT) {  // ω_N^{k2 t1}, ω_N^{k2m t1} (conjugated at use)
           double2 w0 = expi_neg((k2 * q) & (N - 1), N), w1 = expi_neg((k2m * q) & (N - 1), N);
-          w0.y *= -sg;
-          w1.y *= -sg;
-          tws[q] = w0;
-          tws[N1 + q] = w1;
+          w0.y *= sg;
+          w1.y *= sg;
+          twn[q] = w0;
+          twn[N1 + q] = w1;
         }
         __syncthreads();
-        local_fft<true, TF_PLAIN, LOG1, 2 * NF, NT>(buf, stw1, TfScale{nullptr, nullptr, 1, 0, 1.0});
-        for (int q = tid; q < N1 * NF * 2; q += NT) {
-          const int m = q / (N1 * NF), r = q - m * N1 * NF;
-          if (m == 1 && !two) continue;
-          const int t1 = r / NF, c = r - t1 * NF;
-          Yb[((size_t)t1 * N2 + (m ? k2m : k2)) * NC + h * NF + c] =
-              cmul(buf[(m * NF + c) * CS1 + pd(t1)], tws[m * N1 + t1]);
+        double2 v[F1::R1];
+        if (j < F1::R2) {
+#pragma unroll
+          for (int n1 = 0; n1 < F1::R1; ++n1) v[n1] = fb[j * F1::G1 + n1];
         }
+        __syncthreads();  // the gather layout is read: the areas now take the exchange layout
+        if (j < F1::R2) rf_step1<LOG1, true>(v, fb, tw1, j);
         __syncthreads();
-        if (tid == 0) {
-          __threadfence();
-          atomicAdd(cnt + xb, 1u);
+        if (j < F1::R1 && active) {
+          const int k1 = j;
+          double2 u[F1::R2];
+          rf_step2<LOG1, true>(u, fb, k1);
+#pragma unroll
+          for (int k2i = 0; k2i < F1::R2; ++k2i) {
+            const int t1 = k1 + F1::R1 * k2i;
+            Yb[((size_t)t1 * N2 + km) * NC + gp] = cmul_conj(u[k2i], twn[m * N1 + t1]);
+          }
         }
+        fs_signal(cnt + xb);
       }
     }
-    __syncthreads();  // everyone has read s_ticket and finished with buf
-    if (tid == 0) s_ticket = nxt - tick_base;
+    // publish the next ticket in the other slot (its readers passed this item's first barrier; the
+    // loop-top barrier publishes it)
+    if (tid == 0) s_tk[(it + 1) & 1] = nxt - tick_base;
   }
 }
 
@@ -345,7 +406,7 @@ static int fs_nc(int N) {
   int l1, l2;
   fs_logs(N, l1, l2);
   const int mx = l1 > l2 ? l1 : l2;
-  return mx <= 6 ? 32 : mx == 7 ? 16 : 8;
+  return mx <= 6 ? 32 : 16;
 }
 int fstep_nxb(int N, int64_t ld) { return (int)((ld + 2 * fs_nc(N) - 1) / (2 * fs_nc(N))); }
 // Y: nxb blocks of N × NC complex (the last block padded to whole pairs of NC columns)
