@@ -149,8 +149,8 @@ def ncu_traffic(kernel: str, workload: str):
     if os.path.exists(p):
         d = json.load(open(p)).get(kernel)
         if d and d.get("workload") == workload:
-            return d["bytes_per_launch"]
-    return None
+            return d["bytes_per_launch"], d.get("algo_bytes_this_launch"), d.get("launch")
+    return None, None, None
 
 
 # ----------------------------------------------------------------------------------- workload
@@ -242,6 +242,7 @@ def run_gpu(args, rank, world, local):
     peak, peak_src = measured_hbm_peak()
     achieved = d_by / (d_ms * 1e-3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
+    traffic = ncu_traffic(dominant, w.name)
 
     # ---------------- standalone P⁻¹ applies/s and matvec GB/s on 4 seeded N(0,1) vectors (> L2)
     V = synth.random_vectors(w, 4, w.rand_seed)
@@ -314,7 +315,8 @@ def run_gpu(args, rank, world, local):
         "matvec": {"ms": 1e3 * mv_s, "GBps": mv_gbps, "frac": mv_gbps / peak},
         "stream_copy_GBps": copy_best,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(dominant, w.name),
+                     "frac": achieved / peak, "traffic": traffic[0],
+                     "traffic_launch": {"algo_bytes": traffic[1], "which": traffic[2]},
                      "algo_bytes_per_launch": d_by / d_cnt, "peak_source": peak_src,
                      "share_of_step": d_ms / total_prof_ms if total_prof_ms else None,
                      "frac_of_same_run_copy": achieved / copy_best if copy_best else None},
