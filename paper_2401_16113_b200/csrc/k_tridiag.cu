@@ -37,6 +37,7 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdlib>
 #include <cstring>
 
 namespace {
@@ -95,13 +96,14 @@ enum { MODE_VAR = 0, MODE_TOEP = 1, MODE_FAST = 2 };
 //     P0 = pa gd_A + pb fd_B,  R0 = ra fd_B + rb gd_A,  fd ← fd_A − fcA P0,  gd ← gd_B − gaB R0,
 //     x_m = P0 + P1 x_s + P2 x_e,  x_{m+1} = R0 + R1 x_s + R2 x_e;
 //   root (4 entries): x_0 = c0 fd + c1 gd,  x_{m−1} = c2 fd + c3 gd.
-template <int MODE, int L>
-__global__ void __launch_bounds__(256)
+// two CTAs per SM (measured: forcing three for the fast tree, 80 registers, is slower at c2)
+template <int MODE, int L, int MAXT>
+__global__ void __launch_bounds__(MAXT, 2)
     k_tridiag(const double2* __restrict__ what, double2* __restrict__ zhat, const double* __restrict__ lo,
               const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
               const double2* __restrict__ il2, const double2* __restrict__ tab, int m, int64_t W, int K, int G,
               int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status,
-              const double2* __restrict__ lam1) {
+              const double2* __restrict__ lam1, int skip) {
   constexpr bool TOEP = MODE != MODE_VAR;
   constexpr bool FAST = MODE == MODE_FAST;
   constexpr int NCF = FAST ? 2 : 6;  // stored coefficients per merge
@@ -126,7 +128,8 @@ __global__ void __launch_bounds__(256)
   // ---------------- asynchronous load of the system (and its table) into shared memory
   if (act) {
     const double2* src = what + (int64_t)k * W;
-    for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
+    if (!(skip & 1))
+      for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
     if (TOEP)
       for (int i = p; i < TS; i += P) cp_async16(T + i, tab + (size_t)k * TS + i);
   }
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(256)
     const double2 r = crecip(lam1[k]);
     for (int i = p; i < m; i += P) D[sidx(i)] = cmul(D[sidx(i)], r);
   }
-  if (act && !diag_only) {
+  if (act && !diag_only && !(skip & 2)) {
     double2 dl[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) dl[j] = (j < len) ? cmul(D[sidx(i0 + j)], il) : make_double2(0.0, 0.0);
@@ -400,7 +403,8 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (act) {
     double2* dst = zhat + (int64_t)k * W;
-    for (int i = p; i < m; i += P) stg_cs2(dst + i, D[sidx(i)]);
+    if (!(skip & 4))
+      for (int i = p; i < m; i += P) stg_cs2(dst + i, D[sidx(i)]);
     for (int i = m + p; i < W; i += P) dst[i] = make_double2(0.0, 0.0);
   }
 }
@@ -449,8 +453,17 @@ TriCfg tri_cfg(int m, int toeplitz) {
   std::memset(&t, 0, sizeof(t));
   t.small = m < 64;
   // chunks of <= Lcap rows: Lcap = 16 (Toeplitz: only the right-hand side lives in registers) or 8
-  // (variable rows also carry α', γ'); G = warps per system, NS = systems per CTA (<= 8 warps).
-  const int Lcap = toeplitz ? 16 : 8;
+  // (variable rows also carry α', γ'; measured: 8 / 512 threads at c2 and 4 at c3 are slower);
+  // G = warps per system, NS = systems per CTA (<= 8 warps when G < 8).  Tuning overrides:
+  // CNPINT_TRI_LCAP_T / CNPINT_TRI_LCAP_V (4, 8 or 16).
+  static int lcap_t = -1, lcap_v = -1;
+  if (lcap_t < 0) {
+    const char* e = getenv("CNPINT_TRI_LCAP_T");
+    lcap_t = e && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 16) ? atoi(e) : 16;
+    e = getenv("CNPINT_TRI_LCAP_V");
+    lcap_v = e && (atoi(e) == 4 || atoi(e) == 8) ? atoi(e) : 8;
+  }
+  const int Lcap = toeplitz ? lcap_t : lcap_v;
   int G = 1;
   while (G < 16 && 32 * G * Lcap < m) G <<= 1;
   t.G = G;
@@ -483,11 +496,19 @@ TriCfg tri_cfg(int m, int toeplitz) {
   return t;
 }
 
-template <int MODE, int L>
-static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+// timing experiments only (results wrong): CNPINT_TRI_SKIP bit 1 = no load, 2 = no chunk sweeps,
+// 4 = no store
+static int tri_skip() {
+  static int v = -1;
+  if (v < 0) v = getenv("CNPINT_TRI_SKIP") ? atoi(getenv("CNPINT_TRI_SKIP")) : 0;
+  return v;
+}
+
+template <int MODE, int L, int MAXT>
+static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_tridiag<MODE, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_tridiag<MODE, L, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -498,10 +519,18 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
   const int MP = tri_rows_alloc(c->nx, t.padsh);
   const size_t smem = (size_t)(t.NS * (MODE == MODE_VAR ? 3 * MP : MP + t.tabstride) + nw * 31 * ncf +
                                t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
-  k_tridiag<MODE, L><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
+  k_tridiag<MODE, L, MAXT><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
       what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS,
-      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1);
+      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1, tri_skip());
   return cudaGetLastError();
+}
+
+template <int MODE, int L>
+static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+  const int nt = 32 * t.G * t.NS;
+  if (nt <= 256) return run_tri_t<MODE, L, 256>(c, t, what, zhat);
+  if (nt <= 512) return run_tri_t<MODE, L, 512>(c, t, what, zhat);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat) {
