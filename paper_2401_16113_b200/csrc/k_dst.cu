@@ -142,6 +142,201 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Register version for E = 2(n+1) ∈ {256, 512, 1024} (c4, c5): the same odd-extension transform as
+// k_dst, but the E-point FFT runs as three register radix passes, E = R1·R2·R3, with two
+// shared-memory exchanges (Cooley–Tukey, n = m + M n1, M = R2 R3; k = k1 + R1 kk, kk = k2 + R2 k3):
+//   step 1  thread m (M threads / line pair) loads the extension samples x[m + M n1] straight from
+//           HBM, DFT_R1 over n1, twiddle ω_E^{m k1}, store B_{k1}[m];
+//   step 2  thread (k1, m3) reads B_{k1}[m3 + R3 m2], DFT_R2 over m2, twiddle ω_M^{m3 k2}, store
+//           C_{k1,k2}[m3];
+//   step 3  thread (k1, k2) reads C_{k1,k2}[·], DFT_R3 → F[k1 + R1 k2 + R1 R2 k3], k3 < R3.
+// x pass: a line pair is two rows, the 64 or 128 threads of a pair are consecutive (256-B coalesced
+// row reads); y pass: a pair is two adjacent columns, the threads of NC pairs are interleaved pair-
+// fastest so a warp reads 8 pairs × 16 B = 128-B row segments.
+template <int LOGE>
+struct DstPlan {
+  static constexpr int E = 1 << LOGE, M0 = E / 2;  // M0 = n + 1
+  static constexpr int R1 = LOGE == 10 ? 16 : 8;
+  static constexpr int R2 = 8;
+  static constexpr int R3 = E / (R1 * R2);
+  static constexpr int M = R2 * R3;
+  static constexpr int T1 = M, T2 = R1 * R3, T3 = R1 * R2;
+  static constexpr int TP = T1 > T2 ? (T1 > T3 ? T1 : T3) : (T2 > T3 ? T2 : T3);  // threads per pair
+  static constexpr int NC = TP * 8 <= 512 ? 8 : 512 / TP;                             // pairs per CTA
+  static constexpr int NT = TP * NC;
+  static constexpr int SB = M;                   // B_{k1}[m] at k1·SB + m
+  static constexpr int SC = R3 + 1;              // C_{k1,k2}[m3] at (k2·R1 + k1)·SC + m3 (odd)
+  static constexpr int AREA0 = R1 * SB > R1 * R2 * SC ? R1 * SB : R1 * R2 * SC;
+  static constexpr int AREA = AREA0 | 1;         // per-pair area, odd stride (pair-fastest lanes)
+  static constexpr size_t bytes = (size_t)(NC * AREA + E + M0 + 2) * 16;
+};
+
+template <bool YPASS, int LOGE>
+__global__ void __launch_bounds__(DstPlan<LOGE>::NT, LOGE <= 9 ? 2 : 1)
+    k_dst_r(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
+            const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
+            int nx) {
+  using P = DstPlan<LOGE>;
+  constexpr int E = P::E, M0 = P::M0, n = M0 - 1;
+  constexpr int R1 = P::R1, R2 = P::R2, R3 = P::R3, M = P::M, NC = P::NC, TP = P::TP;
+  const int tid = threadIdx.x;
+  // pair slot and role index within the pair
+  const int pr = YPASS ? tid % NC : tid / TP;
+  const int r = YPASS ? tid / NC : tid % TP;
+  double2* const area = tf_smem + pr * P::AREA;
+  double2* const twE = tf_smem + NC * P::AREA;                     // ω_E^q, q < E
+  double* const pre_s = reinterpret_cast<double*>(twE + E);         // pre-scale, index e = 1..n (0 at 0, M0)
+  const double sg = debug_sign ? -1.0 : 1.0;
+  for (int q = tid; q < E; q += P::NT) { double2 w = expi_neg(q, E); w.y *= sg; twE[q] = w; }
+  for (int e = tid; e <= M0; e += P::NT) pre_s[e] = (e == 0 || e == M0) ? 0.0 : (pre ? pre[e - 1] : 1.0);
+  __syncthreads();
+  const int ldi = (int)ld;
+  const int nlines = N * ny;
+  const int pairs_per_t = ldi / 2;
+  const int tiles_per_t = (pairs_per_t + NC - 1) / NC;
+  const int ntiles = YPASS ? N * tiles_per_t : ((nlines + 1) / 2 + NC - 1) / NC;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // ---- this thread's line pair
+    int la = 0, lb = 0, t = 0, p = 0;
+    bool ok;
+    if (!YPASS) {
+      la = (tile * NC + pr) * 2;
+      lb = la + 1;
+      ok = la < nlines;
+    } else {
+      t = tile / tiles_per_t;
+      p = (tile - t * tiles_per_t) * NC + pr;
+      ok = p < pairs_per_t;
+    }
+    // ---- x pass: stage the n samples z_j of every pair into its area (cp.async; the area is free
+    //      here).  y pass: step 1 loads its samples straight from HBM (16-B pair loads, 128-B row
+    //      segments across the 8 interleaved pairs) — measured faster than staging for that pass.
+    if (!YPASS) {
+      const int line0 = tile * NC * 2;
+      for (int q = tid; q < NC * n; q += P::NT) {
+        const int c = q / n, j = q - c * n;
+        const int qa = line0 + 2 * c, qb = qa + 1;
+        double* dst = reinterpret_cast<double*>(tf_smem + c * P::AREA + j);
+        if (qa < nlines) cp_async8(dst, in + (int64_t)qa * ld + j);
+        else dst[0] = 0.0;
+        if (qb < nlines) cp_async8(dst + 1, in + (int64_t)qb * ld + j);
+        else dst[1] = 0.0;
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    auto zget = [&](int j) -> double2 {
+      if (!YPASS) return area[j];
+      return ok ? __ldg(reinterpret_cast<const double2*>(in + ((int64_t)t * ny + j) * ld + 2 * p))
+                : make_double2(0.0, 0.0);
+    };
+    // ---- step 1: thread m, extension samples e = m + M n1 (0 at e = 0, M0; odd about M0)
+    double2 v[R1];
+    if (r < P::T1) {
+      const int m = r;
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int e = m + M * n1;
+        double2 x = make_double2(0.0, 0.0);
+        if (e > 0 && e < M0) x = cscale(zget(e - 1), pre_s[e]);
+        else if (e > M0) x = cscale(zget(E - e - 1), -pre_s[E - e]);
+        v[n1] = x;
+      }
+      dftR<R1, false>(v);
+    }
+    if (!YPASS) __syncthreads();  // the staged samples are consumed: the area takes B
+    if (r < P::T1) {
+      const int m = r;
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) area[k1 * P::SB + m] = k1 ? cmul(v[k1], twE[m * k1]) : v[0];
+    }
+    __syncthreads();
+    // ---- step 2: thread (k1, m3), role r = m3 + R3 k1 (B and C share the area: read, barrier, write)
+    double2 u[R2];
+    const int m3 = r % R3, k1s = r / R3;
+    if (r < P::T2) {
+#pragma unroll
+      for (int m2 = 0; m2 < R2; ++m2) u[m2] = area[k1s * P::SB + m3 + R3 * m2];
+      dftR<R2, false>(u);
+    }
+    __syncthreads();
+    if (r < P::T2) {
+#pragma unroll
+      for (int k2 = 0; k2 < R2; ++k2)
+        area[(k2 * R1 + k1s) * P::SC + m3] = k2 ? cmul(u[k2], twE[(m3 * k2) * R1]) : u[0];
+    }
+    __syncthreads();
+    // ---- step 3: thread (k1, k2), role r = k1 + R1 k2; F_k for k = r + R1 R2 k3
+    if (r < P::T3) {
+      const int k1 = r % R1, k2 = r / R1;
+      double2 w[R3];
+#pragma unroll
+      for (int m3 = 0; m3 < R3; ++m3) w[m3] = area[(k2 * R1 + k1) * P::SC + m3];
+      dftR<R3, false>(w);
+      if (ok) {
+#pragma unroll
+        for (int k3 = 0; k3 < R3; ++k3) {
+          const int k = r + R1 * R2 * k3;  // output x = k − 1 (x = n is the pad column / nothing)
+          if (k < 1 || k > M0) continue;
+          const int x = k - 1;
+          double sa = 0.0, sb = 0.0;
+          if (x < n) {
+            const double g = post ? post[x] : 1.0;
+            sa = -0.5 * w[k3].y * g;
+            sb = 0.5 * w[k3].x * g;
+          }
+          if (!YPASS) {
+            if (x < ldi) {
+              double* oa = out + (int64_t)la * ld + x;
+              *oa = accumulate ? *oa + sa : sa;
+              if (lb < nlines) {
+                double* ob = out + (int64_t)lb * ld + x;
+                *ob = accumulate ? *ob + sb : sb;
+              }
+            }
+          } else if (x < n) {
+            double2 v2 = make_double2(sa, sb);
+            if (2 * p >= nx) v2.x = 0.0;      // padding columns stay exactly zero
+            if (2 * p + 1 >= nx) v2.y = 0.0;
+            double2* o = reinterpret_cast<double2*>(out + ((int64_t)t * ny + x) * ld + 2 * p);
+            if (accumulate) {
+              const double2 q = *o;
+              v2.x += q.x;
+              v2.y += q.y;
+            }
+            stg_cs2(o, v2);
+          }
+        }
+      }
+    }
+    __syncthreads();  // the area is free for the next tile
+  }
+}
+
+template <bool YPASS, int LOGE>
+static cudaError_t run_dst_r(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
+                             int accumulate) {
+  using P = DstPlan<LOGE>;
+  auto kern = k_dst_r<YPASS, LOGE>;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::NT, P::bytes);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    grid_max = per_sm * c->num_sms;
+  }
+  const int nlines = c->N * c->ny;
+  const int ld = (int)c->ld;
+  const int ntiles = YPASS ? c->N * ((ld / 2 + P::NC - 1) / P::NC) : ((nlines + 1) / 2 + P::NC - 1) / P::NC;
+  const int grid = ntiles < grid_max ? ntiles : grid_max;
+  kern<<<grid, P::NT, P::bytes, c->stream>>>(in, out, c->N, c->ny, c->ld, pre, post, accumulate, c->debug & 1, c->nx);
+  return cudaGetLastError();
+}
+
 template <bool YPASS, int LOGE>
 static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
                              int accumulate) {
@@ -175,6 +370,10 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   int logE = 0;
   while ((1 << logE) < 2 * (n + 1)) ++logE;
   const int kid = YPASS ? KID_DST_Y : KID_DST_X;
+  // register kernel for the y pass at E = 512 (c4, c5 n = 255: 269 → 193 µs); the Stockham kernel is
+  // faster for the x pass and at E = 256 / 1024 (profiles/r01_dst_sweep.txt).  debug bit 32 forces
+  // the Stockham kernel everywhere (cross-check).
+  const bool reg = !(c->debug & 32);
   cnp_prof_begin(c, kid);
   cudaError_t e;
   switch (logE) {
@@ -185,7 +384,7 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
     case 6: e = run_dst_t<YPASS, 6>(c, in, out, pre, post, accumulate); break;
     case 7: e = run_dst_t<YPASS, 7>(c, in, out, pre, post, accumulate); break;
     case 8: e = run_dst_t<YPASS, 8>(c, in, out, pre, post, accumulate); break;
-    case 9: e = run_dst_t<YPASS, 9>(c, in, out, pre, post, accumulate); break;
+    case 9: e = (reg && YPASS) ? run_dst_r<YPASS, 9>(c, in, out, pre, post, accumulate) : run_dst_t<YPASS, 9>(c, in, out, pre, post, accumulate); break;
     case 10: e = run_dst_t<YPASS, 10>(c, in, out, pre, post, accumulate); break;
     case 11: e = run_dst_t<YPASS, 11>(c, in, out, pre, post, accumulate); break;
     default: e = cudaErrorInvalidValue; break;

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--op", default="pinv", choices=["pinv", "A", "gmres", "all"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--time", action="store_true", help="print per-kernel event timings (not under ncu)")
+    ap.add_argument("--debug", type=int, default=0, help="cnpint_set_debug flags (kernel-variant selection)")
     args = ap.parse_args()
     import torch
 
@@ -30,6 +31,8 @@ def main():
     if args.alpha is not None:
         w = w.with_(alpha=args.alpha)
     s = problems.make_solver(w, restart_max=w.restart if args.op in ("gmres", "all") else 0)
+    if args.debug:
+        s.set_debug(args.debug)
     rng = torch.Generator(device="cuda").manual_seed(1)
     vs = []
     for _ in range(2):
