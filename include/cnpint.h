@@ -213,9 +213,11 @@ cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, v
 
 /* Test hook (negative controls): 0 = none, 1 = flip the sign of the FFT twiddles,
  * 2 = use the printed Eq. eigCx ordering λ1_k = 1 − a e^{+2πik/N} (R3).
- * The parity suite must fail with either set.  Bit 4 (not a negative control) routes Toeplitz
- * shifted solves through the generic merge tree instead of the tabulated fast tree, so that the
- * parity suite covers both K3 variants on the same inputs. */
+ * The parity suite must fail with either set.  Kernel-variant bits (not negative controls; the
+ * parity suite runs the alternatives on the same inputs): 4 = Toeplitz shifted solves through the
+ * generic merge tree instead of the tabulated fast tree; 8 = the one-column time FFT kernel
+ * (N <= 16384); 16 = the cluster time FFT instead of the four-step kernel for 1D N >= 2048;
+ * 32 = the shared-memory Stockham DST kernel for every 2D sine pass. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

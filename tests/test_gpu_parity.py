@@ -50,6 +50,8 @@ SMALL = {
     "1d_N65536": synth.scaled(synth.C1, 5, 65536, alpha=0.1),
     "2d_N1024_C2": synth.scaled(synth.C4, 15, 1024, alpha=0.01),
     "2d_n63_N2048": synth.scaled(synth.C4, 63, 2048, alpha=0.01),
+    # E = 2(n+1) = 512: the register DST kernel of the y pass (k_dst_r); ragged pair tiles (ld/2 = 128)
+    "2d_n255_N8": synth.scaled(synth.C4, 255, 8, alpha=0.05),
     # NEXT #1: time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8)
     "1d_tv": synth.scaled(synth.C1T, 63, 64, alpha=0.01),
     "1d_tv_price": synth.scaled(synth.C3, 127, 128, alpha=0.01, dt_rate=0.3),
@@ -216,8 +218,28 @@ def test_time_fft_paths(name, debug):
     assert s.device_status() == 0
 
 
+@pytest.mark.parametrize("name", ["2d_small", "2d_mid", "2d_n255_N8"])
+@pytest.mark.parametrize("debug", [0, 32])
+def test_dst_paths(name, debug):
+    """2D P⁻¹ with the register DST kernel (debug 0, used for the y pass at E = 512) and with the
+    Stockham kernel everywhere (debug 32): both match the oracle and keep the padding zero."""
+    w = SMALL[name]
+    s = solver_for(w)
+    s.set_debug(debug)
+    op = problem.build_operator(w)
+    for v in synth.random_vectors(w, 2, 43):
+        z = s.empty()
+        s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12, (name, debug)
+        assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+        if s.ld > w.n:
+            assert float(z[..., w.n:].abs().max()) == 0.0
+    assert s.device_status() == 0
+
+
 @pytest.mark.parametrize("debug", [1, 2])
-@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2"])
+@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2", "2d_n255_N8"])
 def test_negative_controls_break_parity(debug, name):
     """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail (cluster and
     four-step FFT paths)."""
