@@ -28,7 +28,9 @@
 
 #include "fft_tile.cuh"
 
-#define FS_NT 256
+#ifndef FS_NC6
+#define FS_NC6 16  // pair columns per block for N1, N2 <= 64 (8 threads per column; 32 measured slower)
+#endif
 #ifndef FS_MINB6
 #define FS_MINB6 3
 #endif
@@ -91,7 +93,7 @@ template <int LOG1, int LOG2>
 struct FsGeo {
   static constexpr int N1 = 1 << LOG1, N2 = 1 << LOG2, N = N1 * N2, H = N / 2;
   static constexpr int MX = LOG1 > LOG2 ? LOG1 : LOG2;
-  static constexpr int NC = MX <= 6 ? 32 : 16;
+  static constexpr int NC = MX <= 6 ? FS_NC6 : 16;
   static constexpr int NF = NC / 2;
   static constexpr int SCM = RF<LOG1>::SC > RF<LOG2>::SC ? RF<LOG1>::SC : RF<LOG2>::SC;
   static constexpr int off_tw1 = NC * SCM;           // ω_{N1}^j, j < N1
@@ -101,9 +103,10 @@ struct FsGeo {
   static constexpr int HI = N / 64;
   static constexpr int off_g = off_twn + NTW;        // doubles ghi[HI], glo[64]
   static constexpr size_t bytes = (size_t)(off_g + (HI + 64) / 2 + 1) * 16;
-  static constexpr int MINB = MX <= 6 ? FS_MINB6 : 2;
-  static_assert(NC * (RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2) <= FS_NT, "threads");
-  static_assert(NC * (RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2) <= FS_NT, "threads");
+  static constexpr int TP1 = RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2;
+  static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
+  static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
+  static constexpr int MINB = MX <= 6 ? FS_MINB6 * 256 / NT : 2;
 };
 
 }  // namespace
@@ -151,7 +154,7 @@ CNP_DEV void fs_signal(unsigned* cnt) {
 // straight from global memory (HBM for the input vector / spectrum, L2 for Y) into the step-1
 // registers; the only shared-memory traffic is the exchange of the register FFT.
 template <int MODE, int LOG1, int LOG2>
-__global__ void __launch_bounds__(FS_NT, FsGeo<LOG1, LOG2>::MINB)
+__global__ void __launch_bounds__(FsGeo<LOG1, LOG2>::NT, FsGeo<LOG1, LOG2>::MINB)
     k_fstep(const double* __restrict__ vin, const double2* __restrict__ spin, double* __restrict__ vout,
             double2* __restrict__ spout, double2* __restrict__ Y, const double* __restrict__ vscale, int W, int nx,
             const double* __restrict__ gtab, int accumulate, int debug_sign, FsSched S, unsigned* cnt,
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(FS_NT, FsGeo<LOG1, LOG2>::MINB)
   using G = FsGeo<LOG1, LOG2>;
   using F1 = RF<LOG1>;  // family items: length N1
   using F2 = RF<LOG2>;  // t1 items: length N2
-  constexpr int NT = FS_NT;
+  constexpr int NT = G::NT;
   constexpr int N1 = G::N1, N2 = G::N2, N = G::N, H = G::H, NC = G::NC, NF = G::NF;
   constexpr int X = 2 * NC;  // real columns per block
   const int tid = threadIdx.x;
@@ -330,18 +333,32 @@ __global__ void __launch_bounds__(FS_NT, FsGeo<LOG1, LOG2>::MINB)
         // x[n2 + R2 n1] at n2·G1 + n1
         const int n0 = (H - k2) / N2 + 1;
         const int n1r = two ? (H - k2m) / N2 + 1 : 0;
-        for (int q = tid; q < (n0 + n1r) * NF; q += NT) {
+        constexpr int GIT = (N1 * NF + NT - 1) / NT;  // ≥ (n0 + n1r)·NF / NT
+        double2 ga[GIT], gb[GIT];
+#pragma unroll
+        for (int it = 0; it < GIT; ++it) {  // all row loads first (memory-level parallelism)
+          const int q = tid + it * NT;
+          ga[it] = gb[it] = make_double2(0.0, 0.0);
+          if (q < (n0 + n1r) * NF) {
+            const int r = q / NF, pp = q - r * NF;
+            const int k = r < n0 ? k2 + N2 * r : k2m + N2 * (r - n0);
+            const int gcol = col0 + 2 * (h * NF + pp);
+            if (gcol < W) {
+              const double2* src = spin + (int64_t)k * W + gcol;
+              ga[it] = ldg_cs2(src);
+              gb[it] = ldg_cs2(src + 1);
+            }
+          }
+        }
+#pragma unroll
+        for (int it = 0; it < GIT; ++it) {
+          const int q = tid + it * NT;
+          if (q >= (n0 + n1r) * NF) continue;
           const int r = q / NF, pp = q - r * NF;
           const bool m1 = r >= n0;
           const int k1o = m1 ? r - n0 : r;
           const int k = (m1 ? k2m : k2) + N2 * k1o;
-          const int gcol = col0 + 2 * (h * NF + pp);
-          double2 xa = make_double2(0.0, 0.0), xbv = xa;
-          if (gcol < W) {
-            const double2* src = spin + (int64_t)k * W + gcol;
-            xa = ldg_cs2(src);
-            xbv = ldg_cs2(src + 1);
-          }
+          const double2 xa = ga[it], xbv = gb[it];
           double2 zk, zp;
           if (k == 0 || k == H) {
             zk = zp = make_double2(xa.x, xbv.x);
@@ -406,7 +423,7 @@ static int fs_nc(int N) {
   int l1, l2;
   fs_logs(N, l1, l2);
   const int mx = l1 > l2 ? l1 : l2;
-  return mx <= 6 ? 32 : 16;
+  return mx <= 6 ? FS_NC6 : 16;
 }
 int fstep_nxb(int N, int64_t ld) { return (int)((ld + 2 * fs_nc(N) - 1) / (2 * fs_nc(N))); }
 // Y: nxb blocks of N × NC complex (the last block padded to whole pairs of NC columns)
@@ -423,7 +440,7 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   if (!per_sm) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::bytes);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FS_NT, G::bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, G::bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const int W = (int)c->ld;
@@ -442,7 +459,7 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   const unsigned target = c->fs_cnt + (unsigned)S.nA;
   static int no_discard = -1;
   if (no_discard < 0) no_discard = getenv("CNPINT_FS_NODISCARD") ? 1 : 0;
-  kern<<<grid, FS_NT, G::bytes, c->stream>>>(vin, spin, vout, spout, (double2*)c->d_fsY, vscale, W, c->nx,
+  kern<<<grid, G::NT, G::bytes, c->stream>>>(vin, spin, vout, spout, (double2*)c->d_fsY, vscale, W, c->nx,
                                             MODE == 0 ? c->d_gam : c->d_igam, accumulate, c->debug & 1, S,
                                             c->d_fscnt, c->d_fscnt + S.nxb, c->fs_tick, target, no_discard);
   c->fs_cnt = target;
