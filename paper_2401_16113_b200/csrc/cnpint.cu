@@ -134,8 +134,8 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   }
   L.tables_end = off;
   L.spec = op->dim == 1 ? take((size_t)(H + 1) * ld * 16) : take(16);
-  L.fsy = take(fstep_y_bytes(op->dim, N, ld));
-  L.fscnt = take(op->dim == 1 && N >= 2048 ? (size_t)(fstep_nxb(N, ld) + 1) * 4 : 4);
+  L.fsy = take(fstep_y_bytes(op->dim, N, (int64_t)ny * ld));
+  L.fscnt = take(fstep_y_bytes(op->dim, N, (int64_t)ny * ld) ? (size_t)(fstep_nxb(N, (int64_t)ny * ld) + 1) * 4 : 4);
   L.tmp1 = take(vec * 8); L.tmp2 = take(vec * 8); L.tmp3 = take(vec * 8);
   L.io1 = take(vec * 8); L.io2 = take(vec * 8); L.io3 = take(vec * 8);
   if (restart_max >= 1) {
@@ -461,7 +461,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_sk = (double2*)(w + L.sk); c->d_il2 = (double2*)(w + L.il2);
   c->d_tritab = (double2*)(w + L.tri);
   c->d_spec = (double2*)(w + L.spec);
-  c->d_fsY = fstep_y_bytes(op->dim, N, c->ld) ? (double*)(w + L.fsy) : nullptr;
+  c->d_fsY = fstep_y_bytes(op->dim, N, c->slice) ? (double*)(w + L.fsy) : nullptr;
   c->d_fscnt = (unsigned*)(w + L.fscnt);
   c->fs_cnt = 0;
   c->fs_tick = 0;

@@ -58,7 +58,7 @@ struct cnpint_ctx {
   double2* d_il2;      // [H+1] 1/λ2_k
   double2* d_tritab;   // [H+1][tabstride] Toeplitz chunk tables of K3 (1D Toeplitz only)
   double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
-  double* d_fsY;       // four-step FFT intermediate (1D, N >= 2048; k_fstep.cu), else null
+  double* d_fsY;       // four-step FFT intermediate (1D N >= 2048, 2D N >= 256; k_fstep.cu), else null
   unsigned* d_fscnt;   // [nxb] per-block pass-A counters, then the work ticket (monotonic)
   unsigned fs_cnt;     // host mirror: Σ pass-A items per block over all launches so far
   unsigned fs_tick;    // host mirror: tickets consumed so far
@@ -108,8 +108,9 @@ struct DotPtrs {
 };
 // y = 𝓜u fused with the first CGS pass: out[i] = Ṽ_iᵀ y, i < nv <= CNP_MAX_DOT (deterministic fold)
 bool fstep_ok(const cnpint_ctx* c);
-size_t fstep_y_bytes(int dim, int N, int64_t ld);
-int fstep_nxb(int N, int64_t ld);
+size_t fstep_y_bytes(int dim, int N, int64_t W);
+int fstep_nxb(int N, int64_t W);
+cudaError_t launch_fstep_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 cudaError_t launch_fstep_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,

@@ -1,7 +1,9 @@
-// Four-step time FFTs of the 1D P_α⁻¹ for long horizons (N >= 2048): K2 (MODE 0) and K4 (MODE 1)
-// of PAPER.md:296-323 (Eq. 3.2 steps (a) and (c), Remark 3.1), same definitions as k_tfft.cu:
-//   K2  ŵ_k[x] = Σ_t e^{−2πikt/N} · γ_t · s · v_t[x],  k = 0..N/2
-//   K4  z_t[x] = 1/(N γ_t) · Σ_{k<N} e^{+2πikt/N} ẑ_k[x],  ẑ_{N−k} = conj ẑ_k
+// Four-step time FFTs of P_α⁻¹ (Eq. 3.2 steps (a)-(c), Remark 3.1), same
+// definitions as k_tfft.cu:
+//   K2  (MODE 0, 1D)  ŵ_k[x] = Σ_t e^{−2πikt/N} · γ_t · s · v_t[x],  k = 0..N/2
+//   K4  (MODE 1, 1D)  z_t[x] = 1/(N γ_t) · Σ_{k<N} e^{+2πikt/N} ẑ_k[x],  ẑ_{N−k} = conj ẑ_k
+//   K6  (MODE 2, 2D)  z_t = 1/(N γ_t) · iFFT_k[ FFT_t(γ s v)_k / (λ1_k − λ2_k μ) ]  per spatial mode
+//                     column (μ = τ(e_x + e_y) + τ·shift)
 //
 // Why another decomposition.  The cluster kernel keeps all N rows of a column tile on chip, so at
 // N = 4096 a tile is only 8 real columns wide (64-B row segments) and its loads run at ~2 TB/s
@@ -9,18 +11,19 @@
 // k = k2 + N2 k1 and
 //   pass A  Y[t1][k2] = ω_N^{t1 k2} · FFT_{N2}( γ_t s v_{t1 + N1 t2} )[k2]            (per t1)
 //   pass B  X[k2 + N2 k1] = FFT_{N1}( Y[·][k2] )[k1]                                 (per k2)
-// (inverse: the same two passes backwards with conjugate twiddles).  Each pass moves tiles of
-// 2·NC = 64 real columns (512-B row segments).  The intermediate Y of a column block (2 MB at
-// c2) goes through L2 only: both passes run in ONE persistent kernel whose work items are handed
-// out in ticket order — the A items of block b, then (L blocks later) the B items of block b — and
-// a B item waits on a per-block counter until all A items of its block have landed.  A B item is
-// the sole reader of its Y rows and drops them from L2 afterwards (discard.global.L2), so Y is
-// never written back to HBM: HBM traffic is one read of the input and one write of the output.
-// Deadlock freedom: a B item only waits for items with smaller tickets, which were taken by CTAs
-// that are already running and whose A items never wait.
+// (inverse: the same two passes backwards with conjugate twiddles; MODE 2 runs forward pass B, the
+// spectral divide and inverse pass A' in one family item, so the 2D time pass is three phases).
+// Each pass moves tiles of 2·NC real columns.  The intermediate Y of a column block goes through L2
+// only: all phases run in ONE persistent kernel whose work items are handed out in ticket order —
+// phase-0 items of block b, phase-1 items of block b − L, phase-2 items of block b − 2L — and an
+// item of a later phase waits on its block's counter until the earlier phases of the block have
+// landed.  The last reader of a Y row drops it from L2 (discard.global.L2), so Y is never written
+// back to HBM: HBM traffic is one read of the input and one write of the output.  Deadlock
+// freedom: an item only waits for items with smaller tickets, which were taken by CTAs that are
+// already running and whose phase-0 items never wait.
 // Two real columns (a, b) are packed as one complex column z_t = v_t[a] + i v_t[b]; the Hermitian
 // separation X_a[k] = (Z_k + conj Z_{N−k})/2, X_b[k] = (Z_k − conj Z_{N−k})/(2i) pairs k2 with
-// N2 − k2, so pass B items are frequency families {k2, N2 − k2}, k2 = 0..N2/2.
+// N2 − k2, so the pass-B items are frequency families {k2, N2 − k2}, k2 = 0..N2/2.
 #include "common.cuh"
 #include "internal.h"
 
@@ -29,10 +32,7 @@
 #include "fft_tile.cuh"
 
 #ifndef FS_NC6
-#define FS_NC6 16  // pair columns per block for N1, N2 <= 64 (8 threads per column; 32 measured slower)
-#endif
-#ifndef FS_MINB6
-#define FS_MINB6 3
+#define FS_NC6 16  // pair columns per block when N1, N2 = 64 (8 threads per column; 32 measured slower)
 #endif
 
 namespace {
@@ -54,34 +54,37 @@ CNP_DEV double2 twm(double2 a, double2 w) {  // a·w (forward) or a·conj(w) (in
   return INV ? cmul_conj(a, w) : cmul(a, w);
 }
 
-// Register FFT of length L = R1·R2 over one column, two threads roles (Cooley–Tukey, n = n2 + R2 n1,
+// Register FFT of length L = R1·R2 over one column, two thread roles (Cooley–Tukey, n = n2 + R2 n1,
 // k = k1 + R1 k2):  step 1 — thread n2 holds x[n2 + R2 n1] (n1 < R1), R1-point DFT in registers,
 // twiddle ω_L^{n2 k1}, write A[k1][n2] to the column's exchange area; step 2 — thread k1 reads
 // A[k1][·], R2-point DFT → X[k1 + R1 k2] (k2 < R2).  One shared-memory round trip per pass
-// (the Stockham version of fft_tile.cuh makes one per radix stage).
-template <int LOGL>
-struct RF {
-  static constexpr int L = 1 << LOGL;
-  static constexpr int R1 = LOGL >= 8 ? 16 : LOGL >= 6 ? 8 : 4;
-  static constexpr int R2 = L / R1;
+// (the Stockham version of fft_tile.cuh makes one per radix stage).  The transposed plan (R2, R1)
+// takes its input exactly as the plan (R1, R2) leaves its output in the threads, which MODE 2
+// uses to go from the forward to the inverse transform without an exchange.
+template <int A_, int B_>
+struct RP {
+  static constexpr int R1 = A_, R2 = B_, L = A_ * B_;
   static constexpr int SK = R2 + 1;          // exchange layout A[k1][n2] at k1·SK + n2
   static constexpr int G1 = R1 + 1;          // gather layout x[n2 + R2 n1] at n2·G1 + n1
   static constexpr int S1 = R1 * SK, S2 = R2 * G1;
   static constexpr int SC = (S1 > S2 ? S1 : S2) | 1;  // odd per-column stride: lanes = columns, conflict free
 };
+__host__ __device__ constexpr int rf_r1(int logl) { return logl >= 8 ? 16 : logl >= 6 ? 8 : 4; }
+template <int LOGL>
+using RF = RP<rf_r1(LOGL), (1 << LOGL) / rf_r1(LOGL)>;
+template <int LOGL>
+using RFT = RP<(1 << LOGL) / rf_r1(LOGL), rf_r1(LOGL)>;
 
-template <int LOGL, bool INV>
-CNP_DEV void rf_step1(double2 (&v)[RF<LOGL>::R1], double2* col, const double2* twL, int n2) {
-  using F = RF<LOGL>;
+template <class F, bool INV>
+CNP_DEV void rf_step1(double2 (&v)[F::R1], double2* col, const double2* twL, int n2) {
   dftR<F::R1, INV>(v);
 #pragma unroll
   for (int k1 = 1; k1 < F::R1; ++k1) v[k1] = twm<INV>(v[k1], twL[n2 * k1]);
 #pragma unroll
   for (int k1 = 0; k1 < F::R1; ++k1) col[k1 * F::SK + n2] = v[k1];
 }
-template <int LOGL, bool INV>
-CNP_DEV void rf_step2(double2 (&u)[RF<LOGL>::R2], const double2* col, int k1) {
-  using F = RF<LOGL>;
+template <class F, bool INV>
+CNP_DEV void rf_step2(double2 (&u)[F::R2], const double2* col, int k1) {
 #pragma unroll
   for (int n2 = 0; n2 < F::R2; ++n2) u[n2] = col[k1 * F::SK + n2];
   dftR<F::R2, INV>(u);
@@ -89,50 +92,47 @@ CNP_DEV void rf_step2(double2 (&u)[RF<LOGL>::R2], const double2* col, int k1) {
 
 // compile-time geometry: blocks of NC pair columns; t1 items hold NC columns, family items NC
 // columns = 2 members × NF pairs (half of the block's pairs)
-template <int LOG1, int LOG2>
+template <int MODE, int LOG1, int LOG2>
 struct FsGeo {
   static constexpr int N1 = 1 << LOG1, N2 = 1 << LOG2, N = N1 * N2, H = N / 2;
   static constexpr int MX = LOG1 > LOG2 ? LOG1 : LOG2;
-  static constexpr int NC = MX <= 6 ? FS_NC6 : 16;
+  static constexpr int NC = MX <= 5 ? 32 : MX == 6 ? FS_NC6 : 16;
   static constexpr int NF = NC / 2;
   static constexpr int SCM = RF<LOG1>::SC > RF<LOG2>::SC ? RF<LOG1>::SC : RF<LOG2>::SC;
   static constexpr int off_tw1 = NC * SCM;           // ω_{N1}^j, j < N1
   static constexpr int off_tw2 = off_tw1 + N1;       // ω_{N2}^j
   static constexpr int off_twn = off_tw2 + N2;       // per-item ω_N table [2·max(N1, N2)]
   static constexpr int NTW = 2 * (N1 > N2 ? N1 : N2);
+  static constexpr int off_lam = off_twn + NTW;      // MODE 2: λ1[H+1], λ2[H+1]
+  static constexpr int NLAM = MODE == 2 ? 2 * (H + 1) : 0;
   static constexpr int HI = N / 64;
-  static constexpr int off_g = off_twn + NTW;        // doubles ghi[HI], glo[64]
-  static constexpr size_t bytes = (size_t)(off_g + (HI + 64) / 2 + 1) * 16;
+  static constexpr int off_g = off_lam + NLAM;       // doubles: ghi[HI] glo[64] ihi[HI] ilo[64]
+  static constexpr size_t bytes = (size_t)(off_g + (2 * (HI + 64)) / 2 + 1) * 16;
   static constexpr int TP1 = RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2;
   static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
   static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
-  static constexpr int MINB = MX <= 6 ? FS_MINB6 * 256 / NT : 2;
+  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT : 1) : 2;
 };
 
 }  // namespace
 
-// Work-item order: step s = 0 .. nxb−1+L: A items of block s (s < nxb), then B items of block s−L.
+// Work-item order.  Step s (0 ≤ s < nxb + lag_2) lists n[0] slots for phase 0 of block s, n[1] slots
+// for phase 1 of block s − lag_1 and n[2] slots for phase 2 of block s − lag_2 (lag_0 = 0 ≤ lag_1 ≤
+// lag_2; n[1] = 0 for the two-phase 1D transforms); a slot whose block is out of range is empty
+// (its ticket is skipped), which keeps the ticket → item map a division and a few compares.
 struct FsSched {
-  int nxb, nA, nB, L;
+  int nxb, n[3], lag[3];
   unsigned total;
 };
 
-CNP_DEV void fs_item(const FsSched& S, unsigned T, int& isB, int& xb, int& idx) {
-  const unsigned r1 = (unsigned)S.L * S.nA;
-  const unsigned per = (unsigned)(S.nA + S.nB);
-  const unsigned r2 = (unsigned)(S.nxb - S.L) * per;
-  if (T < r1) {
-    isB = 0; xb = T / S.nA; idx = T - xb * S.nA;
-  } else if (T < r1 + r2) {
-    const unsigned u = T - r1;
-    const int s = S.L + u / per;
-    const int r = u - (s - S.L) * per;
-    if (r < S.nA) { isB = 0; xb = s; idx = r; }
-    else { isB = 1; xb = s - S.L; idx = r - S.nA; }
-  } else {
-    const unsigned u = T - r1 - r2;
-    isB = 1; xb = S.nxb - S.L + u / S.nB; idx = u - (xb - (S.nxb - S.L)) * S.nB;
-  }
+CNP_DEV bool fs_item(const FsSched& S, unsigned T, int& ph, int& xb, int& idx) {
+  const int per = S.n[0] + S.n[1] + S.n[2];
+  const int s = (int)(T / (unsigned)per);
+  int r = (int)(T - (unsigned)s * per);
+  ph = r < S.n[0] ? 0 : r < S.n[0] + S.n[1] ? 1 : 2;
+  idx = ph == 0 ? r : ph == 1 ? r - S.n[0] : r - S.n[0] - S.n[1];
+  xb = s - S.lag[ph];
+  return xb >= 0 && xb < S.nxb;
 }
 
 CNP_DEV void fs_wait(const unsigned* cnt, unsigned target) {
@@ -148,77 +148,114 @@ CNP_DEV void fs_signal(unsigned* cnt) {
   }
 }
 
-// Item kinds.  MODE 0: A items (isB = 0) are t1 items, B items are family items.  MODE 1: A items are
-// family items, B items are t1 items.  Family item index = 2·k2 + h (h: which half of the block's
-// pair columns).  Threads: tid = col + NC·j, j = the role index of the register FFT.  Inputs go
-// straight from global memory (HBM for the input vector / spectrum, L2 for Y) into the step-1
-// registers; the only shared-memory traffic is the exchange of the register FFT.
+struct FsArgs {
+  const double* vin;
+  const double2* spin;
+  double* vout;
+  double2* spout;
+  double2* Y;
+  const double* vscale;
+  const double* gam;
+  const double* igam;
+  const double2* lam1;
+  const double2* lam2;
+  const double* ex;
+  const double* ey;
+  double tau, tau_shift;
+  int W, ld, nx, accumulate, debug_sign, no_discard;
+  unsigned* cnt;
+  unsigned* ticket;
+  unsigned tick_base, base;
+};
+
+// Item kinds by mode and phase:
+//   MODE 0: phase 0 forward t1 items (input → Y), phase 2 forward family items (Y → spectrum)
+//   MODE 1: phase 0 inverse family items (spectrum → Y), phase 2 inverse t1 items (Y → output)
+//   MODE 2: phase 0 forward t1 items, phase 1 fused family items (Y → forward, divide, inverse → Y),
+//           phase 2 inverse t1 items
+// Family item index = 2·k2 + h (h: which half of the block's pair columns).  Threads:
+// tid = col + NC·j, j = the role index of the register FFT.
 template <int MODE, int LOG1, int LOG2>
-__global__ void __launch_bounds__(FsGeo<LOG1, LOG2>::NT, FsGeo<LOG1, LOG2>::MINB)
-    k_fstep(const double* __restrict__ vin, const double2* __restrict__ spin, double* __restrict__ vout,
-            double2* __restrict__ spout, double2* __restrict__ Y, const double* __restrict__ vscale, int W, int nx,
-            const double* __restrict__ gtab, int accumulate, int debug_sign, FsSched S, unsigned* cnt,
-            unsigned* ticket, unsigned tick_base, unsigned cnt_target, int no_discard) {
-  using G = FsGeo<LOG1, LOG2>;
-  using F1 = RF<LOG1>;  // family items: length N1
-  using F2 = RF<LOG2>;  // t1 items: length N2
+__global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1, LOG2>::MINB)
+    k_fstep(FsArgs a, FsSched S) {
+  using G = FsGeo<MODE, LOG1, LOG2>;
+  using F1 = RF<LOG1>;   // family items: length N1
+  using F1T = RFT<LOG1>; // MODE 2: the inverse over k1, transposed plan
+  using F2 = RF<LOG2>;   // t1 items: length N2
   constexpr int NT = G::NT;
   constexpr int N1 = G::N1, N2 = G::N2, N = G::N, H = G::H, NC = G::NC, NF = G::NF;
   constexpr int X = 2 * NC;  // real columns per block
   const int tid = threadIdx.x;
   const int col = tid % NC, j = tid / NC;
+  const int W = a.W;
   double2* const buf = tf_smem;
   double2* const tw1 = tf_smem + G::off_tw1;
   double2* const tw2 = tf_smem + G::off_tw2;
   double2* const twn = tf_smem + G::off_twn;
+  double2* const l1s = tf_smem + G::off_lam;
+  double2* const l2s = l1s + (H + 1);
   double* const ghi = reinterpret_cast<double*>(tf_smem + G::off_g);
   double* const glo = ghi + G::HI;
+  double* const ihi = glo + 64;
+  double* const ilo = ihi + G::HI;
   __shared__ unsigned s_tk[2];  // ticket of item i in s_tk[i & 1]
 
-  // ---- per-CTA tables once: ω_{N1}, ω_{N2}; Γ_α (MODE 0) or 1/(NΓ_α) (MODE 1) as two-level tables
-  //      g_t = ghi[t >> 6]·glo[t & 63] (glo of MODE 1 carries the factor N back)
-  const double sg = debug_sign ? -1.0 : 1.0;
+  // ---- per-CTA tables once: ω_{N1}, ω_{N2}; Γ_α and 1/(NΓ_α) as two-level tables
+  //      g_t = ghi[t >> 6]·glo[t & 63], 1/(Nγ_t) = ihi[t >> 6]·ilo[t & 63] (ilo carries the N back)
+  const double sg = a.debug_sign ? -1.0 : 1.0;
   for (int q = tid; q < N1; q += NT) { double2 w = expi_neg(q, N1); w.y *= sg; tw1[q] = w; }
   for (int q = tid; q < N2; q += NT) { double2 w = expi_neg(q, N2); w.y *= sg; tw2[q] = w; }
-  for (int q = tid; q < G::HI; q += NT) ghi[q] = __ldg(gtab + q * 64);
-  for (int q = tid; q < 64; q += NT) glo[q] = MODE == 0 ? __ldg(gtab + q) : (double)N * __ldg(gtab + q);
-  const double s = (MODE == 0 && vscale) ? *vscale : 1.0;
-  if (tid == 0) s_tk[0] = atomicAdd(ticket, 1u) - tick_base;
+  if (MODE != 1) {
+    for (int q = tid; q < G::HI; q += NT) ghi[q] = __ldg(a.gam + q * 64);
+    for (int q = tid; q < 64; q += NT) glo[q] = __ldg(a.gam + q);
+  }
+  if (MODE != 0) {
+    for (int q = tid; q < G::HI; q += NT) ihi[q] = __ldg(a.igam + q * 64);
+    for (int q = tid; q < 64; q += NT) ilo[q] = (double)N * __ldg(a.igam + q);
+  }
+  if (MODE == 2)
+    for (int q = tid; q <= H; q += NT) { l1s[q] = a.lam1[q]; l2s[q] = a.lam2[q]; }
+  const double s = (MODE != 1 && a.vscale) ? *a.vscale : 1.0;
+  if (tid == 0) s_tk[0] = atomicAdd(a.ticket, 1u) - a.tick_base;
 
   for (int it = 0;; ++it) {
     __syncthreads();  // previous item done with buf / twn; s_tk[it & 1] published
     const unsigned T = s_tk[it & 1];
     if (T >= S.total) break;
-    // the next ticket is requested now and published in the other slot at the end of this item
-    unsigned nxt = 0;
-    if (tid == 0) nxt = atomicAdd(ticket, 1u);
-    int isB, xb, idx;
-    fs_item(S, T, isB, xb, idx);
+    unsigned nxt = 0;  // next ticket requested now, published in the other slot at the end
+    if (tid == 0) nxt = atomicAdd(a.ticket, 1u);
+    int ph, xb, idx;
+    if (!fs_item(S, T, ph, xb, idx)) {  // empty slot (schedule edge)
+      if (tid == 0) s_tk[(it + 1) & 1] = nxt - a.tick_base;
+      continue;
+    }
     const int col0 = xb * X;
-    double2* const Yb = Y + (size_t)xb * N * NC;  // block's Y: [t1][k2][c], c < NC
+    double2* const Yb = a.Y + (size_t)xb * N * NC;  // block's Y: [t1][k2][c], c < NC
+    const bool fwd_t1 = MODE != 1 && ph == 0;
+    const bool inv_t1 = MODE != 0 && ph == 2;
+    if (ph > 0) fs_wait(a.cnt + xb, a.base + (unsigned)(ph == 1 ? S.n[0] : S.n[0] + S.n[1]));
 
-    if ((MODE == 0 && !isB) || (MODE == 1 && isB)) {
-      // ================= t1 items (length N2): MODE 0 pass A, MODE 1 pass B'
+    if (fwd_t1 || inv_t1) {
+      // ================= t1 items (length N2): forward pass A or inverse pass B'
       double2* const cb = buf + col * F2::SC;
       const int t1 = idx;
       const int mycol = col0 + 2 * col;
-      const bool padA = mycol >= nx, padB = mycol + 1 >= nx, colok = mycol < W;
-      if (MODE == 0)
+      const int xin = mycol % a.ld;
+      const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
+      if (fwd_t1)
         for (int q = tid; q < N2; q += NT) {  // ω_N^{t1 k2}
           double2 w = expi_neg((t1 * q) & (N - 1), N);
           w.y *= sg;
           twn[q] = w;
         }
-      else
-        fs_wait(cnt + xb, cnt_target);
       if (j < F2::R2) {
         const int n2 = j;
         double2 v[F2::R1];
-        if (MODE == 0) {
+        if (fwd_t1) {
 #pragma unroll
           for (int n1 = 0; n1 < F2::R1; ++n1) {
             const int t = t1 + N1 * (n2 + F2::R2 * n1);
-            v[n1] = colok ? __ldcs(reinterpret_cast<const double2*>(vin + (int64_t)t * W + mycol))
+            v[n1] = colok ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
                           : make_double2(0.0, 0.0);
           }
 #pragma unroll
@@ -226,47 +263,51 @@ __global__ void __launch_bounds__(FsGeo<LOG1, LOG2>::NT, FsGeo<LOG1, LOG2>::MINB
             const int t = t1 + N1 * (n2 + F2::R2 * n1);
             v[n1] = cscale(v[n1], ghi[t >> 6] * glo[t & 63] * s);
           }
+          rf_step1<F2, false>(v, cb, tw2, n2);
         } else {
 #pragma unroll
           for (int n1 = 0; n1 < F2::R1; ++n1) v[n1] = __ldcg(Yb + ((size_t)t1 * N2 + n2 + F2::R2 * n1) * NC + col);
+          rf_step1<F2, true>(v, cb, tw2, n2);
         }
-        rf_step1<LOG2, MODE == 1>(v, cb, tw2, n2);
       }
       __syncthreads();
-      if (MODE == 1 && !no_discard) {  // this t1's Y rows: N2·NC·16 B, contiguous
+      if (inv_t1 && !a.no_discard) {  // this t1's Y rows: N2·NC·16 B, contiguous, last reader
         const char* src = reinterpret_cast<const char*>(Yb + (size_t)t1 * N2 * NC);
         for (int q = tid; q < N2 * NC * 16 / 128; q += NT) discard_l2(src + q * 128);
       }
       if (j < F2::R1) {
         const int k1 = j;
         double2 u[F2::R2];
-        rf_step2<LOG2, MODE == 1>(u, cb, k1);
-        if (MODE == 0) {
+        if (fwd_t1) {
+          rf_step2<F2, false>(u, cb, k1);
 #pragma unroll
           for (int k2 = 0; k2 < F2::R2; ++k2) {
             const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
             Yb[((size_t)t1 * N2 + kk) * NC + col] = cmul(u[k2], twn[kk]);
           }
-        } else if (colok) {
+        } else {
+          rf_step2<F2, true>(u, cb, k1);
+          if (colok) {
 #pragma unroll
-          for (int k2 = 0; k2 < F2::R2; ++k2) {
-            const int t = t1 + N1 * (k1 + F2::R1 * k2);
-            const double g = ghi[t >> 6] * glo[t & 63];
-            double2 val = make_double2(padA ? 0.0 : u[k2].x * g, padB ? 0.0 : u[k2].y * g);
-            double2* dst = reinterpret_cast<double2*>(vout + (int64_t)t * W + mycol);
-            if (accumulate) {
-              const double2 o = *dst;
-              val.x += o.x;
-              val.y += o.y;
+            for (int k2 = 0; k2 < F2::R2; ++k2) {
+              const int t = t1 + N1 * (k1 + F2::R1 * k2);
+              const double g = ihi[t >> 6] * ilo[t & 63];
+              double2 val = make_double2(padA ? 0.0 : u[k2].x * g, padB ? 0.0 : u[k2].y * g);
+              double2* dst = reinterpret_cast<double2*>(a.vout + (int64_t)t * W + mycol);
+              if (a.accumulate) {
+                const double2 o = *dst;
+                val.x += o.x;
+                val.y += o.y;
+              }
+              stg_cs2(dst, val);
             }
-            stg_cs2(dst, val);
           }
         }
       }
-      if (MODE == 0) fs_signal(cnt + xb);
+      if (fwd_t1) fs_signal(a.cnt + xb);
     } else {
-      // ================= family items {k2, N2 − k2} × half block h (length N1): MODE 0 pass B,
-      //                   MODE 1 pass A'.  Column col = m·NF + p: member m, pair h·NF + p.
+      // ================= family items {k2, N2 − k2} × half block h (length N1).  Column
+      //                   col = m·NF + p: member m, pair h·NF + p.
       const int k2 = idx >> 1, h = idx & 1;
       const int k2m = (N2 - k2) & (N2 - 1);
       const bool two = k2m != k2;
@@ -275,90 +316,147 @@ __global__ void __launch_bounds__(FsGeo<LOG1, LOG2>::NT, FsGeo<LOG1, LOG2>::MINB
       const bool active = m == 0 || two;
       const int gp = h * NF + p;
       const int mycol = col0 + 2 * gp;
-      const bool padA = mycol >= nx, padB = mycol + 1 >= nx, colok = mycol < W;
+      const int xin = mycol % a.ld;
+      const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
       double2* const fb = buf + col * F1::SC;
-      if (MODE == 0) {
-        fs_wait(cnt + xb, cnt_target);
+      // partner of frequency index ko of this column (Hermitian pairing k ↔ N − k)
+      auto partner = [&](int ko, int& pcol, int& pko) {
+        if (m == 1) { pcol = col - NF; pko = N1 - 1 - ko; }
+        else if (k2 == 0) { pcol = col; pko = (N1 - ko) & (N1 - 1); }
+        else if (!two) { pcol = col; pko = N1 - 1 - ko; }
+        else { pcol = col + NF; pko = N1 - 1 - ko; }
+      };
+      if (MODE == 0 || MODE == 2) {
+        // ---- forward pass B over t1: Y rows (t1, km) of this half block
         if (j < F1::R2) {
           const int n2 = j;
           double2 v[F1::R1];
 #pragma unroll
           for (int n1 = 0; n1 < F1::R1; ++n1)
             v[n1] = active ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp) : make_double2(0.0, 0.0);
-          rf_step1<LOG1, false>(v, fb, tw1, n2);
+          rf_step1<F1, false>(v, fb, tw1, n2);
         }
         __syncthreads();
-        if (!no_discard) {  // rows (t1, km): NF·16 B = NF/8 lines at each of N1 rows, 2 members
+        if (MODE == 0 && !a.no_discard) {  // rows (t1, km): NF·16 B at each of N1 rows, 2 members
           constexpr int LPR = NF * 16 / 128;
           for (int q = tid; q < 2 * N1 * LPR; q += NT) {
             const int mm = q / (N1 * LPR), r = q - mm * N1 * LPR;
             const int t1 = r / LPR, l = r - t1 * LPR;
             if (mm == 1 && !two) continue;
-            const char* a = reinterpret_cast<const char*>(Yb + ((size_t)t1 * N2 + (mm ? k2m : k2)) * NC + h * NF);
-            discard_l2(a + l * 128);
+            const char* ad = reinterpret_cast<const char*>(Yb + ((size_t)t1 * N2 + (mm ? k2m : k2)) * NC + h * NF);
+            discard_l2(ad + l * 128);
           }
         }
         double2 u[F1::R2];
-        if (j < F1::R1) rf_step2<LOG1, false>(u, fb, j);
+        if (j < F1::R1) rf_step2<F1, false>(u, fb, j);
         __syncthreads();  // every thread has read its exchange row: the areas now take X
         if (j < F1::R1) {
 #pragma unroll
           for (int k2i = 0; k2i < F1::R2; ++k2i) fb[j * F1::SK + k2i] = u[k2i];  // X[k1 + R1 k2] at k1·SK + k2
         }
-        __syncthreads();
-        if (j < F1::R1 && active && colok) {
-          const int k1 = j;
-#pragma unroll
-          for (int k2i = 0; k2i < F1::R2; ++k2i) {
-            const int ko = k1 + F1::R1 * k2i;  // outer frequency: spectrum row km + N2·ko
-            const int k = km + N2 * ko;
-            if (k > H) continue;
-            int pcol, pko;
-            if (m == 1) { pcol = col - NF; pko = N1 - 1 - ko; }
-            else if (k2 == 0) { pcol = col; pko = (N1 - ko) & (N1 - 1); }
-            else if (!two) { pcol = col; pko = N1 - 1 - ko; }
-            else { pcol = col + NF; pko = N1 - 1 - ko; }
-            const double2 zm = buf[pcol * F1::SC + (pko % F1::R1) * F1::SK + pko / F1::R1];
-            double2 xa, xbv;
-            fs_separate(u[k2i], zm, xa, xbv);
-            if (padA) xa = make_double2(0.0, 0.0);
-            if (padB) xbv = make_double2(0.0, 0.0);
-            double2* o = spout + (int64_t)k * W + mycol;
-            stg_cs2(o, xa);
-            stg_cs2(o + 1, xbv);
+        if (MODE == 2)
+          for (int q = tid; q < N1; q += NT) {  // ω_N^{k2 t1}, ω_N^{k2m t1} (conjugated at use)
+            double2 w0 = expi_neg((k2 * q) & (N - 1), N), w1 = expi_neg((k2m * q) & (N - 1), N);
+            w0.y *= sg;
+            w1.y *= sg;
+            twn[q] = w0;
+            twn[N1 + q] = w1;
           }
+        __syncthreads();
+        if (MODE == 0) {
+          if (j < F1::R1 && active && colok) {
+            const int k1 = j;
+#pragma unroll
+            for (int k2i = 0; k2i < F1::R2; ++k2i) {
+              const int ko = k1 + F1::R1 * k2i;  // outer frequency: spectrum row km + N2·ko
+              const int k = km + N2 * ko;
+              if (k > H) continue;
+              int pcol, pko;
+              partner(ko, pcol, pko);
+              const double2 zm = buf[pcol * F1::SC + (pko % F1::R1) * F1::SK + pko / F1::R1];
+              double2 xa, xbv;
+              fs_separate(u[k2i], zm, xa, xbv);
+              if (padA) xa = make_double2(0.0, 0.0);
+              if (padB) xbv = make_double2(0.0, 0.0);
+              double2* o = a.spout + (int64_t)k * W + mycol;
+              stg_cs2(o, xa);
+              stg_cs2(o + 1, xbv);
+            }
+          }
+        } else {
+          // ---- MODE 2: divide every frequency of the member by (λ1_k − λ2_k μ) per real column,
+          //      repack, inverse over k1 with the transposed plan (input = this thread's values)
+          double2 z[F1::R2];
+          if (j < F1::R1) {
+            const int k1 = j;
+            double mua = 0.0, mub = 0.0;
+            if (colok && !padA) {
+              const int yy = mycol / a.ld;
+              mua = a.tau * (a.ex[xin] + a.ey[yy]) + a.tau_shift;
+              if (!padB) mub = a.tau * (a.ex[xin + 1] + a.ey[yy]) + a.tau_shift;
+            }
+#pragma unroll
+            for (int k2i = 0; k2i < F1::R2; ++k2i) {
+              const int ko = k1 + F1::R1 * k2i;
+              const int k = km + N2 * ko;
+              int pcol, pko;
+              partner(ko, pcol, pko);
+              const double2 zm = buf[pcol * F1::SC + (pko % F1::R1) * F1::SK + pko / F1::R1];
+              double2 xa, xbv;
+              fs_separate(u[k2i], zm, xa, xbv);
+              const double2 l1 = k <= H ? l1s[k] : cconj(l1s[N - k]);
+              const double2 l2 = k <= H ? l2s[k] : cconj(l2s[N - k]);
+              xa = cmul(xa, crecip(csub(l1, cscale(l2, mua))));
+              xbv = cmul(xbv, crecip(csub(l1, cscale(l2, mub))));
+              z[k2i] = (k == 0 || k == H) ? make_double2(xa.x, xbv.x) : fs_pack(xa, xbv);
+            }
+          }
+          __syncthreads();  // all partner reads of X done: the areas take the inverse exchange
+          if (j < F1T::R2) rf_step1<F1T, true>(z, fb, tw1, j);
+          __syncthreads();
+          if (j < F1T::R1 && active) {
+            const int k1 = j;
+            double2 w2[F1T::R2];
+            rf_step2<F1T, true>(w2, fb, k1);
+#pragma unroll
+            for (int k2i = 0; k2i < F1T::R2; ++k2i) {
+              const int t1 = k1 + F1T::R1 * k2i;
+              Yb[((size_t)t1 * N2 + km) * NC + gp] = cmul_conj(w2[k2i], twn[m * N1 + t1]);
+            }
+          }
+          fs_signal(a.cnt + xb);
         }
       } else {
-        // gather Z for both members from the stored rows min(k, N − k) into the step-1 layout
-        // x[n2 + R2 n1] at n2·G1 + n1
+        // ---- MODE 1 pass A': gather Z for both members from the stored rows min(k, N − k) into
+        //      the step-1 layout x[n2 + R2 n1] at n2·G1 + n1
         const int n0 = (H - k2) / N2 + 1;
         const int n1r = two ? (H - k2m) / N2 + 1 : 0;
         constexpr int GIT = (N1 * NF + NT - 1) / NT;  // ≥ (n0 + n1r)·NF / NT
         double2 ga[GIT], gb[GIT];
 #pragma unroll
-        for (int it = 0; it < GIT; ++it) {  // all row loads first (memory-level parallelism)
-          const int q = tid + it * NT;
-          ga[it] = gb[it] = make_double2(0.0, 0.0);
+        for (int i2 = 0; i2 < GIT; ++i2) {  // all row loads first (memory-level parallelism)
+          const int q = tid + i2 * NT;
+          ga[i2] = gb[i2] = make_double2(0.0, 0.0);
           if (q < (n0 + n1r) * NF) {
             const int r = q / NF, pp = q - r * NF;
             const int k = r < n0 ? k2 + N2 * r : k2m + N2 * (r - n0);
             const int gcol = col0 + 2 * (h * NF + pp);
             if (gcol < W) {
-              const double2* src = spin + (int64_t)k * W + gcol;
-              ga[it] = ldg_cs2(src);
-              gb[it] = ldg_cs2(src + 1);
+              const double2* src = a.spin + (int64_t)k * W + gcol;
+              ga[i2] = ldg_cs2(src);
+              gb[i2] = ldg_cs2(src + 1);
             }
           }
         }
 #pragma unroll
-        for (int it = 0; it < GIT; ++it) {
-          const int q = tid + it * NT;
+        for (int i2 = 0; i2 < GIT; ++i2) {
+          const int q = tid + i2 * NT;
           if (q >= (n0 + n1r) * NF) continue;
           const int r = q / NF, pp = q - r * NF;
           const bool m1 = r >= n0;
           const int k1o = m1 ? r - n0 : r;
           const int k = (m1 ? k2m : k2) + N2 * k1o;
-          const double2 xa = ga[it], xbv = gb[it];
+          const double2 xa = ga[i2], xbv = gb[i2];
           double2 zk, zp;
           if (k == 0 || k == H) {
             zk = zp = make_double2(xa.x, xbv.x);
@@ -388,24 +486,24 @@ __global__ void __launch_bounds__(FsGeo<LOG1, LOG2>::NT, FsGeo<LOG1, LOG2>::MINB
           for (int n1 = 0; n1 < F1::R1; ++n1) v[n1] = fb[j * F1::G1 + n1];
         }
         __syncthreads();  // the gather layout is read: the areas now take the exchange layout
-        if (j < F1::R2) rf_step1<LOG1, true>(v, fb, tw1, j);
+        if (j < F1::R2) rf_step1<F1, true>(v, fb, tw1, j);
         __syncthreads();
         if (j < F1::R1 && active) {
           const int k1 = j;
           double2 u[F1::R2];
-          rf_step2<LOG1, true>(u, fb, k1);
+          rf_step2<F1, true>(u, fb, k1);
 #pragma unroll
           for (int k2i = 0; k2i < F1::R2; ++k2i) {
             const int t1 = k1 + F1::R1 * k2i;
             Yb[((size_t)t1 * N2 + km) * NC + gp] = cmul_conj(u[k2i], twn[m * N1 + t1]);
           }
         }
-        fs_signal(cnt + xb);
+        fs_signal(a.cnt + xb);
       }
     }
     // publish the next ticket in the other slot (its readers passed this item's first barrier; the
     // loop-top barrier publishes it)
-    if (tid == 0) s_tk[(it + 1) & 1] = nxt - tick_base;
+    if (tid == 0) s_tk[(it + 1) & 1] = nxt - a.tick_base;
   }
 }
 
@@ -417,24 +515,31 @@ static void fs_logs(int N, int& l1, int& l2) {
   l2 = logN - l1;
 }
 
-bool fstep_ok(const cnpint_ctx* c) { return c->dim == 1 && c->N >= 2048 && c->N <= 65536 && c->d_fsY; }
+// 2D: from N = 2048 on (the cluster kernel's own range ends in C = 8 clusters there); at N ≤ 1024 the
+// items of the three-phase pass are 8–16 KB and the cluster kernel measured faster (c4: 326 vs 781
+// µs, profiles/r01_k6_sweep.txt)
+static bool fs_shape_ok(int dim, int N) {
+  return dim == 1 ? (N >= 2048 && N <= 65536) : (N >= 2048 && N <= 16384);
+}
+bool fstep_ok(const cnpint_ctx* c) { return fs_shape_ok(c->dim, c->N) && c->d_fsY; }
 
 static int fs_nc(int N) {
   int l1, l2;
   fs_logs(N, l1, l2);
   const int mx = l1 > l2 ? l1 : l2;
-  return mx <= 6 ? FS_NC6 : 16;
+  return mx <= 5 ? 32 : mx == 6 ? FS_NC6 : 16;
 }
-int fstep_nxb(int N, int64_t ld) { return (int)((ld + 2 * fs_nc(N) - 1) / (2 * fs_nc(N))); }
+// W = real columns of a time row (1D: ld; 2D: ny·ld)
+int fstep_nxb(int N, int64_t W) { return (int)((W + 2 * fs_nc(N) - 1) / (2 * fs_nc(N))); }
 // Y: nxb blocks of N × NC complex (the last block padded to whole pairs of NC columns)
-size_t fstep_y_bytes(int dim, int N, int64_t ld) {
-  return (dim == 1 && N >= 2048 && N <= 65536) ? (size_t)fstep_nxb(N, ld) * N * fs_nc(N) * 16 : 0;
+size_t fstep_y_bytes(int dim, int N, int64_t W) {
+  return fs_shape_ok(dim, N) ? (size_t)fstep_nxb(N, W) * N * fs_nc(N) * 16 : 0;
 }
 
 template <int MODE, int LOG1, int LOG2>
 static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* spin, double* vout, double2* spout,
                              const double* vscale, int accumulate) {
-  using G = FsGeo<LOG1, LOG2>;
+  using G = FsGeo<MODE, LOG1, LOG2>;
   auto kern = k_fstep<MODE, LOG1, LOG2>;
   static int per_sm = 0;
   if (!per_sm) {
@@ -443,27 +548,36 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, G::bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
-  const int W = (int)c->ld;
+  const int W = (int)c->slice;  // real columns per time row
+  const int nfam = 2 * (G::N2 / 2 + 1);
   FsSched S;
   S.nxb = (W + 2 * G::NC - 1) / (2 * G::NC);
-  S.nA = MODE == 0 ? G::N1 : 2 * (G::N2 / 2 + 1);
-  S.nB = MODE == 0 ? 2 * (G::N2 / 2 + 1) : G::N1;
-  S.total = (unsigned)S.nxb * (S.nA + S.nB);
+  S.n[0] = MODE == 1 ? nfam : G::N1;
+  S.n[1] = MODE == 2 ? nfam : 0;
+  S.n[2] = MODE == 0 ? nfam : G::N1;
+  const int per = S.n[0] + S.n[1] + S.n[2];
   const int grid_max = per_sm * c->num_sms;
-  const int grid = (int)(S.total < (unsigned)grid_max ? S.total : (unsigned)grid_max);
-  // lag: enough steps between a block's A and B items that the CTAs in flight (≈ grid) finish the
-  // A items first
-  int L = 2 * ((grid + S.nA + S.nB - 1) / (S.nA + S.nB)) + 1;
+  // lag: enough steps between a block's phases that the CTAs in flight (≈ grid) finish the earlier
+  // phase first
+  int L = 2 * ((grid_max + per - 1) / per) + 1;
   if (const char* e = getenv("CNPINT_FS_LAG")) L = atoi(e) > 0 ? atoi(e) : L;
-  S.L = L < S.nxb ? L : S.nxb;
-  const unsigned target = c->fs_cnt + (unsigned)S.nA;
+  S.lag[0] = 0;
+  S.lag[1] = L;
+  S.lag[2] = MODE == 2 ? 2 * L : L;
+  S.total = (unsigned)(S.nxb + S.lag[2]) * (unsigned)per;  // including the empty edge slots
+  const int grid = (int)(S.total < (unsigned)grid_max ? S.total : (unsigned)grid_max);
   static int no_discard = -1;
   if (no_discard < 0) no_discard = getenv("CNPINT_FS_NODISCARD") ? 1 : 0;
-  kern<<<grid, G::NT, G::bytes, c->stream>>>(vin, spin, vout, spout, (double2*)c->d_fsY, vscale, W, c->nx,
-                                            MODE == 0 ? c->d_gam : c->d_igam, accumulate, c->debug & 1, S,
-                                            c->d_fscnt, c->d_fscnt + S.nxb, c->fs_tick, target, no_discard);
-  c->fs_cnt = target;
-  c->fs_tick += S.total + (unsigned)grid;  // every CTA also takes one ticket past the end
+  FsArgs a;
+  a.vin = vin; a.spin = spin; a.vout = vout; a.spout = spout; a.Y = (double2*)c->d_fsY; a.vscale = vscale;
+  a.gam = c->d_gam; a.igam = c->d_igam; a.lam1 = c->d_lam1; a.lam2 = c->d_lam2; a.ex = c->d_ex; a.ey = c->d_ey;
+  a.tau = c->tau_p; a.tau_shift = c->tau_p * c->shift;
+  a.W = W; a.ld = (int)c->ld; a.nx = c->nx; a.accumulate = accumulate; a.debug_sign = c->debug & 1;
+  a.no_discard = no_discard;
+  a.cnt = c->d_fscnt; a.ticket = c->d_fscnt + S.nxb; a.tick_base = c->fs_tick; a.base = c->fs_cnt;
+  kern<<<grid, G::NT, G::bytes, c->stream>>>(a, S);
+  c->fs_cnt += (unsigned)(S.n[0] + S.n[1]);  // phases 0 and 1 count per block
+  c->fs_tick += S.total + (unsigned)grid;    // every CTA also takes one ticket past the end
   return cudaGetLastError();
 }
 
@@ -474,7 +588,11 @@ static cudaError_t fs_dispatch(cnpint_ctx* c, const double* vin, const double2* 
   fs_logs(c->N, l1, l2);
 #define FS_CASE(A, B) \
   if (l1 == A && l2 == B) return fs_launch<MODE, A, B>(c, vin, spin, vout, spout, vscale, accumulate);
-  FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7) FS_CASE(8, 7) FS_CASE(8, 8)
+  if constexpr (MODE == 2) {
+    FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7)
+  } else {
+    FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7) FS_CASE(8, 7) FS_CASE(8, 8)
+  }
 #undef FS_CASE
   return cudaErrorInvalidValue;
 }
@@ -489,5 +607,11 @@ cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int 
   cnp_prof_begin(c, KID_FFT_INV);
   cudaError_t e = fs_dispatch<1>(c, nullptr, zhat, z, nullptr, nullptr, accumulate);
   cnp_prof_end(c, KID_FFT_INV, 8.0 * cnp_units(c) * (accumulate ? 2.0 : 1.0) + 16.0 * cnp_spec_units(c));
+  return e;
+}
+cudaError_t launch_fstep_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
+  cnp_prof_begin(c, KID_TIMEPASS2D);
+  cudaError_t e = fs_dispatch<2>(c, in, nullptr, out, nullptr, vscale, 0);
+  cnp_prof_end(c, KID_TIMEPASS2D, 16.0 * cnp_units(c));
   return e;
 }

@@ -216,7 +216,8 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
   return cudaGetLastError();
 }
 
-// 1D with N >= 2048: four-step kernel of k_fstep.cu (debug bit 16 opts out); other N <= 16384: the
+// 1D with N >= 2048 and the 2D time pass with N >= 2048: four-step kernel of k_fstep.cu (debug bit 16
+// opts out); other N <= 16384: the
 // cluster kernels of k_tfft.cu; larger N (2D) stays here (one column per CTA, even/odd time
 // packing).  debug bit 8 forces this path (cross-check in the parity tests).
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what) {
@@ -230,6 +231,7 @@ cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int 
   return run_fft<1>(c, nullptr, zhat, z, nullptr, nullptr, accumulate);
 }
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
+  if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_pass_2d(c, in, out, vscale);
   if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_pass_2d(c, in, out, vscale);
   return run_fft<2>(c, in, nullptr, out, nullptr, vscale, 0);
 }

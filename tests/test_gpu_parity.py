@@ -238,8 +238,28 @@ def test_dst_paths(name, debug):
     assert s.device_status() == 0
 
 
+@pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2"])
+@pytest.mark.parametrize("debug", [0, 16])
+def test_timepass_2d_paths(name, debug):
+    """2D time pass: the three-phase four-step kernel (N >= 2048, debug 0) and the cluster kernel
+    (debug 16) both give the oracle's P⁻¹."""
+    w = SMALL[name]
+    s = solver_for(w)
+    s.set_debug(debug)
+    op = problem.build_operator(w)
+    for v in synth.random_vectors(w, 2, 47):
+        z = s.empty()
+        for _ in range(2):  # repeated launches: the four-step counters carry across launches
+            s.apply_Pinv(s.to_device(v), z)
+        zg = s.to_host(z)
+        assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12, (name, debug)
+        if s.ld > w.n:
+            assert float(z[..., w.n:].abs().max()) == 0.0
+    assert s.device_status() == 0
+
+
 @pytest.mark.parametrize("debug", [1, 2])
-@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2", "2d_n255_N8"])
+@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2", "2d_n255_N8", "2d_n63_N2048"])
 def test_negative_controls_break_parity(debug, name):
     """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail (cluster and
     four-step FFT paths)."""
