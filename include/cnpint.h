@@ -217,7 +217,8 @@ cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, v
  * parity suite runs the alternatives on the same inputs): 4 = Toeplitz shifted solves through the
  * generic merge tree instead of the tabulated fast tree; 8 = the one-column time FFT kernel
  * (N <= 16384); 16 = the cluster time FFT instead of the four-step kernel for 1D N >= 2048;
- * 32 = the shared-memory Stockham DST kernel for every 2D sine pass. */
+ * 32 = the shared-memory Stockham DST kernel for every 2D sine pass; 64 = the cluster kernel instead
+ * of the register time pass for 2D N = 256, 512. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

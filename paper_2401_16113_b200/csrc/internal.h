@@ -111,6 +111,8 @@ bool fstep_ok(const cnpint_ctx* c);
 size_t fstep_y_bytes(int dim, int N, int64_t W);
 int fstep_nxb(int N, int64_t W);
 cudaError_t launch_fstep_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
+bool tpass_ok(const cnpint_ctx* c);
+cudaError_t launch_tpass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 cudaError_t launch_fstep_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,

@@ -52,6 +52,9 @@ SMALL = {
     "2d_n63_N2048": synth.scaled(synth.C4, 63, 2048, alpha=0.01),
     # E = 2(n+1) = 512: the register DST kernel of the y pass (k_dst_r); ragged pair tiles (ld/2 = 128)
     "2d_n255_N8": synth.scaled(synth.C4, 255, 8, alpha=0.05),
+    # register 2D time pass (k_tpass.cu): N = 256 and 512
+    "2d_n15_N512": synth.scaled(synth.C4, 15, 512, alpha=0.01),
+    "2d_n31_N256": synth.scaled(synth.C4, 31, 256, alpha=0.02),
     # NEXT #1: time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8)
     "1d_tv": synth.scaled(synth.C1T, 63, 64, alpha=0.01),
     "1d_tv_price": synth.scaled(synth.C3, 127, 128, alpha=0.01, dt_rate=0.3),
@@ -238,11 +241,11 @@ def test_dst_paths(name, debug):
     assert s.device_status() == 0
 
 
-@pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2"])
-@pytest.mark.parametrize("debug", [0, 16])
+@pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2", "2d_n15_N512", "2d_n31_N256"])
+@pytest.mark.parametrize("debug", [0, 16, 64])
 def test_timepass_2d_paths(name, debug):
-    """2D time pass: the three-phase four-step kernel (N >= 2048, debug 0) and the cluster kernel
-    (debug 16) both give the oracle's P⁻¹."""
+    """2D time pass: the three-phase four-step kernel (N >= 2048), the register kernel (N = 256, 512)
+    — both default (debug 0) — and the cluster kernel (debug 16 / 64) all give the oracle's P⁻¹."""
     w = SMALL[name]
     s = solver_for(w)
     s.set_debug(debug)
@@ -259,7 +262,7 @@ def test_timepass_2d_paths(name, debug):
 
 
 @pytest.mark.parametrize("debug", [1, 2])
-@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2", "2d_n255_N8", "2d_n63_N2048"])
+@pytest.mark.parametrize("name", ["1d_small", "1d_N4096_C2", "2d_n255_N8", "2d_n63_N2048", "2d_n15_N512"])
 def test_negative_controls_break_parity(debug, name):
     """Flipped twiddle sign / printed Eq. eigCx ordering must make the parity check fail (cluster and
     four-step FFT paths)."""
