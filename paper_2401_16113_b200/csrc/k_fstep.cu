@@ -163,6 +163,7 @@ struct FsArgs {
   const double* ey;
   double tau, tau_shift;
   int W, ld, nx, accumulate, debug_sign, no_discard;
+  int skip;  // timing experiments only (CNPINT_FS_SKIP): 1 no input loads, 2 no spectrum stores, 4 no Y traffic
   unsigned* cnt;
   unsigned* ticket;
   unsigned tick_base, base;
@@ -255,8 +256,8 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
           for (int n1 = 0; n1 < F2::R1; ++n1) {
             const int t = t1 + N1 * (n2 + F2::R2 * n1);
-            v[n1] = colok ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
-                          : make_double2(0.0, 0.0);
+            v[n1] = (colok && !(a.skip & 1)) ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
+                                             : make_double2(0.0, 0.0);
           }
 #pragma unroll
           for (int n1 = 0; n1 < F2::R1; ++n1) {
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
           for (int k2 = 0; k2 < F2::R2; ++k2) {
             const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
-            Yb[((size_t)t1 * N2 + kk) * NC + col] = cmul(u[k2], twn[kk]);
+            if (!(a.skip & 4)) Yb[((size_t)t1 * N2 + kk) * NC + col] = cmul(u[k2], twn[kk]);
           }
         } else {
           rf_step2<F2, true>(u, cb, k1);
@@ -333,7 +334,8 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
           double2 v[F1::R1];
 #pragma unroll
           for (int n1 = 0; n1 < F1::R1; ++n1)
-            v[n1] = active ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp) : make_double2(0.0, 0.0);
+            v[n1] = (active && !(a.skip & 4)) ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp)
+                                              : make_double2(0.0, 0.0);
           rf_step1<F1, false>(v, fb, tw1, n2);
         }
         __syncthreads();
@@ -379,8 +381,10 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
               if (padA) xa = make_double2(0.0, 0.0);
               if (padB) xbv = make_double2(0.0, 0.0);
               double2* o = a.spout + (int64_t)k * W + mycol;
-              stg_cs2(o, xa);
-              stg_cs2(o + 1, xbv);
+              if (!(a.skip & 2)) {
+                stg_cs2(o, xa);
+                stg_cs2(o + 1, xbv);
+              }
             }
           }
         } else {
@@ -574,6 +578,9 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   a.tau = c->tau_p; a.tau_shift = c->tau_p * c->shift;
   a.W = W; a.ld = (int)c->ld; a.nx = c->nx; a.accumulate = accumulate; a.debug_sign = c->debug & 1;
   a.no_discard = no_discard;
+  static int skip = -1;
+  if (skip < 0) skip = getenv("CNPINT_FS_SKIP") ? atoi(getenv("CNPINT_FS_SKIP")) : 0;
+  a.skip = skip;
   a.cnt = c->d_fscnt; a.ticket = c->d_fscnt + S.nxb; a.tick_base = c->fs_tick; a.base = c->fs_cnt;
   kern<<<grid, G::NT, G::bytes, c->stream>>>(a, S);
   c->fs_cnt += (unsigned)(S.n[0] + S.n[1]);  // phases 0 and 1 count per block
