@@ -112,6 +112,10 @@ struct FsGeo {
   static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
   static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
   static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT : 1) : 2;
+  // items per block and phase (see k_fstep); PER = slots per schedule step
+  static constexpr int NFAM = 2 * (N2 / 2 + 1);
+  static constexpr int NP0 = MODE == 1 ? NFAM : N1, NP1 = MODE == 2 ? NFAM : 0, NP2 = MODE == 0 ? NFAM : N1;
+  static constexpr int PER = NP0 + NP1 + NP2;
 };
 
 }  // namespace
@@ -125,13 +129,13 @@ struct FsSched {
   unsigned total;
 };
 
+template <class G>
 CNP_DEV bool fs_item(const FsSched& S, unsigned T, int& ph, int& xb, int& idx) {
-  const int per = S.n[0] + S.n[1] + S.n[2];
-  const int s = (int)(T / (unsigned)per);
-  int r = (int)(T - (unsigned)s * per);
-  ph = r < S.n[0] ? 0 : r < S.n[0] + S.n[1] ? 1 : 2;
-  idx = ph == 0 ? r : ph == 1 ? r - S.n[0] : r - S.n[0] - S.n[1];
-  xb = s - S.lag[ph];
+  const int st = (int)(T / (unsigned)G::PER);  // constant divisor
+  const int r = (int)(T - (unsigned)st * G::PER);
+  ph = r < G::NP0 ? 0 : r < G::NP0 + G::NP1 ? 1 : 2;
+  idx = ph == 0 ? r : ph == 1 ? r - G::NP0 : r - G::NP0 - G::NP1;
+  xb = st - (ph == 0 ? 0 : ph == 1 ? S.lag[1] : S.lag[2]);
   return xb >= 0 && xb < S.nxb;
 }
 
@@ -157,6 +161,7 @@ struct FsArgs {
   const double* vscale;
   const double* gam;
   const double* igam;
+  const double2* twN;  // ω_N^q, q < N (host long-double table, debug sign applied)
   const double2* lam1;
   const double2* lam2;
   const double* ex;
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
     unsigned nxt = 0;  // next ticket requested now, published in the other slot at the end
     if (tid == 0) nxt = atomicAdd(a.ticket, 1u);
     int ph, xb, idx;
-    if (!fs_item(S, T, ph, xb, idx)) {  // empty slot (schedule edge)
+    if (!fs_item<G>(S, T, ph, xb, idx)) {  // empty slot (schedule edge)
       if (tid == 0) s_tk[(it + 1) & 1] = nxt - a.tick_base;
       continue;
     }
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
     double2* const Yb = a.Y + (size_t)xb * N * NC;  // block's Y: [t1][k2][c], c < NC
     const bool fwd_t1 = MODE != 1 && ph == 0;
     const bool inv_t1 = MODE != 0 && ph == 2;
-    if (ph > 0) fs_wait(a.cnt + xb, a.base + (unsigned)(ph == 1 ? S.n[0] : S.n[0] + S.n[1]));
+    if (ph > 0) fs_wait(a.cnt + xb, a.base + (unsigned)(ph == 1 ? G::NP0 : G::NP0 + G::NP1));
 
     if (fwd_t1 || inv_t1) {
       // ================= t1 items (length N2): forward pass A or inverse pass B'
@@ -244,11 +249,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
       const int xin = mycol % a.ld;
       const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
       if (fwd_t1)
-        for (int q = tid; q < N2; q += NT) {  // ω_N^{t1 k2}
-          double2 w = expi_neg((t1 * q) & (N - 1), N);
-          w.y *= sg;
-          twn[q] = w;
-        }
+        for (int q = tid; q < N2; q += NT) twn[q] = __ldg(a.twN + ((t1 * q) & (N - 1)));  // ω_N^{t1 k2}
       if (j < F2::R2) {
         const int n2 = j;
         double2 v[F2::R1];
@@ -358,11 +359,8 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
         }
         if (MODE == 2)
           for (int q = tid; q < N1; q += NT) {  // ω_N^{k2 t1}, ω_N^{k2m t1} (conjugated at use)
-            double2 w0 = expi_neg((k2 * q) & (N - 1), N), w1 = expi_neg((k2m * q) & (N - 1), N);
-            w0.y *= sg;
-            w1.y *= sg;
-            twn[q] = w0;
-            twn[N1 + q] = w1;
+            twn[q] = __ldg(a.twN + ((k2 * q) & (N - 1)));
+            twn[N1 + q] = __ldg(a.twN + ((k2m * q) & (N - 1)));
           }
         __syncthreads();
         if (MODE == 0) {
@@ -477,11 +475,8 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
           buf[(pm * NF + pp) * F1::SC + (pk % F1::R2) * F1::G1 + pk / F1::R2] = zp;
         }
         for (int q = tid; q < N1; q += NT) {  // ω_N^{k2 t1}, ω_N^{k2m t1} (conjugated at use)
-          double2 w0 = expi_neg((k2 * q) & (N - 1), N), w1 = expi_neg((k2m * q) & (N - 1), N);
-          w0.y *= sg;
-          w1.y *= sg;
-          twn[q] = w0;
-          twn[N1 + q] = w1;
+          twn[q] = __ldg(a.twN + ((k2 * q) & (N - 1)));
+          twn[N1 + q] = __ldg(a.twN + ((k2m * q) & (N - 1)));
         }
         __syncthreads();
         double2 v[F1::R1];
@@ -553,13 +548,12 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   }
   const int W = (int)c->slice;  // real columns per time row
-  const int nfam = 2 * (G::N2 / 2 + 1);
   FsSched S;
   S.nxb = (W + 2 * G::NC - 1) / (2 * G::NC);
-  S.n[0] = MODE == 1 ? nfam : G::N1;
-  S.n[1] = MODE == 2 ? nfam : 0;
-  S.n[2] = MODE == 0 ? nfam : G::N1;
-  const int per = S.n[0] + S.n[1] + S.n[2];
+  S.n[0] = G::NP0;
+  S.n[1] = G::NP1;
+  S.n[2] = G::NP2;
+  const int per = G::PER;
   const int grid_max = per_sm * c->num_sms;
   // lag: enough steps between a block's phases that the CTAs in flight (≈ grid) finish the earlier
   // phase first
@@ -574,7 +568,7 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   if (no_discard < 0) no_discard = getenv("CNPINT_FS_NODISCARD") ? 1 : 0;
   FsArgs a;
   a.vin = vin; a.spin = spin; a.vout = vout; a.spout = spout; a.Y = (double2*)c->d_fsY; a.vscale = vscale;
-  a.gam = c->d_gam; a.igam = c->d_igam; a.lam1 = c->d_lam1; a.lam2 = c->d_lam2; a.ex = c->d_ex; a.ey = c->d_ey;
+  a.gam = c->d_gam; a.igam = c->d_igam; a.twN = c->d_tw; a.lam1 = c->d_lam1; a.lam2 = c->d_lam2; a.ex = c->d_ex; a.ey = c->d_ey;
   a.tau = c->tau_p; a.tau_shift = c->tau_p * c->shift;
   a.W = W; a.ld = (int)c->ld; a.nx = c->nx; a.accumulate = accumulate; a.debug_sign = c->debug & 1;
   a.no_discard = no_discard;
