@@ -70,7 +70,7 @@ typedef enum {
  *   2D (dim = 2):          L_h = I_y ⊗ L_x + L_y ⊗ I_x + shift·I,  L_x = tridiag(xs, xd, xu)
  *                          (nx×nx Toeplitz), L_y = tridiag(ys, yd, yu) (ny×ny Toeplitz).
  *       Requires xs*xu > 0 and ys*yu > 0 (diagonal similarity to a symmetric Toeplitz matrix,
- *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two <= 1024.
+ *       diagonalised by DST-I) and nx + 1, ny + 1 powers of two in [4, 1024].
  *   1D sizes: 2 <= nx <= 4096 (Toeplitz) or 2048 (variable rows).  N: power of two, 2..65536
  *   (1D time-axis FFT: thread-block clusters for N < 2048, the four-step L2-resident kernel for
  *   N >= 2048); 2D: N <= 16384 (cluster / one-column time pass). */

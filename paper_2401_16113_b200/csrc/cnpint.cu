@@ -102,6 +102,7 @@ const char* check_op(int N, const cnpint_operator* op, int* unsupported) {
       return "2D requires nx+1 and ny+1 powers of two (DST-I via FFT)";
     }
     if (op->nx + 1 > 1024 || op->ny + 1 > 1024) { *unsupported = 1; return "2D n+1 > 1024 unsupported"; }
+    if (op->nx < 3 || op->ny < 3) { *unsupported = 1; return "2D needs nx, ny >= 3"; }
     if (N > 16384) { *unsupported = 1; return "2D needs N <= 16384 (time pass on chip)"; }
     if (!(op->xs * op->xu > 0.0) || !(op->ys * op->yu > 0.0))
       return "2D requires xs*xu > 0 and ys*yu > 0 (diagonal symmetrisation)";

@@ -122,7 +122,8 @@ CNP_DEV void dftR(double2* v) {
 // items are read before one barrier and written after it.  First-stage input modes (FIRST):
 //   TF_SCALE  input i multiplied by gm[i]·s (gm = a CTA's residue slice of Γ_α, s = basis scale);
 //   TF_ODDEXT odd extension of a sequence held in slots 1..N2/2−1: elements 0 and N2/2 are 0 and
-//             element i > N2/2 is −element(N2 − i) (the DST-I embedding of K5).
+//             element i > N2/2 is −element(N2 − i) (the DST-I embedding of K5); if sc.ghi is set,
+//             slot j is first multiplied by sc.ghi[j] (K5's diagonal pre-scaling D⁻¹).
 enum { TF_PLAIN = 0, TF_SCALE = 1, TF_ODDEXT = 2 };
 // TF_SCALE's factor for element i is the time row t = i·cstride + crank:
 //   γ_t · s = ghi[t >> 6] · glo[t & 63] · s   (two-level table of Γ_α, see k_tfft.cu).
@@ -159,6 +160,7 @@ CNP_DEV void stage(double2* buf, const double2* stw, const TfScale& sc) {
           constexpr int HALF = 1 << (LOGN2 - 1);
           const int src = i <= HALF ? i : (1 << LOGN2) - i;
           double2 x = buf[c * CS + pd(src)];
+          if (sc.ghi) x = cscale(x, sc.ghi[src]);  // optional pre-scale table (0 at 0 and HALF)
           if (i == 0 || i == HALF) x = make_double2(0.0, 0.0);
           v[it][r] = i > HALF ? make_double2(-x.x, -x.y) : x;
         } else {

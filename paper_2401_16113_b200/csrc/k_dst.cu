@@ -87,20 +87,13 @@ __global__ void __launch_bounds__(256, 2)
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    if (pre) {  // pre-scale the n samples in place (D⁻¹ for the forward transform)
-      for (int q = tid; q < NC * n; q += NT) {
-        const int c = q / n, e = q - c * n + 1;
-        double2* p = buf + c * CS + pd(e);
-        *p = cscale(*p, pre_s[e]);
-      }
-      __syncthreads();
-    }
-    local_fft<false, TF_ODDEXT, LOGE, NC, NT>(buf, stw, TfScale{nullptr, nullptr, 1, 0, 1.0});
+    // the D⁻¹ pre-scaling (forward transform) is applied inside the first butterfly stage
+    local_fft<false, TF_ODDEXT, LOGE, NC, NT>(buf, stw, TfScale{pre ? pre_s : nullptr, nullptr, 1, 0, 1.0});
     // ---- F_k = −2i S(a)_k + 2 S(b)_k, k = 1..n: S(a) = −Im F/2, S(b) = Re F/2, then post-scale
-    if (!YPASS) {
+    if (!YPASS) {  // x pass: the row pitch is M = n + 1 (n + 1 a power of two ≥ 4)
       const int line0 = tile * NC * 2;
-      for (int q = tid; q < NC * ldi; q += NT) {
-        const int c = q / ldi, x = q - c * ldi;
+      for (int q = tid; q < NC * M; q += NT) {
+        const int c = q / M, x = q - c * M;
         const int la = line0 + 2 * c, lb = la + 1;
         double sa = 0.0, sb = 0.0;
         if (x < n) {
