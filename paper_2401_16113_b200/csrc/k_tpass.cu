@@ -2,7 +2,7 @@
 // FFTs.  Per spatial-mode column pair (PAPER.md:315-316 with Eq. 3.2 steps (a)-(c)):
 //   z_t = 1/(N γ_t) · iFFT_k[ FFT_t(γ s v)_k / (λ1_k − λ2_k μ) ],  μ = τ(e_x + e_y) + τ·shift,
 // the same operation as k_tfft.cu MODE 2.  A tile is NC = 8 adjacent column pairs × all N rows
-// (128-B row segments); the N-point transforms are three register radix passes, N = R1·R2·R3, with
+// (128-B row segments; 4 pairs at N = 1024); the N-point transforms are three register radix passes, N = R1·R2·R3, with
 // two shared-memory exchanges (Cooley–Tukey, n = m + M n1, M = R2 R3; k = k1 + R1 kk,
 // kk = k2 + R2 k3 — the scheme of k_dst_r in k_dst.cu), instead of one shared round trip per
 // radix-8 stage.  The forward transform leaves frequency k = r + R1R2·k3 in thread r; the inverse
@@ -65,8 +65,9 @@ struct TpPlan {
   static constexpr int N = 1 << LOGN, H = N / 2;
   using F = P3<8, 8, N / 64>;           // forward
   using I = P3<N / 64, 8, 8>;           // inverse (transposed)
-  static constexpr int NC = 8;          // column pairs per tile
-  static constexpr int TP = 64;         // max role count of both plans
+  static constexpr int TP = N >= 1024 ? N / 8 : 64;  // max role count of both plans
+  static constexpr int NC = 512 / TP;   // column pairs per tile (8: 128-B row segments; 4 at N = 1024)
+  static constexpr int MINB = N >= 1024 ? 1 : 2;
   static constexpr int NT = NC * TP;
   static constexpr int AREA = (F::AREA > I::AREA ? F::AREA : I::AREA) | 1;
   static constexpr int HI = N / 64;
@@ -81,7 +82,7 @@ struct TpPlan {
 }  // namespace
 
 template <int LOGN>
-__global__ void __launch_bounds__(TpPlan<LOGN>::NT, 2)
+__global__ void __launch_bounds__(TpPlan<LOGN>::NT, TpPlan<LOGN>::MINB)
     k_tpass_r(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ vscale, int64_t W,
               int ld, int nx, const double* __restrict__ gam, const double* __restrict__ igam,
               const double2* __restrict__ lam1, const double2* __restrict__ lam2, const double* __restrict__ ex,
@@ -211,6 +212,8 @@ static cudaError_t run_tpass(cnpint_ctx* c, const double* in, double* out, const
   return cudaGetLastError();
 }
 
+// N = 1024 (plan 8·8·16, four pairs per tile, 128 registers) measured slower than the cluster kernel
+// (c5 n255: 815 vs 754 µs) and is not routed
 bool tpass_ok(const cnpint_ctx* c) { return c->dim == 2 && (c->N == 256 || c->N == 512) && !(c->debug & 64); }
 
 cudaError_t launch_tpass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
