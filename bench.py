@@ -267,13 +267,17 @@ def run_gpu(args, rank, world, local):
     mv_s = e0.elapsed_time(e1) * 1e-3 / reps_p
     unknowns = w.unknowns
     mv_gbps = 16.0 * unknowns / mv_s / 1e9
-    pinv_gbps_structured = (16.0 * unknowns + 32.0 * (w.N // 2 + 1) * w.m + 16.0 * unknowns) / pinv_s / 1e9
+    if w.dim == 1:  # K2 (8 B in, 16 B/complex out), K3 (in + out), K4: three passes
+        pinv_gbps_structured = (16.0 * unknowns + 32.0 * (w.N // 2 + 1) * w.m + 16.0 * unknowns) / pinv_s / 1e9
+    else:  # 2D: DST x, DST y, time pass, DST y, DST x — five real passes of 16 B per unknown
+        pinv_gbps_structured = 80.0 * unknowns / pinv_s / 1e9
     del dv, out
 
     # ---------------- end to end through the host-buffer C-ABI call (pinned host memory)
-    bh = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
-    bh.copy_(b[..., : w.m].cpu())
-    uh = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
+    hshape = synth.shape_of(w)  # packed host layout: (N, m) in 1D, (N, n, n) in 2D
+    bh = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b[..., : w.n].cpu())
+    uh = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
     bnp, unp = bh.numpy(), uh.numpy()
     s.gmres_host(bnp, w.tol, w.restart, u=unp)
     torch.cuda.synchronize()
@@ -298,9 +302,9 @@ def run_gpu(args, rank, world, local):
         st_i = torch.cuda.Stream()
         with torch.cuda.stream(st_i):
             s_i = problems.make_solver(w, restart_max=w.restart)
-        bh_i = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
+        bh_i = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
         bh_i.copy_(bh)
-        uh_i = torch.empty((w.N, w.m), dtype=torch.float64, pin_memory=True)
+        uh_i = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
         handles.append((s_i, st_i, bh_i.numpy(), uh_i.numpy()))
     counts = [args.steps // ne + (1 if i < args.steps % ne else 0) for i in range(ne)]
     reps_e2e = [None] * ne
