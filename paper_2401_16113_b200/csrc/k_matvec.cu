@@ -116,39 +116,59 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
     if (hasR) pr = alpha * r[xr];
   }
   double acc = 0.0;
-#pragma unroll 4
-  for (int t = t0; t < t1; ++t) {
-    const double* r = u + (int64_t)t * ld;
-    double2 cv = make_double2(0.0, 0.0);
-    double cl = 0.0, cr = 0.0;
-    if (active) cv = ldg_cs2(reinterpret_cast<const double2*>(r + x0));
-    if (hasL) cl = r[xl];
-    if (hasR) cr = r[xr];
-    const double s0 = cv.x + pv.x, s1 = cv.y + pv.y;
-    const double d0 = cv.x - pv.x, d1 = cv.y - pv.y;
-    double sl = __shfl_up_sync(0xffffffffu, s1, 1);
-    double sr = __shfl_down_sync(0xffffffffu, s0, 1);
-    if (lane == 0) sl = hasL ? cl + pl : 0.0;
-    if (lane == 31) sr = hasR ? cr + pr : 0.0;
-    const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
-    double y0 = d0 - ht * fma(lo0, sl, fma(di0, s0, up0 * s1));
-    double y1 = d1 - ht * fma(lo1, s0, fma(di1, s1, up1 * sr));
-    if (MODE >= 2) {
-      double2 bv = make_double2(0.0, 0.0);
-      if (active) bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * ld + x0));
-      y0 = bv.x - y0;
-      y1 = bv.y - y1;
-    }
-    if (active && MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
-    if (NVD > 0 && active) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+  // rows in batches of TB: all loads of a batch are issued before any is used (memory-level
+  // parallelism; a row-at-a-time loop leaves one load per warp in flight and stalls on it)
+  constexpr int TB = NVD <= 1 ? 4 : NVD <= 3 ? 2 : 1;  // rows per batch (the dot vectors add loads per row)
+  for (int tb = t0; tb < t1; tb += TB) {
+    double2 cvb[TB], bvb[TB], vvb[TB][NVD > 0 ? NVD : 1];
+    double clb[TB], crb[TB];
 #pragma unroll
-      for (int i = 0; i < NVD; ++i) {
-        const double2 v = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * ld + x0));
-        dacc[i] = fma(v.x, y0, fma(v.y, y1, dacc[i]));
+    for (int q = 0; q < TB; ++q) {
+      const int t = tb + q;
+      cvb[q] = bvb[q] = make_double2(0.0, 0.0);
+      clb[q] = crb[q] = 0.0;
+#pragma unroll
+      for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) vvb[q][i] = make_double2(0.0, 0.0);
+      if (t < t1) {
+        const double* r = u + (int64_t)t * ld;
+        if (active) cvb[q] = ldg_cs2(reinterpret_cast<const double2*>(r + x0));
+        if (hasL) clb[q] = r[xl];
+        if (hasR) crb[q] = r[xr];
+        if (MODE >= 2 && active) bvb[q] = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * ld + x0));
+        if (NVD > 0 && active) {
+#pragma unroll
+          for (int i = 0; i < NVD; ++i)
+            vvb[q][i] = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * ld + x0));
+        }
       }
     }
-    if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
-    pv = cv; pl = cl; pr = cr;
+#pragma unroll
+    for (int q = 0; q < TB; ++q) {
+      const int t = tb + q;
+      if (t >= t1) break;
+      const double2 cv = cvb[q];
+      const double cl = clb[q], cr = crb[q];
+      const double s0 = cv.x + pv.x, s1 = cv.y + pv.y;
+      const double d0 = cv.x - pv.x, d1 = cv.y - pv.y;
+      double sl = __shfl_up_sync(0xffffffffu, s1, 1);
+      double sr = __shfl_down_sync(0xffffffffu, s0, 1);
+      if (lane == 0) sl = hasL ? cl + pl : 0.0;
+      if (lane == 31) sr = hasR ? cr + pr : 0.0;
+      const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
+      double y0 = d0 - ht * fma(lo0, sl, fma(di0, s0, up0 * s1));
+      double y1 = d1 - ht * fma(lo1, s0, fma(di1, s1, up1 * sr));
+      if (MODE >= 2) {
+        y0 = bvb[q].x - y0;
+        y1 = bvb[q].y - y1;
+      }
+      if (active && MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * ld + x0), make_double2(y0, y1));
+      if (NVD > 0 && active) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+#pragma unroll
+        for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
+      }
+      if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
+      pv = cv; pl = cl; pr = cr;
+    }
   }
   if (NORM) block_partial<128>(acc, part, out, counter);
   if constexpr (NVD > 0) {
