@@ -225,48 +225,69 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   }
   double acc = 0.0;
   int buf = 0;
-  for (int t = t0; t < t1; ++t) {
-    const double* r = u + (int64_t)t * slice;
-    double2 cv = make_double2(0, 0), ch = make_double2(0, 0);
-    double cl = 0, cr = 0;
-    if (act) cv = ldg_cs2(reinterpret_cast<const double2*>(r + off));
-    if (hact) ch = *reinterpret_cast<const double2*>(r + hoff);
-    if (hasL) cl = r[off - 1];
-    if (hasR) cr = r[off + 2];
-    const double2 s = make_double2(cv.x + pv.x, cv.y + pv.y);
-    S[buf][wy + 1][lane] = s;
-    if (wy == 0) S[buf][0][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
-    if (wy == 7) S[buf][9][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
-    __syncthreads();
-    const double2 sd = S[buf][wy][lane];       // row y-1
-    const double2 su = S[buf][wy + 2][lane];   // row y+1
-    double sl = __shfl_up_sync(0xffffffffu, s.y, 1);
-    double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
-    if (lane == 0) sl = hasL ? cl + pl : 0.0;
-    if (lane == 31) sr = hasR ? cr + pr : 0.0;
-    const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
-    double y0 = (cv.x - pv.x) - ht * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
-    double y1 = (cv.y - pv.y) - ht * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
-    if (x0 >= nx) y0 = 0.0;
-    if (x0 + 1 >= nx) y1 = 0.0;
-    if (MODE >= 2 && act) {
-      double2 bv = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * slice + off));
-      y0 = bv.x - y0;
-      y1 = bv.y - y1;
-    }
-    if (act) {
-      if (MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
-      if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+  // rows in batches whose loads are all issued before use (see k_matvec1d)
+  constexpr int TB = NVD <= 1 ? 4 : NVD <= 3 ? 2 : 1;
+  for (int tb = t0; tb < t1; tb += TB) {
+    double2 cvb[TB], chb[TB], bvb[TB], vvb[TB][NVD > 0 ? NVD : 1];
+    double clb[TB], crb[TB];
 #pragma unroll
-        for (int i = 0; i < NVD; ++i) {
-          const double2 v = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * slice + off));
-          dacc[i] = fma(v.x, y0, fma(v.y, y1, dacc[i]));
+    for (int q = 0; q < TB; ++q) {
+      const int t = tb + q;
+      cvb[q] = chb[q] = bvb[q] = make_double2(0, 0);
+      clb[q] = crb[q] = 0.0;
+#pragma unroll
+      for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) vvb[q][i] = make_double2(0, 0);
+      if (t < t1) {
+        const double* r = u + (int64_t)t * slice;
+        if (act) cvb[q] = ldg_cs2(reinterpret_cast<const double2*>(r + off));
+        if (hact) chb[q] = *reinterpret_cast<const double2*>(r + hoff);
+        if (hasL) clb[q] = r[off - 1];
+        if (hasR) crb[q] = r[off + 2];
+        if (MODE >= 2 && act) bvb[q] = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * slice + off));
+        if (NVD > 0 && act) {
+#pragma unroll
+          for (int i = 0; i < NVD; ++i)
+            vvb[q][i] = ldg_cs2(reinterpret_cast<const double2*>(vd.p[i] + (int64_t)t * slice + off));
         }
       }
-      if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
     }
-    pv = cv; ph = ch; pl = cl; pr = cr;
-    buf ^= 1;
+#pragma unroll
+    for (int q = 0; q < TB; ++q) {
+      const int t = tb + q;
+      if (t >= t1) break;  // uniform over the block (t1 is)
+      const double2 cv = cvb[q], ch = chb[q];
+      const double cl = clb[q], cr = crb[q];
+      const double2 s = make_double2(cv.x + pv.x, cv.y + pv.y);
+      S[buf][wy + 1][lane] = s;
+      if (wy == 0) S[buf][0][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
+      if (wy == 7) S[buf][9][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
+      __syncthreads();
+      const double2 sd = S[buf][wy][lane];       // row y-1
+      const double2 su = S[buf][wy + 2][lane];   // row y+1
+      double sl = __shfl_up_sync(0xffffffffu, s.y, 1);
+      double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
+      if (lane == 0) sl = hasL ? cl + pl : 0.0;
+      if (lane == 31) sr = hasR ? cr + pr : 0.0;
+      const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
+      double y0 = (cv.x - pv.x) - ht * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
+      double y1 = (cv.y - pv.y) - ht * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
+      if (x0 >= nx) y0 = 0.0;
+      if (x0 + 1 >= nx) y1 = 0.0;
+      if (MODE >= 2 && act) {
+        y0 = bvb[q].x - y0;
+        y1 = bvb[q].y - y1;
+      }
+      if (act) {
+        if (MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
+        if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+#pragma unroll
+          for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
+        }
+        if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
+      }
+      pv = cv; ph = ch; pl = cl; pr = cr;
+      buf ^= 1;
+    }
   }
   if (NORM) block_partial<256>(acc, part, out, counter);
   if constexpr (NVD > 0) {
