@@ -44,6 +44,12 @@ def test_workspace_bytes_validation():
     assert lib.cnpint_workspace_bytes(512, C.byref(bad2), 0) == 0    # n+1 not a power of two
     sym = cnpint.Operator(2, 255, 255, 1, None, None, None, -1.0, -2.0, 1.0, 1.0, -2.0, 1.0, 0.0)
     assert lib.cnpint_workspace_bytes(512, C.byref(sym), 0) == 0     # xs*xu <= 0
+    assert lib.cnpint_workspace_bytes(32768, C.byref(op2), 0) == 0   # 2D time pass limited to N <= 16384
+    assert lib.cnpint_workspace_bytes(65536, C.byref(op), 0) > 0     # 1D up to N = 65536 (four-step FFT)
+    tiny = cnpint.Operator(2, 1, 3, 1, None, None, None, 1.0, -2.0, 1.0, 1.0, -2.0, 1.0, 0.0)
+    assert lib.cnpint_workspace_bytes(64, C.byref(tiny), 0) == 0     # 2D needs nx, ny >= 3
+    # the four-step intermediate and counters are part of the workspace from 1D N = 2048 on
+    assert lib.cnpint_workspace_bytes(2048, C.byref(op), 0) > 2 * lib.cnpint_workspace_bytes(1024, C.byref(op), 0)
 
 
 def test_workspace_scales_with_restart():
