@@ -38,8 +38,11 @@ struct DstLayout {
 
 }  // namespace
 
+#ifndef DST_MINB
+#define DST_MINB 2
+#endif
 template <bool YPASS, int LOGE, int NC>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, DST_MINB)
     k_dst(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
           const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
           int nx) {
