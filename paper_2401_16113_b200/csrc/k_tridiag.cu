@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(MAXT, 2)
   auto sidx = [&](int i) { return i ^ ((i >> padsh) & smask); };
   const int k = blockIdx.x * NS + g;
   const bool act = k < K;  // uniform over the system's warps
+  // per-frequency scalars first: their latency overlaps the copy issue below
+  double2 il = make_double2(0.0, 0.0), skk = il;
+  if (act) { il = __ldg(il2 + k); skk = __ldg(sk + k); }
   // ---------------- asynchronous load of the system (and its table) into shared memory
   if (act) {
     const double2* src = what + (int64_t)k * W;
@@ -139,8 +142,6 @@ __global__ void __launch_bounds__(MAXT, 2)
   const int i0 = p < nlong ? p * (Lmin + 1) : nlong * (Lmin + 1) + (p - nlong) * Lmin;
   const int i1 = i0 + len;
   bool ok = true;
-  double2 il = make_double2(0.0, 0.0), skk = il;
-  if (act) { il = il2[k]; skk = sk[k]; }
   cp_async_wait<0>();
   __syncthreads();
   Seg sg;
