@@ -34,6 +34,15 @@
 #ifndef FS_NC6
 #define FS_NC6 16  // pair columns per block when N1, N2 = 64 (8 threads per column; 32 measured slower)
 #endif
+#ifndef FS_NC5
+#define FS_NC5 32  // pair columns per block when max(N1, N2) <= 32 (2D time pass, N <= 1024)
+#endif
+#ifndef FS_NC7
+#define FS_NC7 16  // pair columns per block when max(N1, N2) >= 128 (16 threads per column)
+#endif
+#ifndef FS_MINB7
+#define FS_MINB7 2
+#endif
 
 namespace {
 
@@ -96,7 +105,7 @@ template <int MODE, int LOG1, int LOG2>
 struct FsGeo {
   static constexpr int N1 = 1 << LOG1, N2 = 1 << LOG2, N = N1 * N2, H = N / 2;
   static constexpr int MX = LOG1 > LOG2 ? LOG1 : LOG2;
-  static constexpr int NC = MX <= 5 ? 32 : MX == 6 ? FS_NC6 : 16;
+  static constexpr int NC = MX <= 5 ? FS_NC5 : MX == 6 ? FS_NC6 : FS_NC7;
   static constexpr int NF = NC / 2;
   static constexpr int SCM = RF<LOG1>::SC > RF<LOG2>::SC ? RF<LOG1>::SC : RF<LOG2>::SC;
   static constexpr int off_tw1 = NC * SCM;           // ω_{N1}^j, j < N1
@@ -111,7 +120,7 @@ struct FsGeo {
   static constexpr int TP1 = RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2;
   static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
   static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
-  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT : 1) : 2;
+  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT : 1) : MODE == 2 ? 2 : FS_MINB7;
   // items per block and phase (see k_fstep); PER = slots per schedule step
   static constexpr int NFAM = 2 * (N2 / 2 + 1);
   static constexpr int NP0 = MODE == 1 ? NFAM : N1, NP1 = MODE == 2 ? NFAM : 0, NP2 = MODE == 0 ? NFAM : N1;
@@ -517,8 +526,13 @@ static void fs_logs(int N, int& l1, int& l2) {
 // 2D: from N = 2048 on (the cluster kernel's own range ends in C = 8 clusters there); at N ≤ 1024 the
 // items of the three-phase pass are 8–16 KB and the cluster kernel measured faster (c4: 326 vs 781
 // µs, profiles/r01_k6_sweep.txt)
+static int fs_min2d() {  // CNPINT_FS_2D_MIN: tuning experiments only
+  static int v = -1;
+  if (v < 0) v = getenv("CNPINT_FS_2D_MIN") ? atoi(getenv("CNPINT_FS_2D_MIN")) : 2048;
+  return v;
+}
 static bool fs_shape_ok(int dim, int N) {
-  return dim == 1 ? (N >= 2048 && N <= 65536) : (N >= 2048 && N <= 16384);
+  return dim == 1 ? (N >= 2048 && N <= 65536) : (N >= fs_min2d() && N >= 256 && N <= 16384);
 }
 bool fstep_ok(const cnpint_ctx* c) { return fs_shape_ok(c->dim, c->N) && c->d_fsY; }
 
@@ -526,7 +540,7 @@ static int fs_nc(int N) {
   int l1, l2;
   fs_logs(N, l1, l2);
   const int mx = l1 > l2 ? l1 : l2;
-  return mx <= 5 ? 32 : mx == 6 ? FS_NC6 : 16;
+  return mx <= 5 ? FS_NC5 : mx == 6 ? FS_NC6 : FS_NC7;
 }
 // W = real columns of a time row (1D: ld; 2D: ny·ld)
 int fstep_nxb(int N, int64_t W) { return (int)((W + 2 * fs_nc(N) - 1) / (2 * fs_nc(N))); }
@@ -590,7 +604,7 @@ static cudaError_t fs_dispatch(cnpint_ctx* c, const double* vin, const double2* 
 #define FS_CASE(A, B) \
   if (l1 == A && l2 == B) return fs_launch<MODE, A, B>(c, vin, spin, vout, spout, vscale, accumulate);
   if constexpr (MODE == 2) {
-    FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7)
+    FS_CASE(4, 4) FS_CASE(5, 4) FS_CASE(5, 5) FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7)
   } else {
     FS_CASE(6, 5) FS_CASE(6, 6) FS_CASE(7, 6) FS_CASE(7, 7) FS_CASE(8, 7) FS_CASE(8, 8)
   }
