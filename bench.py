@@ -240,6 +240,8 @@ def run_gpu(args, rank, world, local):
     dominant = max(prof.items(), key=lambda kv: kv[1][0] if kv[1][2] > 0 else -1)[0]
     d_ms, d_cnt, d_by = prof[dominant]
     peak, peak_src = measured_hbm_peak()
+    for k in kernels.values():  # every kernel's fraction of the same HBM peak
+        k["frac"] = k["algo_GBps"] / peak if k["algo_GBps"] else None
     achieved = d_by / (d_ms * 1e-3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
     traffic = ncu_traffic(dominant, w.name)
