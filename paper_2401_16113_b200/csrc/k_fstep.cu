@@ -37,6 +37,9 @@
 #ifndef FS_NC5
 #define FS_NC5 32  // pair columns per block when max(N1, N2) <= 32 (2D time pass, N <= 1024)
 #endif
+#ifndef FS_TT6
+#define FS_TT6 1  // t1 values per t1 item when N1, N2 = 64 (2 measured slower: 166 registers, fewer CTAs)
+#endif
 #ifndef FS_NC7
 #define FS_NC7 16  // pair columns per block when max(N1, N2) >= 128 (16 threads per column)
 #endif
@@ -107,8 +110,11 @@ struct FsGeo {
   static constexpr int MX = LOG1 > LOG2 ? LOG1 : LOG2;
   static constexpr int NC = MX <= 5 ? FS_NC5 : MX == 6 ? FS_NC6 : FS_NC7;
   static constexpr int NF = NC / 2;
-  static constexpr int SCM = RF<LOG1>::SC > RF<LOG2>::SC ? RF<LOG1>::SC : RF<LOG2>::SC;
-  static constexpr int off_tw1 = NC * SCM;           // ω_{N1}^j, j < N1
+  // t1 items take TT consecutive t1 values (independent FFTs interleaved in every thread: more
+  // memory- and instruction-level parallelism per item, fewer items)
+  static constexpr int TT = MX == 6 ? FS_TT6 : 1;
+  static constexpr int AREA_T = TT * NC * RF<LOG2>::SC, AREA_F = NC * RF<LOG1>::SC;
+  static constexpr int off_tw1 = AREA_T > AREA_F ? AREA_T : AREA_F;  // ω_{N1}^j, j < N1
   static constexpr int off_tw2 = off_tw1 + N1;       // ω_{N2}^j
   static constexpr int off_twn = off_tw2 + N2;       // per-item ω_N table [2·max(N1, N2)]
   static constexpr int NTW = 2 * (N1 > N2 ? N1 : N2);
@@ -120,10 +126,10 @@ struct FsGeo {
   static constexpr int TP1 = RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2;
   static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
   static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
-  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT : 1) : MODE == 2 ? 2 : FS_MINB7;
+  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT / TT : 1) : MODE == 2 ? 2 : FS_MINB7;
   // items per block and phase (see k_fstep); PER = slots per schedule step
   static constexpr int NFAM = 2 * (N2 / 2 + 1);
-  static constexpr int NP0 = MODE == 1 ? NFAM : N1, NP1 = MODE == 2 ? NFAM : 0, NP2 = MODE == 0 ? NFAM : N1;
+  static constexpr int NP0 = MODE == 1 ? NFAM : N1 / TT, NP1 = MODE == 2 ? NFAM : 0, NP2 = MODE == 0 ? NFAM : N1 / TT;
   static constexpr int PER = NP0 + NP1 + NP2;
 };
 
@@ -251,59 +257,81 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
     if (ph > 0) fs_wait(a.cnt + xb, a.base + (unsigned)(ph == 1 ? G::NP0 : G::NP0 + G::NP1));
 
     if (fwd_t1 || inv_t1) {
-      // ================= t1 items (length N2): forward pass A or inverse pass B'
-      double2* const cb = buf + col * F2::SC;
-      const int t1 = idx;
+      // ================= t1 items (length N2): forward pass A or inverse pass B' for the TT rows
+      //                   t1 = idx·TT + tt (TT interleaved transforms per thread)
+      constexpr int TT = G::TT;
+      const int t1b = idx * TT;
       const int mycol = col0 + 2 * col;
       const int xin = mycol % a.ld;
       const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
       if (fwd_t1)
-        for (int q = tid; q < N2; q += NT) twn[q] = __ldg(a.twN + ((t1 * q) & (N - 1)));  // ω_N^{t1 k2}
+        for (int q = tid; q < TT * N2; q += NT) {  // ω_N^{t1 k2} for each t1 of the item
+          const int tt = q / N2, k2 = q - tt * N2;
+          twn[q] = __ldg(a.twN + (((t1b + tt) * k2) & (N - 1)));
+        }
       if (j < F2::R2) {
         const int n2 = j;
-        double2 v[F2::R1];
+        double2 v[TT][F2::R1];
         if (fwd_t1) {
 #pragma unroll
-          for (int n1 = 0; n1 < F2::R1; ++n1) {
-            const int t = t1 + N1 * (n2 + F2::R2 * n1);
-            v[n1] = (colok && !(a.skip & 1)) ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
-                                             : make_double2(0.0, 0.0);
-          }
+          for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
-          for (int n1 = 0; n1 < F2::R1; ++n1) {
-            const int t = t1 + N1 * (n2 + F2::R2 * n1);
-            v[n1] = cscale(v[n1], ghi[t >> 6] * glo[t & 63] * s);
+            for (int n1 = 0; n1 < F2::R1; ++n1) {
+              const int t = t1b + tt + N1 * (n2 + F2::R2 * n1);
+              v[tt][n1] = (colok && !(a.skip & 1)) ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
+                                                   : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt) {
+#pragma unroll
+            for (int n1 = 0; n1 < F2::R1; ++n1) {
+              const int t = t1b + tt + N1 * (n2 + F2::R2 * n1);
+              v[tt][n1] = cscale(v[tt][n1], ghi[t >> 6] * glo[t & 63] * s);
+            }
+            rf_step1<F2, false>(v[tt], buf + (tt * NC + col) * F2::SC, tw2, n2);
           }
-          rf_step1<F2, false>(v, cb, tw2, n2);
         } else {
 #pragma unroll
-          for (int n1 = 0; n1 < F2::R1; ++n1) v[n1] = __ldcg(Yb + ((size_t)t1 * N2 + n2 + F2::R2 * n1) * NC + col);
-          rf_step1<F2, true>(v, cb, tw2, n2);
+          for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+            for (int n1 = 0; n1 < F2::R1; ++n1)
+              v[tt][n1] = __ldcg(Yb + ((size_t)(t1b + tt) * N2 + n2 + F2::R2 * n1) * NC + col);
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt) rf_step1<F2, true>(v[tt], buf + (tt * NC + col) * F2::SC, tw2, n2);
         }
       }
       __syncthreads();
-      if (inv_t1 && !a.no_discard) {  // this t1's Y rows: N2·NC·16 B, contiguous, last reader
-        const char* src = reinterpret_cast<const char*>(Yb + (size_t)t1 * N2 * NC);
-        for (int q = tid; q < N2 * NC * 16 / 128; q += NT) discard_l2(src + q * 128);
+      if (inv_t1 && !a.no_discard) {  // these t1's Y rows: TT·N2·NC·16 B, contiguous, last reader
+        const char* src = reinterpret_cast<const char*>(Yb + (size_t)t1b * N2 * NC);
+        for (int q = tid; q < TT * N2 * NC * 16 / 128; q += NT) discard_l2(src + q * 128);
       }
       if (j < F2::R1) {
         const int k1 = j;
-        double2 u[F2::R2];
+        double2 u[TT][F2::R2];
         if (fwd_t1) {
-          rf_step2<F2, false>(u, cb, k1);
 #pragma unroll
-          for (int k2 = 0; k2 < F2::R2; ++k2) {
-            const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
-            if (!(a.skip & 4)) Yb[((size_t)t1 * N2 + kk) * NC + col] = cmul(u[k2], twn[kk]);
-          }
+          for (int tt = 0; tt < TT; ++tt) rf_step2<F2, false>(u[tt], buf + (tt * NC + col) * F2::SC, k1);
         } else {
-          rf_step2<F2, true>(u, cb, k1);
-          if (colok) {
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt) rf_step2<F2, true>(u[tt], buf + (tt * NC + col) * F2::SC, k1);
+        }
+        if (fwd_t1) {
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt)
 #pragma unroll
             for (int k2 = 0; k2 < F2::R2; ++k2) {
-              const int t = t1 + N1 * (k1 + F2::R1 * k2);
+              const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
+              if (!(a.skip & 4))
+                Yb[((size_t)(t1b + tt) * N2 + kk) * NC + col] = cmul(u[tt][k2], twn[tt * N2 + kk]);
+            }
+        } else if (colok) {
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt)
+#pragma unroll
+            for (int k2 = 0; k2 < F2::R2; ++k2) {
+              const int t = t1b + tt + N1 * (k1 + F2::R1 * k2);
               const double g = ihi[t >> 6] * ilo[t & 63];
-              double2 val = make_double2(padA ? 0.0 : u[k2].x * g, padB ? 0.0 : u[k2].y * g);
+              double2 val = make_double2(padA ? 0.0 : u[tt][k2].x * g, padB ? 0.0 : u[tt][k2].y * g);
               double2* dst = reinterpret_cast<double2*>(a.vout + (int64_t)t * W + mycol);
               if (a.accumulate) {
                 const double2 o = *dst;
@@ -312,7 +340,6 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
               }
               stg_cs2(dst, val);
             }
-          }
         }
       }
       if (fwd_t1) fs_signal(a.cnt + xb);
