@@ -692,13 +692,15 @@ static cnpint_status gmres_args(cnpint_ctx* c, const double* d_b, double* d_u, d
 }
 
 // CGS2 of w (already in its basis slot) against Ṽ_0..Ṽ_{nv−1}: c1 = Ṽᵀw (unless the producer fused
-// it: have_c1), w −= Ṽ(s²c1) with c2 = Ṽᵀw fused, w −= Ṽ(s²c2) with ||w||² fused into scal[2].
+// it: have_c1), c2 = Ṽᵀ(w − Ṽs²c1), w −= Ṽ s²(c1 + c2) with ||w||² fused into scal[2].
 // More than CNP_MAX_DOT vectors: groups of CNP_MAX_DOT (dots, update, dots, update, norm).
 static cnpint_status cgs2(cnpint_ctx* c, double* const* V, int nv, double* w, bool have_c1) {
   if (nv <= CNP_MAX_DOT) {
     if (!have_c1) CK(launch_dots(c, V, nv, w, c->d_part, c->d_c1));
-    CK(launch_update(c, V, nv, c->d_c1, 0, w, w, 1, 0, c->d_part, c->d_c2));
-    CK(launch_update(c, V, nv, c->d_c2, 0, w, w, 0, 1, c->d_part, c->d_scal + 2));
+    // c2 = Ṽᵀ(w − Ṽs²c1) without storing the intermediate, then w ← w − Ṽs²(c1 + c2) with ‖w‖²:
+    // the same two projections (CGS2) with one write of w instead of two
+    CK(launch_cgs2_pass(c, V, nv, c->d_c1, nullptr, w, c->d_part, c->d_c2, 0));
+    CK(launch_cgs2_pass(c, V, nv, c->d_c1, c->d_c2, w, c->d_part, c->d_scal + 2, 1));
     return CNPINT_OK;
   }
   for (int pass = 0; pass < 2; ++pass) {

@@ -69,16 +69,19 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
   grid_fold(part, gridDim.x, stride, 1, out, counter);
 }
 
-// w_out = w − Σ_i coef_i Ṽ_i with coef_i = cd[i]·s_i² (MODE 0) or coef_i = cd[i] (MODE 1, combine,
-// w may be null), optionally fused partial dots with Ṽ (DOTS) or Σ w_out² (NORM).
-template <int NV, int MODE, bool DOTS, bool NORM>
+// w_out = w − Σ_i coef_i Ṽ_i with coef_i = (cd[i] + cd2[i])·s_i² (MODE 0; cd2 may be null) or
+// coef_i = cd[i] (MODE 1, combine, w may be null), optionally fused partial dots with Ṽ (DOTS) or
+// Σ w_out² (NORM).  NOWRITE: w_out is only formed in registers (its dots are the product), nothing
+// is stored — CGS2's second projection c2 = Ṽᵀ(w − Ṽ s²c1) without writing the intermediate.
+template <int NV, int MODE, bool DOTS, bool NORM, bool NOWRITE = false>
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const double* __restrict__ cd,
                                                              const double* __restrict__ scl, const double* w,
                                                              double* wout, size_t n2, double* __restrict__ part,
-                                                             int stride, double* __restrict__ out, unsigned* counter) {
+                                                             int stride, double* __restrict__ out, unsigned* counter,
+                                                             const double* __restrict__ cd2 = nullptr) {
   double coef[NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? cd[i] * scl[i] * scl[i] : cd[i];
+  for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? (cd[i] + (cd2 ? cd2[i] : 0.0)) * scl[i] * scl[i] : cd[i];
   constexpr int NA = DOTS ? NV : 1;
   double acc[NA];
 #pragma unroll
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
       if (MODE == 0) { x.x = fma(-coef[i], v[i].x, x.x); x.y = fma(-coef[i], v[i].y, x.y); }
       else { x.x = fma(coef[i], v[i].x, x.x); x.y = fma(coef[i], v[i].y, x.y); }
     }
-    o2[e] = x;
+    if (!NOWRITE) o2[e] = x;
     if constexpr (DOTS) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) acc[i] = fma(v[i].x, x.x, fma(v[i].y, x.y, acc[i]));
@@ -231,6 +234,39 @@ static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w
                 double* out) {
   k_update<NV, MODE, DOTS, NORM><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
       V, cd, c->d_scl, w, wout, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
+}
+
+template <int NV>
+static void upd_cgs(cnpint_ctx* c, const VPtrs& V, const double* c1, const double* c2, double* w, double* part,
+                    double* out, int phase) {
+  if (phase == 0)  // c2 = Ṽᵀ(w − Ṽ s² c1), nothing written
+    k_update<NV, 0, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
+        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, nullptr);
+  else  // w ← w − Ṽ s² (c1 + c2), ‖w‖²
+    k_update<NV, 0, false, true, false><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
+        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2);
+}
+
+// CGS2 with one write: phase 0 forms c2 = Ṽᵀ(w − Ṽ s²c1) (reads Ṽ and w, writes nothing), phase 1
+// applies both projections at once, w ← w − Ṽ s²(c1 + c2), with ‖w‖² fused.
+cudaError_t launch_cgs2_pass(cnpint_ctx* c, double* const* Vp, int nv, const double* c1, const double* c2,
+                             double* w, double* part, double* out, int phase) {
+  VPtrs V;
+  for (int i = 0; i < CNP_MAX_DOT; ++i) V.p[i] = i < nv ? Vp[i] : nullptr;
+  cnp_prof_begin(c, KID_UPDATE);
+  switch (nv) {
+    case 1: upd_cgs<1>(c, V, c1, c2, w, part, out, phase); break;
+    case 2: upd_cgs<2>(c, V, c1, c2, w, part, out, phase); break;
+    case 3: upd_cgs<3>(c, V, c1, c2, w, part, out, phase); break;
+    case 4: upd_cgs<4>(c, V, c1, c2, w, part, out, phase); break;
+    case 5: upd_cgs<5>(c, V, c1, c2, w, part, out, phase); break;
+    case 6: upd_cgs<6>(c, V, c1, c2, w, part, out, phase); break;
+    case 7: upd_cgs<7>(c, V, c1, c2, w, part, out, phase); break;
+    case 8: upd_cgs<8>(c, V, c1, c2, w, part, out, phase); break;
+    default: return cudaErrorInvalidValue;
+  }
+  cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (phase == 0 ? 1 : 2)));
+  return cudaGetLastError();
 }
 
 template <int NV>
