@@ -117,6 +117,8 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
 
 void cnpint_destroy(cnpint_ctx* ctx);
 const char* cnpint_last_error(const cnpint_ctx* ctx);
+/* Moves the handle to another stream; if it differs from the current one, the current stream is
+ * synchronised first (the handle's kernels are ordered on one stream at a time). */
 cnpint_status cnpint_set_stream(cnpint_ctx* ctx, void* cuda_stream);
 
 int64_t cnpint_ld(const cnpint_ctx* ctx);          /* row pitch in doubles */

@@ -514,7 +514,12 @@ const char* cnpint_last_error(const cnpint_ctx* c) { return c ? c->err : "null h
 
 cnpint_status cnpint_set_stream(cnpint_ctx* c, void* s) {
   if (!c) return CNPINT_EINVAL;
-  c->stream = (cudaStream_t)s;
+  if ((cudaStream_t)s != c->stream) {
+    // the persistent four-step kernels carry per-handle counters from launch to launch, so the work
+    // already enqueued on the old stream must finish before anything runs on the new one
+    CK(cudaStreamSynchronize(c->stream));
+    c->stream = (cudaStream_t)s;
+  }
   return CNPINT_OK;
 }
 

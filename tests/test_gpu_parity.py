@@ -635,3 +635,24 @@ def test_theorem_4_5_on_gpu_meshes(delta):
         torch.cuda.empty_cache()
     # mesh independent: refinement never increases the count (α = δ/√N shrinks, so it can decrease)
     assert all(its[N] <= its[256] for N in its) and max(its.values()) <= 8, its
+
+
+def test_stream_switching_keeps_four_step_state():
+    """The persistent four-step FFT carries per-handle counters across launches: moving the handle
+    between CUDA streams (the binding follows torch's current stream) must keep results exact."""
+    w = SMALL["1d_N4096_C2"]
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 51)[0]
+    zo = precond.pinv_dft(w, op, v)
+    vd = s.to_device(v)
+    z0 = s.empty()
+    s.apply_Pinv(vd, z0)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for i in range(6):
+        with torch.cuda.stream(streams[i % 2]):
+            z = s.empty()
+            s.apply_Pinv(vd, z)
+            torch.cuda.current_stream().synchronize()
+        assert torch.equal(z, z0), i
+    assert rel(s.to_host(z0), zo) < 1e-12
