@@ -613,9 +613,13 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   a.tau = c->tau_p; a.tau_shift = c->tau_p * c->shift;
   a.W = W; a.ld = (int)c->ld; a.nx = c->nx; a.accumulate = accumulate; a.debug_sign = c->debug & 1;
   a.no_discard = no_discard;
+#ifdef CNPINT_EXPERIMENTS  // result-corrupting timing knob: only in experiment builds
   static int skip = -1;
   if (skip < 0) skip = getenv("CNPINT_FS_SKIP") ? atoi(getenv("CNPINT_FS_SKIP")) : 0;
   a.skip = skip;
+#else
+  a.skip = 0;
+#endif
   a.cnt = c->d_fscnt; a.ticket = c->d_fscnt + S.nxb; a.tick_base = c->fs_tick; a.base = c->fs_cnt;
   kern<<<grid, G::NT, G::bytes, c->stream>>>(a, S);
   c->fs_cnt += (unsigned)(S.n[0] + S.n[1]);  // phases 0 and 1 count per block

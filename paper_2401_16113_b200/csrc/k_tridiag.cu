@@ -499,10 +499,15 @@ TriCfg tri_cfg(int m, int toeplitz) {
 
 // timing experiments only (results wrong): CNPINT_TRI_SKIP bit 1 = no load, 2 = no chunk sweeps,
 // 4 = no store
+// (read only in builds with -DCNPINT_EXPERIMENTS; the product build always runs every phase)
 static int tri_skip() {
+#ifdef CNPINT_EXPERIMENTS
   static int v = -1;
   if (v < 0) v = getenv("CNPINT_TRI_SKIP") ? atoi(getenv("CNPINT_TRI_SKIP")) : 0;
   return v;
+#else
+  return 0;
+#endif
 }
 
 template <int MODE, int L, int MAXT>
