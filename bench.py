@@ -446,7 +446,7 @@ def main(argv=None):
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--alpha", type=float, default=0.01)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-streams", type=int, default=3, help="concurrent handles for the e2e measurement")
+    ap.add_argument("--e2e-streams", type=int, default=4, help="concurrent handles for the e2e measurement")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "cnpint":
         args.warmup = 3  # timing rule: at least 3 warm-up steps
