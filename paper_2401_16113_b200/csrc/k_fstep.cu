@@ -465,62 +465,39 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
           fs_signal(a.cnt + xb);
         }
       } else {
-        // ---- MODE 1 pass A': gather Z for both members from the stored rows min(k, N − k) into
-        //      the step-1 layout x[n2 + R2 n1] at n2·G1 + n1
-        const int n0 = (H - k2) / N2 + 1;
-        const int n1r = two ? (H - k2m) / N2 + 1 : 0;
-        constexpr int GIT = (N1 * NF + NT - 1) / NT;  // ≥ (n0 + n1r)·NF / NT
-        double2 ga[GIT], gb[GIT];
-#pragma unroll
-        for (int i2 = 0; i2 < GIT; ++i2) {  // all row loads first (memory-level parallelism)
-          const int q = tid + i2 * NT;
-          ga[i2] = gb[i2] = make_double2(0.0, 0.0);
-          if (q < (n0 + n1r) * NF) {
-            const int r = q / NF, pp = q - r * NF;
-            const int k = r < n0 ? k2 + N2 * r : k2m + N2 * (r - n0);
-            const int gcol = col0 + 2 * (h * NF + pp);
-            if (gcol < W) {
-              const double2* src = a.spin + (int64_t)k * W + gcol;
-              ga[i2] = ldg_cs2(src);
-              gb[i2] = ldg_cs2(src + 1);
-            }
-          }
-        }
-#pragma unroll
-        for (int i2 = 0; i2 < GIT; ++i2) {
-          const int q = tid + i2 * NT;
-          if (q >= (n0 + n1r) * NF) continue;
-          const int r = q / NF, pp = q - r * NF;
-          const bool m1 = r >= n0;
-          const int k1o = m1 ? r - n0 : r;
-          const int k = (m1 ? k2m : k2) + N2 * k1o;
-          const double2 xa = ga[i2], xbv = gb[i2];
-          double2 zk, zp;
-          if (k == 0 || k == H) {
-            zk = zp = make_double2(xa.x, xbv.x);
-          } else {
-            zk = fs_pack(xa, xbv);
-            zp = fs_pack(cconj(xa), cconj(xbv));
-          }
-          int pm, pk;
-          if (m1) { pm = 0; pk = N1 - 1 - k1o; }
-          else if (k2 == 0) { pm = 0; pk = (N1 - k1o) & (N1 - 1); }
-          else if (!two) { pm = 0; pk = N1 - 1 - k1o; }
-          else { pm = 1; pk = N1 - 1 - k1o; }
-          buf[((m1 ? NF : 0) + pp) * F1::SC + (k1o % F1::R2) * F1::G1 + k1o / F1::R2] = zk;
-          buf[(pm * NF + pp) * F1::SC + (pk % F1::R2) * F1::G1 + pk / F1::R2] = zp;
-        }
+        // ---- MODE 1 pass A': every step-1 thread loads the Z values of its own column straight from
+        //      the stored half spectrum: Z_k for k = km + N2 j ≤ H from row k, else the conjugate of
+        //      row N − k (the partner member's row, or the own member's for the self-paired
+        //      families) — each row is read by both member columns (the second read hits L2/L1)
         for (int q = tid; q < N1; q += NT) {  // ω_N^{k2 t1}, ω_N^{k2m t1} (conjugated at use)
           twn[q] = __ldg(a.twN + ((k2 * q) & (N - 1)));
           twn[N1 + q] = __ldg(a.twN + ((k2m * q) & (N - 1)));
         }
-        __syncthreads();
         double2 v[F1::R1];
         if (j < F1::R2) {
+          const int n2 = j;
+          double2 ga[F1::R1], gb[F1::R1];
 #pragma unroll
-          for (int n1 = 0; n1 < F1::R1; ++n1) v[n1] = fb[j * F1::G1 + n1];
+          for (int n1 = 0; n1 < F1::R1; ++n1) {  // all loads first
+            const int jj = n2 + F1::R2 * n1;
+            const int k = km + N2 * jj;
+            const int kr = k <= H ? k : N - k;
+            ga[n1] = gb[n1] = make_double2(0.0, 0.0);
+            if (active && colok) {
+              const double2* src = a.spin + (int64_t)kr * W + mycol;
+              ga[n1] = ldg_cs2(src);
+              gb[n1] = ldg_cs2(src + 1);
+            }
+          }
+#pragma unroll
+          for (int n1 = 0; n1 < F1::R1; ++n1) {
+            const int k = km + N2 * (n2 + F1::R2 * n1);
+            const double2 xa = ga[n1], xbv = gb[n1];
+            v[n1] = (k == 0 || k == H) ? make_double2(xa.x, xbv.x)
+                    : k < H ? fs_pack(xa, xbv) : fs_pack(cconj(xa), cconj(xbv));
+          }
         }
-        __syncthreads();  // the gather layout is read: the areas now take the exchange layout
+        __syncthreads();  // twn ready; the previous users of the areas are done
         if (j < F1::R2) rf_step1<F1, true>(v, fb, tw1, j);
         __syncthreads();
         if (j < F1::R1 && active) {
