@@ -188,61 +188,60 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
                                                   double cyu, double cdiag, int tchunk, double* __restrict__ part,
                                                   double* __restrict__ out, unsigned* counter,
                                                   DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr) {
+  // Warp wy of the block owns y row ybase + wy; its y−1 / y+1 neighbours are read straight from
+  // global memory through L1 (the block's other warps load the same rows, so most of those reads
+  // hit L1) — no shared-memory exchange and no barrier per time row.  x-neighbours by __shfl.
   double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
   for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
-  __shared__ double2 S[2][10][32];
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
-  const int ybase = blockIdx.y * 8;
-  const int yrow = ybase + wy;
-  const int ntiles_t = gridDim.z;
+  const int yrow = blockIdx.y * 8 + wy;
   const int t0 = blockIdx.z * tchunk;
   const int t1 = min(N, t0 + tchunk);
-  (void)ntiles_t;
   const bool colok = x0 < ld;
   const bool rowok = yrow < ny;
   const bool act = colok && rowok;
-  // halo rows handled by warp 0 (row ybase-1) and warp 7 (row ybase+8)
-  const int hrow = (wy == 0) ? ybase - 1 : (wy == 7 ? ybase + 8 : -1);
-  const bool hact = colok && hrow >= 0 && hrow < ny && (wy == 0 || wy == 7);
   const bool hasL = act && lane == 0 && x0 > 0;
   const bool hasR = act && lane == 31 && x0 + 2 < ld;
+  const bool hasD = act && yrow > 0;
+  const bool hasU = act && yrow + 1 < ny;
   const int64_t slice = (int64_t)ny * ld;
   const int64_t off = (int64_t)yrow * ld + x0;
-  const int64_t hoff = (int64_t)hrow * ld + x0;
 
-  double2 pv = make_double2(0, 0), ph = make_double2(0, 0);
+  auto ld2 = [&](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
+  double2 pv = make_double2(0, 0), pd = pv, pu = pv;
   double pl = 0, pr = 0;
   if (t0 > 0 || MODE == 1) {
     const double sc = (t0 > 0) ? 1.0 : alpha;
-    const double* r = u + (int64_t)((t0 > 0) ? t0 - 1 : N - 1) * slice;
-    if (act) pv = *reinterpret_cast<const double2*>(r + off);
-    if (hact) ph = *reinterpret_cast<const double2*>(r + hoff);
-    if (hasL) pl = r[off - 1];
-    if (hasR) pr = r[off + 2];
-    pv.x *= sc; pv.y *= sc; ph.x *= sc; ph.y *= sc; pl *= sc; pr *= sc;
+    const double* r = u + (int64_t)((t0 > 0) ? t0 - 1 : N - 1) * slice + off;
+    if (act) pv = ld2(r);
+    if (hasD) pd = ld2(r - ld);
+    if (hasU) pu = ld2(r + ld);
+    if (hasL) pl = r[-1];
+    if (hasR) pr = r[2];
+    pv.x *= sc; pv.y *= sc; pd.x *= sc; pd.y *= sc; pu.x *= sc; pu.y *= sc; pl *= sc; pr *= sc;
   }
   double acc = 0.0;
-  int buf = 0;
   // rows in batches whose loads are all issued before use (see k_matvec1d)
   constexpr int TB = NVD <= 1 ? 4 : NVD <= 3 ? 2 : 1;
   for (int tb = t0; tb < t1; tb += TB) {
-    double2 cvb[TB], chb[TB], bvb[TB], vvb[TB][NVD > 0 ? NVD : 1];
+    double2 cvb[TB], cdb[TB], cub[TB], bvb[TB], vvb[TB][NVD > 0 ? NVD : 1];
     double clb[TB], crb[TB];
 #pragma unroll
     for (int q = 0; q < TB; ++q) {
       const int t = tb + q;
-      cvb[q] = chb[q] = bvb[q] = make_double2(0, 0);
+      cvb[q] = cdb[q] = cub[q] = bvb[q] = make_double2(0, 0);
       clb[q] = crb[q] = 0.0;
 #pragma unroll
       for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) vvb[q][i] = make_double2(0, 0);
       if (t < t1) {
-        const double* r = u + (int64_t)t * slice;
-        if (act) cvb[q] = ldg_cs2(reinterpret_cast<const double2*>(r + off));
-        if (hact) chb[q] = *reinterpret_cast<const double2*>(r + hoff);
-        if (hasL) clb[q] = r[off - 1];
-        if (hasR) crb[q] = r[off + 2];
+        const double* r = u + (int64_t)t * slice + off;
+        if (act) cvb[q] = ld2(r);
+        if (hasD) cdb[q] = ld2(r - ld);
+        if (hasU) cub[q] = ld2(r + ld);
+        if (hasL) clb[q] = r[-1];
+        if (hasR) crb[q] = r[2];
         if (MODE >= 2 && act) bvb[q] = ldg_cs2(reinterpret_cast<const double2*>(b + (int64_t)t * slice + off));
         if (NVD > 0 && act) {
 #pragma unroll
@@ -254,20 +253,15 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
 #pragma unroll
     for (int q = 0; q < TB; ++q) {
       const int t = tb + q;
-      if (t >= t1) break;  // uniform over the block (t1 is)
-      const double2 cv = cvb[q], ch = chb[q];
-      const double cl = clb[q], cr = crb[q];
+      if (t >= t1) break;
+      const double2 cv = cvb[q];
       const double2 s = make_double2(cv.x + pv.x, cv.y + pv.y);
-      S[buf][wy + 1][lane] = s;
-      if (wy == 0) S[buf][0][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
-      if (wy == 7) S[buf][9][lane] = hact ? make_double2(ch.x + ph.x, ch.y + ph.y) : make_double2(0, 0);
-      __syncthreads();
-      const double2 sd = S[buf][wy][lane];       // row y-1
-      const double2 su = S[buf][wy + 2][lane];   // row y+1
+      const double2 sd = make_double2(cdb[q].x + pd.x, cdb[q].y + pd.y);  // row y−1
+      const double2 su = make_double2(cub[q].x + pu.x, cub[q].y + pu.y);  // row y+1
       double sl = __shfl_up_sync(0xffffffffu, s.y, 1);
       double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
-      if (lane == 0) sl = hasL ? cl + pl : 0.0;
-      if (lane == 31) sr = hasR ? cr + pr : 0.0;
+      if (lane == 0) sl = hasL ? clb[q] + pl : 0.0;
+      if (lane == 31) sr = hasR ? crb[q] + pr : 0.0;
       const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
       double y0 = (cv.x - pv.x) - ht * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
       double y1 = (cv.y - pv.y) - ht * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
@@ -285,8 +279,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
         }
         if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
       }
-      pv = cv; ph = ch; pl = cl; pr = cr;
-      buf ^= 1;
+      pv = cv; pd = cdb[q]; pu = cub[q]; pl = clb[q]; pr = crb[q];
     }
   }
   if (NORM) block_partial<256>(acc, part, out, counter);
