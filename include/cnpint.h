@@ -115,6 +115,7 @@ size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max)
 cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op,
                             int restart_max, void* d_workspace, size_t ws_bytes, void* cuda_stream);
 
+/* Waits for the handle's stream, then frees the handle (not the caller's workspace). */
 void cnpint_destroy(cnpint_ctx* ctx);
 const char* cnpint_last_error(const cnpint_ctx* ctx);
 /* Moves the handle to another stream; if it differs from the current one, the current stream is

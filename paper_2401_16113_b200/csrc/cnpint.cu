@@ -505,6 +505,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
 
 void cnpint_destroy(cnpint_ctx* c) {
   if (!c) return;
+  cudaStreamSynchronize(c->stream);  // the caller may release the workspace right after this call
   prof_free(c);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
