@@ -697,6 +697,20 @@ static cnpint_status gmres_args(cnpint_ctx* c, const double* d_b, double* d_u, d
   return CNPINT_OK;
 }
 
+// Post-fold GMRES steps (see PostOp): the reducing kernel that produces ||w||² runs them in its last
+// block instead of a separate single-thread launch.
+static PostOp post_cycle_start(const cnpint_ctx* c, int first) {
+  PostOp p{};
+  p.op = 2; p.first = first; p.rmax = c->restart_max; p.scl = c->d_scl; p.g = c->d_g; p.scal = c->d_scal;
+  return p;
+}
+static PostOp post_finalize(const cnpint_ctx* c, int j) {
+  PostOp p{};
+  p.op = 1; p.j = j; p.ldh = c->restart_max + 1; p.c1 = c->d_c1; p.c2 = c->d_c2; p.scl = c->d_scl; p.H = c->d_H;
+  p.cs = c->d_cs; p.sn = c->d_sn; p.g = c->d_g; p.scal = c->d_scal;
+  return p;
+}
+
 // CGS2 of w (already in its basis slot) against Ṽ_0..Ṽ_{nv−1}: c1 = Ṽᵀw (unless the producer fused
 // it: have_c1), c2 = Ṽᵀ(w − Ṽs²c1), w −= Ṽ s²(c1 + c2) with ||w||² fused into scal[2].
 // More than CNP_MAX_DOT vectors: groups of CNP_MAX_DOT (dots, update, dots, update, norm).
@@ -733,6 +747,7 @@ static cnpint_status cgs2(cnpint_ctx* c, double* const* V, int nv, double* w, bo
 cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
                            cnpint_gmres_report* rep) {
   if (cnpint_status a = gmres_args(c, d_b, d_u, tol, restart, maxit)) return a;
+  c->post = PostOp{};
   auto t0 = std::chrono::steady_clock::now();
   const int64_t vec = c->vec;
   double* h = c->h_pinned;
@@ -746,8 +761,8 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   // ||b||: first basis vector is b itself (x0 = 0 ⇒ r0 = b)
   double* b_nc = const_cast<double*>(d_b);
   V[0] = b_nc;
+  c->post = post_cycle_start(c, 1);  // run by launch_norm2's folding block
   CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));
-  CK(launch_small(c, 0, 0, 1));
   CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
@@ -775,8 +790,9 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       } else {
         CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
       }
+      if (nv <= CNP_MAX_DOT) c->post = post_finalize(c, j);  // run by CGS2's last (norm) pass
       if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
-      CK(launch_small(c, 1, j, 0));
+      if (nv > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
       CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       ++its;
@@ -800,16 +816,16 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     // store); otherwise r is written into the workspace slot of Ṽ_0 for the next cycle (b is kept)
     V[0] = c->d_V;
     const bool likely_done = est <= tol;
+    c->post = post_cycle_start(c, 0);  // run by the residual matvec's folding block
     CK(launch_matvec(c, d_u, V[0], likely_done ? 3 : 2, d_b, c->d_part, c->d_scal + 2));
-    CK(launch_small(c, 0, 0, 0));
     CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     relres_true = h[4];
     ++cycles;
     if (relres_true <= tol) { converged = 1; break; }
     if (likely_done) {  // estimate and true residual disagree: form r for the restart after all
+      c->post = post_cycle_start(c, 0);
       CK(launch_matvec(c, d_u, V[0], 2, d_b, c->d_part, c->d_scal + 2));
-      CK(launch_small(c, 0, 0, 0));
     }
     if (its >= maxit) { result = CNPINT_ENOCONV; break; }
     if (!std::isfinite(relres_true)) { seterr(c, "gmres: residual not finite"); result = CNPINT_EBREAKDOWN; break; }
@@ -834,6 +850,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
 cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, double tol, int restart, int maxit,
                                 cnpint_gmres_report* rep) {
   if (cnpint_status a = gmres_args(c, d_b, d_u, tol, restart, maxit)) return a;
+  c->post = PostOp{};
   auto t0 = std::chrono::steady_clock::now();
   const int64_t vec = c->vec;
   double* h = c->h_pinned;
@@ -847,8 +864,8 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
   CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 7));
   // r_0 = P⁻¹b (x0 = 0), β = ||r_0||
   if (cnpint_status st = pinv_dev(c, d_b, nullptr, V[0], 0)) return st;
+  c->post = post_cycle_start(c, 1);
   CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
-  CK(launch_small(c, 0, 0, 1));
   CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const double bnorm = std::sqrt(h[7]);
@@ -874,8 +891,9 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
       CK(launch_matvec(c, V[j], tmp, 0, nullptr, nullptr));
       double* w = V[j + 1];
       if (cnpint_status st = pinv_dev(c, tmp, c->d_scl + j, w, 0)) return st;
+      if (j + 1 <= CNP_MAX_DOT) c->post = post_finalize(c, j);
       if (cnpint_status cs = cgs2(c, V.data(), j + 1, w, false)) return cs;
-      CK(launch_small(c, 1, j, 0));
+      if (j + 1 > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
       CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       ++its;
@@ -899,8 +917,8 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
     // b − 𝓜u (its norm²: the unpreconditioned residual), r = P⁻¹(b − 𝓜u) → Ṽ_0 of the next cycle
     CK(launch_matvec(c, d_u, tmp, 2, d_b, c->d_part, c->d_scal + 6));
     if (cnpint_status st = pinv_dev(c, tmp, nullptr, V[0], 0)) return st;
+    c->post = post_cycle_start(c, 0);
     CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
-    CK(launch_small(c, 0, 0, 0));
     CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     relres_prec = h[4];

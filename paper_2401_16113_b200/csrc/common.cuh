@@ -66,8 +66,9 @@ CNP_DEV void block_reduce_nv(double (&acc)[NV], double* part, int stride) {
 // (col < ncols); the last block to arrive (atomic ticket) adds them up in block order — lane l sums
 // b = l, l+32, ... in order, then a fixed shuffle tree — and writes out[col], so the result does not
 // depend on which block finishes last (bitwise reproducible).  Partials are read with ld.global.cg
-// (L2) since other blocks wrote them.  The counter is reset for the next launch.
-CNP_DEV void grid_fold(const double* part, int nparts, int stride, int ncols, double* out, unsigned* counter) {
+// (L2) since other blocks wrote them.  The counter is reset for the next launch.  Returns true in
+// the block that folded.
+CNP_DEV bool grid_fold(const double* part, int nparts, int stride, int ncols, double* out, unsigned* counter) {
   __shared__ bool amlast;
   __shared__ double red[32][10];
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
@@ -75,7 +76,7 @@ CNP_DEV void grid_fold(const double* part, int nparts, int stride, int ncols, do
   __syncthreads();
   if (tid == 0) amlast = atomicAdd(counter, 1u) == (unsigned)(nparts - 1);
   __syncthreads();
-  if (!amlast) return;
+  if (!amlast) return false;
   __threadfence();
   // every thread sums a fixed strided subset of the partials for all columns (independent L2 loads),
   // then warp trees and a fixed-order sum over warps
@@ -105,6 +106,7 @@ CNP_DEV void grid_fold(const double* part, int nparts, int stride, int ncols, do
     out[tid] = v;
   }
   if (tid == 0) *counter = 0u;
+  return true;  // this block did the fold (its thread tid < ncols wrote out[tid])
 }
 
 // Padded shared-memory index for complex FFT buffers: one pad entry every 16 elements breaks the

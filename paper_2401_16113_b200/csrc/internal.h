@@ -31,6 +31,23 @@ static inline __host__ __device__ int tri_rows_alloc(int m, int padsh) {
   return (m + B - 1) / B * B;
 }
 
+// Small GMRES step run by the last block of a reducing kernel right after its deterministic fold
+// (saves a single-thread kernel launch): op 1 = Arnoldi finalize of column j (Hessenberg column,
+// Givens, estimate; reads the fold's ||w||² from scal[2]), op 2 = cycle start (β = sqrt(scal[2]),
+// first: ||b||, scale s_0 = 1/β, g = β e_1).  Set in cnpint_ctx::post by the host before the launch
+// of the reducing kernel, which passes it on and clears it.
+struct PostOp {
+  int op, j, ldh, first, rmax;
+  const double* c1;
+  const double* c2;
+  double* scl;
+  double* H;
+  double* cs;
+  double* sn;
+  double* g;
+  double* scal;
+};
+
 struct cnpint_ctx {
   // problem
   int dim, nx, ny, N, H, toeplitz;
@@ -94,6 +111,7 @@ struct cnpint_ctx {
   int* d_status;       // device status word (bit 0: singular pivot)
   unsigned* d_counter; // grid_fold ticket counter (zero between launches)
   double* h_pinned;    // pinned host scalars [8]
+  PostOp post;         // pending post-fold operation for the next reducing launch (op 0 = none)
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
   void* prof;          // CnpProf* (host event pools), null when profiling is off

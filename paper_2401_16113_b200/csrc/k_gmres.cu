@@ -11,6 +11,7 @@
 // one block per output sums them in a fixed order (bitwise reproducible runs, no atomics).
 #include "common.cuh"
 #include "internal.h"
+#include "post_op.cuh"
 
 struct VPtrs {
   const double* p[CNP_MAX_DOT];
@@ -58,7 +59,8 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double*
 // Σ w² (one read of w), folded into out
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restrict__ w, size_t n2,
                                                             double* __restrict__ part, int stride,
-                                                            double* __restrict__ out, unsigned* counter) {
+                                                            double* __restrict__ out, unsigned* counter,
+                                                            PostOp post) {
   double acc[1] = {0.0};
   const double2* w2 = reinterpret_cast<const double2*>(w);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
     acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
   }
   block_reduce_write<1>(acc, part, stride);
-  grid_fold(part, gridDim.x, stride, 1, out, counter);
+  if (grid_fold(part, gridDim.x, stride, 1, out, counter)) run_post(post);
 }
 
 // w_out = w − Σ_i coef_i Ṽ_i with coef_i = (cd[i] + cd2[i])·s_i² (MODE 0; cd2 may be null) or
@@ -78,7 +80,8 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
                                                              const double* __restrict__ scl, const double* w,
                                                              double* wout, size_t n2, double* __restrict__ part,
                                                              int stride, double* __restrict__ out, unsigned* counter,
-                                                             const double* __restrict__ cd2 = nullptr) {
+                                                             const double* __restrict__ cd2 = nullptr,
+                                                             PostOp post = PostOp{}) {
   double coef[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? (cd[i] + (cd2 ? cd2[i] : 0.0)) * scl[i] * scl[i] : cd[i];
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
     if (out) grid_fold(part, gridDim.x, stride, NV, out, counter);
   } else if constexpr (NORM) {
     block_reduce_write<1>(acc, part, stride);
-    if (out) grid_fold(part, gridDim.x, stride, 1, out, counter);
+    if (out && grid_fold(part, gridDim.x, stride, 1, out, counter)) run_post(post);
   }
 }
 
@@ -133,42 +136,12 @@ __global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ part,
 // scal[0] = ||b||, scal[1] = estimate, scal[2] = ||w||² (reduced), scal[3] = non-finite flag,
 // scal[4] = true residual ||r||/||b||
 __global__ void k_cycle_start(double* scl, double* g, double* scal, int first, int rmax) {
-  if (threadIdx.x != 0) return;
-  const double beta = sqrt(scal[2]);
-  if (first) scal[0] = beta;
-  scal[4] = beta / scal[0];
-  scl[0] = beta > 0.0 ? 1.0 / beta : 0.0;
-  for (int i = 0; i <= rmax; ++i) g[i] = 0.0;
-  g[0] = beta;
-  if (!isfinite(beta)) scal[3] = 1.0;
+  if (threadIdx.x == 0) cycle_start_dev(scl, g, scal, first, rmax);
 }
 
 __global__ void k_arnoldi_finalize(int j, int ldh, const double* c1, const double* c2, double* scl, double* H,
                                    double* cs, double* sn, double* g, double* scal) {
-  if (threadIdx.x != 0) return;
-  double* h = H + (size_t)j * ldh;
-  for (int i = 0; i <= j; ++i) h[i] = scl[i] * (c1[i] + c2[i]);
-  const double beta = sqrt(scal[2]);
-  h[j + 1] = beta;
-  scl[j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
-  for (int i = 0; i < j; ++i) {  // previous rotations
-    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
-    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
-    h[i] = t;
-  }
-  const double den = hypot(h[j], h[j + 1]);
-  const double c = den > 0.0 ? h[j] / den : 1.0;
-  const double s = den > 0.0 ? h[j + 1] / den : 0.0;
-  cs[j] = c;
-  sn[j] = s;
-  h[j] = den;
-  h[j + 1] = 0.0;
-  g[j + 1] = -s * g[j];
-  g[j] = c * g[j];
-  const double est = fabs(g[j + 1]) / scal[0];
-  scal[1] = est;
-  if (!isfinite(est) || !isfinite(den)) scal[3] = 1.0;
-  if (beta == 0.0) scal[5] = 1.0;  // happy breakdown
+  if (threadIdx.x == 0) arnoldi_finalize_dev(j, ldh, c1, c2, scl, H, cs, sn, g, scal);
 }
 
 // y = H[0:k,0:k]^{-1} g[0:k]; coef_i = y_i s_i  (combination Σ coef_i Ṽ_i = V y)
@@ -213,7 +186,10 @@ cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* 
 
 cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* out) {
   cnp_prof_begin(c, KID_DOTS);
-  k_norm2<<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
+  const PostOp post = c->post;
+  c->post = PostOp{};
+  k_norm2<<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
+                                                             post);
   cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c));
   return cudaGetLastError();
 }
@@ -242,9 +218,12 @@ static void upd_cgs(cnpint_ctx* c, const VPtrs& V, const double* c1, const doubl
   if (phase == 0)  // c2 = Ṽᵀ(w − Ṽ s² c1), nothing written
     k_update<NV, 0, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
         V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, nullptr);
-  else  // w ← w − Ṽ s² (c1 + c2), ‖w‖²
+  else {  // w ← w − Ṽ s² (c1 + c2), ‖w‖², then the pending post-fold step (Arnoldi finalize)
+    const PostOp post = c->post;
+    c->post = PostOp{};
     k_update<NV, 0, false, true, false><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
-        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2);
+        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2, post);
+  }
 }
 
 // CGS2 with one write: phase 0 forms c2 = Ṽᵀ(w − Ṽ s²c1) (reads Ṽ and w, writes nothing), phase 1

@@ -8,6 +8,7 @@
 // exchange.  16 B/unknown of compulsory traffic (read u, write y).
 #include "common.cuh"
 #include "internal.h"
+#include "post_op.cuh"
 
 #include <algorithm>
 
@@ -59,7 +60,8 @@ cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir
 
 // ------------------------------------------------------------------------ block-level sum helper
 template <int NT>
-CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsigned* counter = nullptr) {
+CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsigned* counter = nullptr,
+                           const PostOp& post = PostOp{}) {
   __shared__ double red[NT / 32];
   v = warp_sum(v);
   int w = threadIdx.x / 32 + threadIdx.y * (blockDim.x / 32);
@@ -70,7 +72,7 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
     for (int i = 0; i < NT / 32; ++i) s += red[i];
     part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (size_t)blockIdx.z)] = s;
   }
-  if (out) grid_fold(part, gridDim.x * gridDim.y * gridDim.z, 1, 1, out, counter);
+  if (out && grid_fold(part, gridDim.x * gridDim.y * gridDim.z, 1, 1, out, counter)) run_post(post);
 }
 
 // ------------------------------------------------------------------------------- K1 1D
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   int N, int64_t ld, double htau, double alpha, int tchunk,
                                                   double* __restrict__ part, double* __restrict__ out,
                                                   unsigned* counter, DotPtrs vd = DotPtrs{},
-                                                  const double* __restrict__ dt = nullptr) {
+                                                  const double* __restrict__ dt = nullptr, PostOp post = PostOp{}) {
   double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
   for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
       pv = cv; pl = cl; pr = cr;
     }
   }
-  if (NORM) block_partial<128>(acc, part, out, counter);
+  if (NORM) block_partial<128>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
     grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
@@ -187,7 +189,8 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
                                                   double htau, double alpha, double cxs, double cxu, double cys,
                                                   double cyu, double cdiag, int tchunk, double* __restrict__ part,
                                                   double* __restrict__ out, unsigned* counter,
-                                                  DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr) {
+                                                  DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr,
+                                                  PostOp post = PostOp{}) {
   // Warp wy of the block owns y row ybase + wy; its y−1 / y+1 neighbours are read straight from
   // global memory through L1 (the block's other warps load the same rows, so most of those reads
   // hit L1) — no shared-memory exchange and no barrier per time row.  x-neighbours by __shfl.
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
       pv = cv; pd = cdb[q]; pu = cub[q]; pl = clb[q]; pr = crb[q];
     }
   }
-  if (NORM) block_partial<256>(acc, part, out, counter);
+  if (NORM) block_partial<256>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
     grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
@@ -296,20 +299,23 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
   // 𝓜 (modes 0, 2, 3) weights row t by d(t_{t+½}); P_α (mode 1) uses d̄
   const double htau = 0.5 * (MODE == 1 ? c->tau_p : c->tau);
   const double* dt = MODE == 1 ? nullptr : c->d_dt;
+  const PostOp post = NORM ? c->post : PostOp{};  // pending post-fold step (cycle start)
+  if (NORM) c->post = PostOp{};
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec1d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau,
-                                                         c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt);
+                                                         c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt,
+                                                         post);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec2d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
                                                          c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
-                                                         part, out, c->d_counter, DotPtrs{}, dt);
+                                                         part, out, c->d_counter, DotPtrs{}, dt, post);
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
   return cudaGetLastError();

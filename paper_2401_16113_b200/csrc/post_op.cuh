@@ -1,0 +1,53 @@
+// Device bodies of the small GMRES steps (k_gmres.cu's single-thread kernels and the post-fold hook
+// of the reducing kernels).  scal[0] = ||r_0||, scal[1] = estimate, scal[2] = ||w||² (reduced),
+// scal[3] = non-finite flag, scal[4] = ||r||/||r_0||, scal[5] = happy breakdown.
+#pragma once
+#include "common.cuh"
+#include "internal.h"
+
+CNP_DEV void cycle_start_dev(double* scl, double* g, double* scal, int first, int rmax) {
+  const double beta = sqrt(scal[2]);
+  if (first) scal[0] = beta;
+  scal[4] = beta / scal[0];
+  scl[0] = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i <= rmax; ++i) g[i] = 0.0;
+  g[0] = beta;
+  if (!isfinite(beta)) scal[3] = 1.0;
+}
+
+CNP_DEV void arnoldi_finalize_dev(int j, int ldh, const double* c1, const double* c2, double* scl, double* H,
+                                  double* cs, double* sn, double* g, double* scal) {
+  double* h = H + (size_t)j * ldh;
+  for (int i = 0; i <= j; ++i) h[i] = scl[i] * (c1[i] + c2[i]);
+  const double beta = sqrt(scal[2]);
+  h[j + 1] = beta;
+  scl[j + 1] = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i < j; ++i) {  // previous rotations
+    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+    h[i] = t;
+  }
+  const double den = hypot(h[j], h[j + 1]);
+  const double c = den > 0.0 ? h[j] / den : 1.0;
+  const double s = den > 0.0 ? h[j + 1] / den : 0.0;
+  cs[j] = c;
+  sn[j] = s;
+  h[j] = den;
+  h[j + 1] = 0.0;
+  g[j + 1] = -s * g[j];
+  g[j] = c * g[j];
+  const double est = fabs(g[j + 1]) / scal[0];
+  scal[1] = est;
+  if (!isfinite(est) || !isfinite(den)) scal[3] = 1.0;
+  if (beta == 0.0) scal[5] = 1.0;  // happy breakdown
+}
+
+// Called by the whole last block after grid_fold returned true (its thread 0 wrote scal[2]).
+CNP_DEV void run_post(const PostOp& p) {
+  if (p.op == 0) return;
+  __threadfence_block();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    if (p.op == 1) arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
+    else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax);
+  }
+}
