@@ -806,11 +806,15 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
     }
     // cycle end: y = H⁻¹g, u += Σ y_j z_j  (= P⁻¹ V y: the stored z_j make the extra P⁻¹ unnecessary)
-    CK(launch_small(c, 2, jdone, 0));
-    for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
-      int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
-      const bool fresh = cycles == 0 && g0 == 0;  // u = Σ y_j z_j (no read of an initial zero u)
-      CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part, nullptr));
+    if (jdone <= CNP_MAX_DOT) {  // back-substitution inside the combine kernel
+      CK(launch_combine_backsolve(c, Z.data(), jdone, 0, cycles == 0 ? nullptr : d_u, d_u));
+    } else {
+      CK(launch_small(c, 2, jdone, 0));
+      for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
+        int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
+        const bool fresh = cycles == 0 && g0 == 0;  // u = Σ y_j z_j (no read of an initial zero u)
+        CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part, nullptr));
+      }
     }
     // true residual ‖b − 𝓜u‖: when the estimate says converged only its norm is needed (mode 3, no
     // store); otherwise r is written into the workspace slot of Ṽ_0 for the next cycle (b is kept)
@@ -907,12 +911,16 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
       if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
     }
     // cycle end: y = H⁻¹g, u += V y = Σ (y_i s_i) Ṽ_i  (no P⁻¹ with left preconditioning)
-    CK(launch_small(c, 2, jdone, 0));
-    for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
-      int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
-      const bool fresh = cycles == 0 && g0 == 0;
-      CK(launch_update(c, V.data() + g0, ng, c->d_coef + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part,
-                       nullptr));
+    if (jdone <= CNP_MAX_DOT) {  // back-substitution inside the combine kernel (coef = y s)
+      CK(launch_combine_backsolve(c, V.data(), jdone, 1, cycles == 0 ? nullptr : d_u, d_u));
+    } else {
+      CK(launch_small(c, 2, jdone, 0));
+      for (int g0 = 0; g0 < jdone; g0 += CNP_MAX_DOT) {
+        int ng = jdone - g0 < CNP_MAX_DOT ? jdone - g0 : CNP_MAX_DOT;
+        const bool fresh = cycles == 0 && g0 == 0;
+        CK(launch_update(c, V.data() + g0, ng, c->d_coef + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part,
+                         nullptr));
+      }
     }
     // b − 𝓜u (its norm²: the unpreconditioned residual), r = P⁻¹(b − 𝓜u) → Ṽ_0 of the next cycle
     CK(launch_matvec(c, d_u, tmp, 2, d_b, c->d_part, c->d_scal + 6));

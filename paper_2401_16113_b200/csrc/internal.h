@@ -167,6 +167,8 @@ cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* o
 // partial sums into part; if out != nullptr the last block folds them (deterministically) into out
 cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w, double* part, double* out);
 cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int accumulate_sq);
+cudaError_t launch_combine_backsolve(cnpint_ctx* c, double* const* X, int nv, int scaled, const double* u_in,
+                                     double* u_out);
 cudaError_t launch_cgs2_pass(cnpint_ctx* c, double* const* V, int nv, const double* c1, const double* c2,
                              double* w, double* part, double* out, int phase);
 cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,

@@ -212,6 +212,63 @@ static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w
       V, cd, c->d_scl, w, wout, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
 }
 
+// Cycle end with the Hessenberg back-substitution folded in: every block solves y = H[0:NV,0:NV]⁻¹g
+// (NV ≤ CNP_MAX_DOT, a few hundred flops, H from L2) into shared memory, then u ← u + Σ coef_i X_i
+// with coef_i = y_i (right preconditioning, X = Z) or y_i s_i (left, X = Ṽ).  Replaces k_backsolve
+// + k_update<MODE 1>.  u_in may be null (fresh u).
+template <int NV>
+__global__ void __launch_bounds__(CNP_RED_THREADS) k_combine_bs(VPtrs X, const double* __restrict__ H, int ldh,
+                                                                 const double* __restrict__ g,
+                                                                 const double* __restrict__ scl, int scaled,
+                                                                 const double* u_in, double* u_out, size_t n2) {
+  __shared__ double cs_[NV];
+  if (threadIdx.x == 0) {
+    double y[NV];
+#pragma unroll
+    for (int i = NV - 1; i >= 0; --i) {
+      double s = g[i];
+#pragma unroll
+      for (int l = i + 1; l < NV; ++l) s -= H[i + (size_t)l * ldh] * y[l];
+      y[i] = s / H[i + (size_t)i * ldh];
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) cs_[i] = scaled ? y[i] * scl[i] : y[i];
+  }
+  __syncthreads();
+  double coef[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) coef[i] = cs_[i];
+  const double2* w2 = reinterpret_cast<const double2*>(u_in);
+  double2* o2 = reinterpret_cast<double2*>(u_out);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+    double2 x = w2 ? w2[e] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 v = ldg_cs2(reinterpret_cast<const double2*>(X.p[i]) + e);
+      x.x = fma(coef[i], v.x, x.x);
+      x.y = fma(coef[i], v.y, x.y);
+    }
+    o2[e] = x;
+  }
+}
+
+cudaError_t launch_combine_backsolve(cnpint_ctx* c, double* const* Xp, int nv, int scaled, const double* u_in,
+                                     double* u_out) {
+  VPtrs X;
+  for (int i = 0; i < CNP_MAX_DOT; ++i) X.p[i] = i < nv ? Xp[i] : nullptr;
+  const int ldh = c->restart_max + 1;
+  cnp_prof_begin(c, KID_UPDATE);
+#define CB_CASE(K) \
+  case K: k_combine_bs<K><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(X, c->d_H, ldh, c->d_g, c->d_scl, scaled, u_in, u_out, n2_of(c)); break;
+  switch (nv) {
+    CB_CASE(1) CB_CASE(2) CB_CASE(3) CB_CASE(4) CB_CASE(5) CB_CASE(6) CB_CASE(7) CB_CASE(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef CB_CASE
+  cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (u_in ? 2 : 1)));
+  return cudaGetLastError();
+}
+
 template <int NV>
 static void upd_cgs(cnpint_ctx* c, const VPtrs& V, const double* c1, const double* c2, double* w, double* part,
                     double* out, int phase) {
