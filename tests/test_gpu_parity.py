@@ -385,8 +385,11 @@ def test_gmres_c3_c4():
 
 
 # ------------------------------------------------------------------------------ API behaviour
-def test_host_entry_points_match_device():
-    w = SMALL["1d_ragged"]
+@pytest.mark.parametrize("name", ["1d_ragged", "2d_small", "1d_N2048_ragged"])
+def test_host_entry_points_match_device(name):
+    """The host-buffer entry points (packed host arrays, device repack) give bitwise the device
+    results, in 1D (ragged pitch), 2D, and on the four-step FFT path."""
+    w = SMALL[name].with_(restart=20)
     s = solver_for(w, restart_max=w.restart)
     v = synth.random_vectors(w, 1, 9)[0]
     z = s.empty()
