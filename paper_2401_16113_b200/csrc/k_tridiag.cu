@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(MAXT, 2)
     const double2 r = crecip(lam1[k]);
     for (int i = p; i < m; i += P) D[sidx(i)] = cmul(D[sidx(i)], r);
   }
+  double2 dl[L];  // the chunk's right-hand side; for Toeplitz rows δ' stays here until the back-substitution
   if (act && !diag_only && !(skip & 2)) {
-    double2 dl[L];
 #pragma unroll
     for (int j = 0; j < L; ++j) dl[j] = (j < len) ? cmul(D[sidx(i0 + j)], il) : make_double2(0.0, 0.0);
     if (TOEP) {
@@ -183,9 +183,11 @@ __global__ void __launch_bounds__(MAXT, 2)
         sg.fc = tv[2];
       }
       sg.fd = len >= 3 ? crfms(dl[0], c, dl[1]) : dl[0];
+      if (!FAST) {  // the fast tree keeps δ' in registers through the merges (enough registers there)
 #pragma unroll
-      for (int j = 1; j < L - 1; ++j)
-        if (j <= len - 2) D[sidx(i0 + j)] = dl[j];
+        for (int j = 1; j < L - 1; ++j)
+          if (j <= len - 2) D[sidx(i0 + j)] = dl[j];
+      }
     } else {
       double2 ap[L], gp[L];
       double2 alp = make_double2(0.0, 0.0), gam = alp, last = dl[0];
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(MAXT, 2)
       for (int j = 1; j < L - 1; ++j) {
         if (j <= len - 2) {
           const int q = sidx(i0 + j);
-          D[q] = cfms(cfms(D[q], tv[3 + j], xs), tv[3 + L + j], xe);
+          D[q] = cfms(cfms(FAST ? dl[j] : D[q], tv[3 + j], xs), tv[3 + L + j], xe);
         }
       }
     } else {
