@@ -114,11 +114,25 @@ CNP_DEV bool grid_fold(const double* part, int nparts, int stride, int ncols, do
 CNP_DEV int padi(int i) { return i + (i >> 4); }
 static inline int padi_host(int i) { return i + (i >> 4); }
 
-// Streaming (evict-first) global loads/stores for single-use vector traffic.
+// Vector-stream loads use the default (L2-allocating) policy: measured on B200 (profiles/
+// r01_l2_policy.txt) the GMRES update finds part of the Krylov vectors the previous kernels left in
+// the 126-MB L2 (c2: K7 86.5 -> 84.6 us, c4: 182.8 -> 177.7 us); evict-first (.cs) loads were no
+// faster anywhere.  CNP_L2_STREAM_LOADS restores evict-first loads.  Stores stay evict-first
+// (CNP_L2_KEEP_STORES: default policy; measured no gain).
+#ifdef CNP_L2_STREAM_LOADS
 CNP_DEV double2 ldg_cs2(const double2* p) { return __ldcs(p); }
-CNP_DEV void stg_cs2(double2* p, double2 v) { __stcs(p, v); }
 CNP_DEV double ldg_cs(const double* p) { return __ldcs(p); }
+#else
+CNP_DEV double2 ldg_cs2(const double2* p) { return __ldg(p); }
+CNP_DEV double ldg_cs(const double* p) { return __ldg(p); }
+#endif
+#ifdef CNP_L2_KEEP_STORES
+CNP_DEV void stg_cs2(double2* p, double2 v) { *p = v; }
+CNP_DEV void stg_cs(double* p, double v) { *p = v; }
+#else
+CNP_DEV void stg_cs2(double2* p, double2 v) { __stcs(p, v); }
 CNP_DEV void stg_cs(double* p, double v) { __stcs(p, v); }
+#endif
 
 // Asynchronous 16-byte global→shared copies (cp.async, LDGSTS): no register staging, any number
 // in flight; completion per thread by commit/wait groups, then a barrier for visibility.

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
             for (int n1 = 0; n1 < F2::R1; ++n1) {
               const int t = t1b + tt + N1 * (n2 + F2::R2 * n1);
-              v[tt][n1] = (colok && !(a.skip & 1)) ? __ldcs(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
+              v[tt][n1] = (colok && !(a.skip & 1)) ? ldg_cs2(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
                                                    : make_double2(0.0, 0.0);
             }
 #pragma unroll

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(TpPlan<LOGN>::NT, TpPlan<LOGN>::MINB)
 #pragma unroll
       for (int n1 = 0; n1 < F::R1; ++n1) {
         const int t = r + F::M * n1;
-        v[n1] = ok ? __ldcs(reinterpret_cast<const double2*>(in + (int64_t)t * W + col)) : make_double2(0.0, 0.0);
+        v[n1] = ok ? ldg_cs2(reinterpret_cast<const double2*>(in + (int64_t)t * W + col)) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int n1 = 0; n1 < F::R1; ++n1) {
