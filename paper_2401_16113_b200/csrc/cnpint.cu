@@ -491,7 +491,8 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
     cudaError_t e = cudaMemcpyAsync(w, img.data(), L.tables_end, cudaMemcpyHostToDevice, c->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(w + L.tables_end, 0, L.total - L.tables_end, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-    if (e == cudaSuccess) e = cudaMallocHost((void**)&c->h_pinned, 16 * sizeof(double));
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->h_pinned, 16 * sizeof(double), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&c->d_hmap, c->h_pinned, 0);
     if (e != cudaSuccess) st = cuda_fail(c, e, "cnpint_create");
   }
   if (st != CNPINT_OK) {
@@ -578,10 +579,9 @@ cnpint_status cnpint_time_ifft(cnpint_ctx* c, const double* zhat, double* z) {
 
 cnpint_status cnpint_device_status(cnpint_ctx* c) {
   if (!c) return CNPINT_EINVAL;
-  int st = 0;
-  CK(cudaMemcpyAsync(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(launch_scal_to_host(c));  // status word via the mapped buffer (no copy-engine transfer)
   CK(cudaStreamSynchronize(c->stream));
-  if (st) {
+  if (c->h_pinned[8] != 0.0) {
     CK(cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream));
     CK(cudaStreamSynchronize(c->stream));
     seterr(c, "zero or non-finite pivot in a shifted solve (P_alpha singular to working precision)");
@@ -763,7 +763,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   V[0] = b_nc;
   c->post = post_cycle_start(c, 1);  // run by launch_norm2's folding block
   CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));
-  CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(launch_scal_to_host(c));
   CK(cudaStreamSynchronize(c->stream));
   if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
     CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
@@ -793,7 +793,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       if (nv <= CNP_MAX_DOT) c->post = post_finalize(c, j);  // run by CGS2's last (norm) pass
       if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
       if (nv > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
-      CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(launch_scal_to_host(c));
       CK(cudaStreamSynchronize(c->stream));
       ++its;
       jdone = j + 1;
@@ -822,7 +822,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     const bool likely_done = est <= tol;
     c->post = post_cycle_start(c, 0);  // run by the residual matvec's folding block
     CK(launch_matvec(c, d_u, V[0], likely_done ? 3 : 2, d_b, c->d_part, c->d_scal + 2));
-    CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(launch_scal_to_host(c));
     CK(cudaStreamSynchronize(c->stream));
     relres_true = h[4];
     ++cycles;
@@ -870,7 +870,7 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
   if (cnpint_status st = pinv_dev(c, d_b, nullptr, V[0], 0)) return st;
   c->post = post_cycle_start(c, 1);
   CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
-  CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(launch_scal_to_host(c));
   CK(cudaStreamSynchronize(c->stream));
   const double bnorm = std::sqrt(h[7]);
   if (h[7] == 0.0) {  // b = 0 ⇒ u = 0
@@ -898,7 +898,7 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
       if (j + 1 <= CNP_MAX_DOT) c->post = post_finalize(c, j);
       if (cnpint_status cs = cgs2(c, V.data(), j + 1, w, false)) return cs;
       if (j + 1 > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
-      CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CK(launch_scal_to_host(c));
       CK(cudaStreamSynchronize(c->stream));
       ++its;
       jdone = j + 1;
@@ -927,7 +927,7 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
     if (cnpint_status st = pinv_dev(c, tmp, nullptr, V[0], 0)) return st;
     c->post = post_cycle_start(c, 0);
     CK(launch_norm2(c, V[0], c->d_part, c->d_scal + 2));
-    CK(cudaMemcpyAsync(h, c->d_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(launch_scal_to_host(c));
     CK(cudaStreamSynchronize(c->stream));
     relres_prec = h[4];
     relres_true = std::sqrt(h[6]) / bnorm;

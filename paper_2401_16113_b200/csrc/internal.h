@@ -110,7 +110,8 @@ struct cnpint_ctx {
   double* d_scal;      // [8] misc scalars: 0 = ||b||, 1 = est, 2 = beta^2, 3 = nonfinite flag
   int* d_status;       // device status word (bit 0: singular pivot)
   unsigned* d_counter; // grid_fold ticket counter (zero between launches)
-  double* h_pinned;    // pinned host scalars [8]
+  double* h_pinned;    // mapped pinned host scalars [16]: d_scal[0..7], status at [8]
+  double* d_hmap;      // its device alias
   PostOp post;         // pending post-fold operation for the next reducing launch (op 0 = none)
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
@@ -174,6 +175,7 @@ cudaError_t launch_cgs2_pass(cnpint_ctx* c, double* const* V, int nv, const doub
 cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,
                           double* w, double* wout, int want_dots, int want_norm, double* part, double* out);
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg);
+cudaError_t launch_scal_to_host(cnpint_ctx* c);
 
 // profiler hooks (cnpint.cu); no-ops unless cnpint_profile_enable(ctx, 1)
 void cnp_prof_begin(cnpint_ctx* c, int kid);

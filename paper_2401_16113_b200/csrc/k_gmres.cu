@@ -335,6 +335,20 @@ cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double
   return cudaGetLastError();
 }
 
+// GMRES scalars d_scal[0..7] and the status word → the handle's mapped pinned host buffer, written by
+// the SM over PCIe instead of a copy-engine transfer: with several handles solving at once (bench.py
+// e2e), an 8-byte cudaMemcpyAsync waits behind the other handles' 134-MB vector copies on the shared
+// copy engine (measured: 2.4 ms per wait at c2), this write does not.
+__global__ void k_to_host(const double* __restrict__ scal, const int* __restrict__ status, volatile double* h) {
+  const int i = threadIdx.x;
+  if (i < 8) h[i] = scal[i];
+  if (i == 8) h[8] = (double)*status;
+}
+cudaError_t launch_scal_to_host(cnpint_ctx* c) {
+  k_to_host<<<1, 32, 0, c->stream>>>(c->d_scal, c->d_status, c->d_hmap);
+  return cudaGetLastError();
+}
+
 // op 0: cycle_start(first = arg); op 1: arnoldi_finalize(j); op 2: backsolve(k = j)
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg) {
   const int ldh = c->restart_max + 1;
