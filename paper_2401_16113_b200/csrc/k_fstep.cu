@@ -47,6 +47,13 @@
 #define FS_MINB7 2
 #endif
 
+// timing-experiment knob (CNPINT_FS_SKIP): compiled out of product builds
+#ifdef CNPINT_EXPERIMENTS
+#define FS_SKIP(b) (a.skip & (b))
+#else
+#define FS_SKIP(b) 0
+#endif
+
 namespace {
 
 CNP_DEV void fs_separate(double2 zk, double2 zm, double2& xa, double2& xb) {
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
       constexpr int TT = G::TT;
       const int t1b = idx * TT;
       const int mycol = col0 + 2 * col;
-      const int xin = mycol % a.ld;
+      const int xin = MODE == 2 ? mycol % a.ld : mycol;  // 1D: W = ld
       const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
       if (fwd_t1)
         for (int q = tid; q < TT * N2; q += NT) {  // ω_N^{t1 k2} for each t1 of the item
@@ -278,15 +285,21 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
             for (int n1 = 0; n1 < F2::R1; ++n1) {
               const int t = t1b + tt + N1 * (n2 + F2::R2 * n1);
-              v[tt][n1] = (colok && !(a.skip & 1)) ? ldg_cs2(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
+              v[tt][n1] = (colok && !FS_SKIP(1)) ? ldg_cs2(reinterpret_cast<const double2*>(a.vin + (int64_t)t * W + mycol))
                                                    : make_double2(0.0, 0.0);
             }
+          double gls[TT];
+#pragma unroll
+          for (int tt = 0; tt < TT; ++tt) gls[tt] = glo[(t1b + tt) & 63] * s;
 #pragma unroll
           for (int tt = 0; tt < TT; ++tt) {
 #pragma unroll
             for (int n1 = 0; n1 < F2::R1; ++n1) {
               const int t = t1b + tt + N1 * (n2 + F2::R2 * n1);
-              v[tt][n1] = cscale(v[tt][n1], ghi[t >> 6] * glo[t & 63] * s);
+              // g_t: for N1 ≥ 64, t & 63 = t1 & 63 and t >> 6 = (t1 >> 6) + (N1/64)(n2 + R2 n1)
+              const double g = N1 >= 64 ? ghi[((t1b + tt) >> 6) + (N1 >> 6) * (n2 + F2::R2 * n1)] * gls[tt]
+                                        : ghi[t >> 6] * glo[t & 63] * s;
+              v[tt][n1] = cscale(v[tt][n1], g);
             }
             rf_step1<F2, false>(v[tt], buf + (tt * NC + col) * F2::SC, tw2, n2);
           }
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
             for (int k2 = 0; k2 < F2::R2; ++k2) {
               const int kk = k1 + F2::R1 * k2;  // pass frequency k2' of the four-step
-              if (!(a.skip & 4))
+              if (!FS_SKIP(4))
                 Yb[((size_t)(t1b + tt) * N2 + kk) * NC + col] = cmul(u[tt][k2], twn[tt * N2 + kk]);
             }
         } else if (colok) {
@@ -330,7 +343,8 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
 #pragma unroll
             for (int k2 = 0; k2 < F2::R2; ++k2) {
               const int t = t1b + tt + N1 * (k1 + F2::R1 * k2);
-              const double g = ihi[t >> 6] * ilo[t & 63];
+              const double g = N1 >= 64 ? ihi[((t1b + tt) >> 6) + (N1 >> 6) * (k1 + F2::R1 * k2)] * ilo[(t1b + tt) & 63]
+                                        : ihi[t >> 6] * ilo[t & 63];
               double2 val = make_double2(padA ? 0.0 : u[tt][k2].x * g, padB ? 0.0 : u[tt][k2].y * g);
               double2* dst = reinterpret_cast<double2*>(a.vout + (int64_t)t * W + mycol);
               if (a.accumulate) {
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
       const bool active = m == 0 || two;
       const int gp = h * NF + p;
       const int mycol = col0 + 2 * gp;
-      const int xin = mycol % a.ld;
+      const int xin = MODE == 2 ? mycol % a.ld : mycol;  // 1D: W = ld
       const bool padA = xin >= a.nx, padB = xin + 1 >= a.nx, colok = mycol < W;
       double2* const fb = buf + col * F1::SC;
       // partner of frequency index ko of this column (Hermitian pairing k ↔ N − k)
@@ -371,7 +385,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
           double2 v[F1::R1];
 #pragma unroll
           for (int n1 = 0; n1 < F1::R1; ++n1)
-            v[n1] = (active && !(a.skip & 4)) ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp)
+            v[n1] = (active && !FS_SKIP(4)) ? __ldcg(Yb + ((size_t)(n2 + F1::R2 * n1) * N2 + km) * NC + gp)
                                               : make_double2(0.0, 0.0);
           rf_step1<F1, false>(v, fb, tw1, n2);
         }
@@ -415,7 +429,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
               if (padA) xa = make_double2(0.0, 0.0);
               if (padB) xbv = make_double2(0.0, 0.0);
               double2* o = a.spout + (int64_t)k * W + mycol;
-              if (!(a.skip & 2)) {
+              if (!FS_SKIP(2)) {
                 stg_cs2(o, xa);
                 stg_cs2(o + 1, xbv);
               }
