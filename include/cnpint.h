@@ -221,7 +221,9 @@ cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, v
  * generic merge tree instead of the tabulated fast tree; 8 = the one-column time FFT kernel
  * (N <= 16384); 16 = the cluster time FFT instead of the four-step kernel for 1D N >= 2048;
  * 32 = the shared-memory Stockham DST kernel for every 2D sine pass; 64 = the cluster kernel instead
- * of the register time pass for 2D N = 256, 512. */
+ * of the register time pass for 2D N = 256, 512; 128 = classic CGS2 in cnpint_gmres (a second
+ * reading pass c2 = Ṽᵀ(w − Ṽs²c1)) instead of the Gram form c2 = c1 − G̃s²c1, whose Gram row
+ * Ṽᵀ Ṽ_j is reduced inside the matvec (K7). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -74,7 +74,7 @@ bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 struct Layout {
   size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
-  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, scal, status;
+  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status;
   size_t total;
 };
 
@@ -146,15 +146,17 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
     L.H = take((size_t)(restart_max + 1) * restart_max * 8);
     L.cs = take(restart_max * 8); L.sn = take(restart_max * 8); L.g = take((restart_max + 2) * 8);
     L.y = take(restart_max * 8); L.coef = take((restart_max + 2) * 8);
+    L.G = take((size_t)(restart_max + 1) * (restart_max + 1) * 8); L.cg = take(2 * CNP_MAX_DOT * 8);
   }
-  // partial sums: dots/updates use CNP_RED_BLOCKS rows of (MAX_DOT+1); the residual matvec one per block
+  // partial sums: dots/updates use CNP_RED_BLOCKS rows of (MAX_DOT+1), the Gram matvec one row of
+  // 2·MAX_DOT per block, the residual matvec one per block
   {
     cnpint_ctx tmp;
     std::memset(&tmp, 0, sizeof(tmp));
     tmp.dim = op->dim; tmp.N = N; tmp.ld = ld; tmp.ny = ny;
     size_t mv = (size_t)matvec_partial_blocks(&tmp);
     size_t blocks = mv > CNP_RED_BLOCKS ? mv : CNP_RED_BLOCKS;
-    L.part = take(blocks * (CNP_MAX_DOT + 1) * 8);
+    L.part = take(blocks * (2 * CNP_MAX_DOT) * 8);
   }
   L.scal = take(16 * 8);
   L.status = take(64);
@@ -480,6 +482,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
     c->d_coef = (double*)(w + L.coef);
   }
   c->d_part = (double*)(w + L.part);
+  if (restart_max >= 1) { c->d_G = (double*)(w + L.G); c->d_cg = (double*)(w + L.cg); }
   c->d_scal = (double*)(w + L.scal);
   c->d_status = (int*)(w + L.status);
   c->d_counter = (unsigned*)(w + L.status + 32);
@@ -704,6 +707,12 @@ static PostOp post_cycle_start(const cnpint_ctx* c, int first) {
   p.op = 2; p.first = first; p.rmax = c->restart_max; p.scl = c->d_scl; p.g = c->d_g; p.scal = c->d_scal;
   return p;
 }
+static PostOp post_gram(const cnpint_ctx* c, int j) {
+  PostOp p{};
+  p.op = 3; p.j = j; p.ldh = c->restart_max + 1; p.cg = c->d_cg; p.G = c->d_G; p.c1w = c->d_c1; p.c2w = c->d_c2;
+  p.scl = c->d_scl;
+  return p;
+}
 static PostOp post_finalize(const cnpint_ctx* c, int j) {
   PostOp p{};
   p.op = 1; p.j = j; p.ldh = c->restart_max + 1; p.c1 = c->d_c1; p.c2 = c->d_c2; p.scl = c->d_scl; p.H = c->d_H;
@@ -784,15 +793,25 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       // w = 𝓜 z_j, written straight into the slot of Ṽ_{j+1}
       double* w = V[j + 1];
       const int nv = j + 1;
-      if (nv <= CNP_MAX_DOT) {
-        // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw)
-        CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
+      if (nv <= CNP_MAX_DOT && !(c->debug & 128)) {
+        // Gram CGS2: w = 𝓜 z_j with c1 = Ṽᵀw and the Gram row Ṽᵀ Ṽ_j in the same pass; the
+        // folding block forms c2 = Ṽᵀ(w − Ṽs²c1) = c1 − G̃ s² c1 from them (post op 3), then one
+        // update w −= Ṽs²(c1 + c2) with ‖w‖² — the same two projections, one reading pass fewer
+        c->post = post_gram(c, j);
+        CK(launch_matvec_dots_gram(c, Z[j], w, V.data(), nv));
+        c->post = post_finalize(c, j);  // run by the update's norm fold
+        CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_scal + 2, 1));
       } else {
-        CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
+        if (nv <= CNP_MAX_DOT) {
+          // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw); classic second pass (debug bit 128)
+          CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
+        } else {
+          CK(launch_matvec(c, Z[j], w, 0, nullptr, nullptr));
+        }
+        if (nv <= CNP_MAX_DOT) c->post = post_finalize(c, j);  // run by CGS2's last (norm) pass
+        if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
+        if (nv > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
       }
-      if (nv <= CNP_MAX_DOT) c->post = post_finalize(c, j);  // run by CGS2's last (norm) pass
-      if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
-      if (nv > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
       CK(launch_scal_to_host(c));
       CK(cudaStreamSynchronize(c->stream));
       ++its;

@@ -68,9 +68,10 @@ CNP_DEV void block_reduce_nv(double (&acc)[NV], double* part, int stride) {
 // depend on which block finishes last (bitwise reproducible).  Partials are read with ld.global.cg
 // (L2) since other blocks wrote them.  The counter is reset for the next launch.  Returns true in
 // the block that folded.
+template <int MAXC = 10>  // columns folded at most
 CNP_DEV bool grid_fold(const double* part, int nparts, int stride, int ncols, double* out, unsigned* counter) {
   __shared__ bool amlast;
-  __shared__ double red[32][10];
+  __shared__ double red[32][MAXC];
   const int tid = threadIdx.x + threadIdx.y * blockDim.x;
   __threadfence();
   __syncthreads();
@@ -81,17 +82,17 @@ CNP_DEV bool grid_fold(const double* part, int nparts, int stride, int ncols, do
   // every thread sums a fixed strided subset of the partials for all columns (independent L2 loads),
   // then warp trees and a fixed-order sum over warps
   const int nthr = blockDim.x * blockDim.y, lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
-  double acc[10];
+  double acc[MAXC];
 #pragma unroll
-  for (int col = 0; col < 10; ++col) acc[col] = 0.0;
+  for (int col = 0; col < MAXC; ++col) acc[col] = 0.0;
   for (int b = tid; b < nparts; b += nthr) {
     const double* pb = part + (size_t)b * stride;
 #pragma unroll
-    for (int col = 0; col < 10; ++col)
+    for (int col = 0; col < MAXC; ++col)
       if (col < ncols) acc[col] += __ldcg(pb + col);
   }
 #pragma unroll
-  for (int col = 0; col < 10; ++col) {
+  for (int col = 0; col < MAXC; ++col) {
     if (col < ncols) {
       double v = acc[col];
 #pragma unroll

@@ -42,12 +42,33 @@ CNP_DEV void arnoldi_finalize_dev(int j, int ldh, const double* c1, const double
   if (beta == 0.0) scal[5] = 1.0;  // happy breakdown
 }
 
+// Gram CGS2 step j (op 3).  cg[0..j] = c1 = Ṽᵀw, cg[j+1..2j+1] = Ṽᵢᵀ Ṽ_j (i ≤ j), folded by the
+// matvec.  Stores row/column j of the Gram matrix G̃ (the rows i < j were stored at steps i of this
+// cycle) and forms the second projection without a pass over the vectors:
+//   c2 = Ṽᵀ(w − Ṽ S² c1) = c1 − G̃ S² c1,   S = diag(s_i), v_i = s_i Ṽ_i,
+// the coefficients classic CGS2's second pass reads back (north_star (5); the algebra is exact,
+// rounding differs by O(ε‖c1‖), the size of the classic pass's own rounding).
+CNP_DEV void gram_c2_dev(int j, int ldh, const double* cg, double* G, const double* scl, double* c1, double* c2) {
+  for (int i = 0; i <= j; ++i) {
+    const double gij = cg[j + 1 + i];
+    G[(size_t)j * ldh + i] = gij;
+    G[(size_t)i * ldh + j] = gij;
+    c1[i] = cg[i];
+  }
+  for (int i = 0; i <= j; ++i) {
+    double acc = c1[i];
+    for (int k = 0; k <= j; ++k) acc -= G[(size_t)i * ldh + k] * (scl[k] * scl[k] * c1[k]);
+    c2[i] = acc;
+  }
+}
+
 // Called by the whole last block after grid_fold returned true (its thread 0 wrote scal[2]).
 CNP_DEV void run_post(const PostOp& p) {
   if (p.op == 0) return;
-  __threadfence_block();
+  __syncthreads();  // the fold's outputs (written by threads < ncols) are visible to thread 0
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     if (p.op == 1) arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
+    else if (p.op == 3) gram_c2_dev(p.j, p.ldh, p.cg, p.G, p.scl, p.c1w, p.c2w);
     else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax);
   }
 }
