@@ -146,17 +146,16 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
     L.H = take((size_t)(restart_max + 1) * restart_max * 8);
     L.cs = take(restart_max * 8); L.sn = take(restart_max * 8); L.g = take((restart_max + 2) * 8);
     L.y = take(restart_max * 8); L.coef = take((restart_max + 2) * 8);
-    L.G = take((size_t)(restart_max + 1) * (restart_max + 1) * 8); L.cg = take(2 * CNP_MAX_DOT * 8);
+    L.G = take((size_t)(restart_max + 1) * (restart_max + 1) * 8); L.cg = take((CNP_MAX_DOT + 1) * 8);
   }
-  // partial sums: dots/updates use CNP_RED_BLOCKS rows of (MAX_DOT+1), the Gram matvec one row of
-  // 2·MAX_DOT per block, the residual matvec one per block
+  // partial sums: dots/updates use CNP_RED_BLOCKS rows of (MAX_DOT+1), the matvec one row per block
   {
     cnpint_ctx tmp;
     std::memset(&tmp, 0, sizeof(tmp));
     tmp.dim = op->dim; tmp.N = N; tmp.ld = ld; tmp.ny = ny;
     size_t mv = (size_t)matvec_partial_blocks(&tmp);
     size_t blocks = mv > CNP_RED_BLOCKS ? mv : CNP_RED_BLOCKS;
-    L.part = take(blocks * (2 * CNP_MAX_DOT) * 8);
+    L.part = take(blocks * (CNP_MAX_DOT + 1) * 8);
   }
   L.scal = take(16 * 8);
   L.status = take(64);
@@ -705,18 +704,23 @@ static cnpint_status gmres_args(cnpint_ctx* c, const double* d_b, double* d_u, d
 static PostOp post_cycle_start(const cnpint_ctx* c, int first) {
   PostOp p{};
   p.op = 2; p.first = first; p.rmax = c->restart_max; p.scl = c->d_scl; p.g = c->d_g; p.scal = c->d_scal;
+  p.G = c->d_G;  // G̃_00 for Gram CGS2 (null without a GMRES workspace)
   return p;
 }
-static PostOp post_gram(const cnpint_ctx* c, int j) {
+static PostOp post_gram_c2(const cnpint_ctx* c, int j) {
   PostOp p{};
-  p.op = 3; p.j = j; p.ldh = c->restart_max + 1; p.cg = c->d_cg; p.G = c->d_G; p.c1w = c->d_c1; p.c2w = c->d_c2;
-  p.scl = c->d_scl;
+  p.op = 3; p.j = j; p.ldh = c->restart_max + 1; p.G = c->d_G; p.c1 = c->d_c1; p.c2w = c->d_c2; p.scl = c->d_scl;
   return p;
 }
 static PostOp post_finalize(const cnpint_ctx* c, int j) {
   PostOp p{};
   p.op = 1; p.j = j; p.ldh = c->restart_max + 1; p.c1 = c->d_c1; p.c2 = c->d_c2; p.scl = c->d_scl; p.H = c->d_H;
   p.cs = c->d_cs; p.sn = c->d_sn; p.g = c->d_g; p.scal = c->d_scal;
+  return p;
+}
+static PostOp post_gram_finalize(const cnpint_ctx* c, int j) {
+  PostOp p = post_finalize(c, j);
+  p.op = 4; p.cg = c->d_cg; p.G = c->d_G;
   return p;
 }
 
@@ -794,13 +798,14 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       double* w = V[j + 1];
       const int nv = j + 1;
       if (nv <= CNP_MAX_DOT && !(c->debug & 128)) {
-        // Gram CGS2: w = 𝓜 z_j with c1 = Ṽᵀw and the Gram row Ṽᵀ Ṽ_j in the same pass; the
-        // folding block forms c2 = Ṽᵀ(w − Ṽs²c1) = c1 − G̃ s² c1 from them (post op 3), then one
-        // update w −= Ṽs²(c1 + c2) with ‖w‖² — the same two projections, one reading pass fewer
-        c->post = post_gram(c, j);
-        CK(launch_matvec_dots_gram(c, Z[j], w, V.data(), nv));
-        c->post = post_finalize(c, j);  // run by the update's norm fold
-        CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_scal + 2, 1));
+        // Gram CGS2: w = 𝓜 z_j with c1 = Ṽᵀw; the folding block forms c2 = Ṽᵀ(w − Ṽs²c1) =
+        // c1 − G̃s²c1 from the stored Gram matrix (post op 3); one update w −= Ṽs²(c1 + c2) that also
+        // reduces ‖w‖² and the Gram row Ṽᵀw of the new vector (post op 4 stores it, then the
+        // Arnoldi finalize) — the same two projections as classic CGS2, one reading pass fewer
+        c->post = post_gram_c2(c, j);
+        CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
+        c->post = post_gram_finalize(c, j);
+        CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));
       } else {
         if (nv <= CNP_MAX_DOT) {
           // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw); classic second pass (debug bit 128)

@@ -46,10 +46,10 @@ struct PostOp {
   double* sn;
   double* g;
   double* scal;
-  // op 3 (Gram reorthogonalisation): cg = folded [Ṽᵀw (j+1), Ṽᵀ Ṽ_j (j+1)] → G row/column j, c1w, c2w
+  // Gram CGS2 (post_op.cuh): op 3 c2 = c1 − G̃S²c1 (into c2w); op 4 stores the Gram row j+1 from the
+  // update's fold cg = [‖Ṽ_{j+1}‖², Ṽᵢᵀ Ṽ_{j+1}] and runs op 1; op 2 records G̃_00 when G is set
   const double* cg;
   double* G;
-  double* c1w;
   double* c2w;
 };
 
@@ -103,7 +103,7 @@ struct cnpint_ctx {
   double* d_V;         // [(restart_max+1)][vec]
   double* d_Z;         // [restart_max][vec] z_j = P_α⁻¹ v_j of the current restart cycle
   double* d_G;         // [(restart_max+1)²] Gram matrix Ṽᵢᵀ Ṽₖ of the cycle's basis (Gram CGS2)
-  double* d_cg;        // [2·CNP_MAX_DOT] folded dots of the Gram matvec
+  double* d_cg;        // [CNP_MAX_DOT+1] the Gram-CGS2 update's fold [‖w‖², Ṽᵀw]
   double* d_part;      // [CNP_RED_BLOCKS][CNP_MAX_DOT+1]
   double* d_c1;        // [restart_max+1] raw dots (pass 1)
   double* d_c2;        // [restart_max+1] raw dots (pass 2)
@@ -143,8 +143,6 @@ cudaError_t launch_fstep_fwd(cnpint_ctx* c, const double* v, const double* vscal
 cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
                                double* out);
-// w = 𝓜u with Ṽᵀw and the Gram row Ṽᵀ Ṽ_{nv−1} folded into c->d_cg; runs c->post (Gram step) after the fold
-cudaError_t launch_matvec_dots_gram(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv);
 // host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed
 cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
 

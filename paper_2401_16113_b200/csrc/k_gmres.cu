@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
 // coef_i = cd[i] (MODE 1, combine, w may be null), optionally fused partial dots with Ṽ (DOTS) or
 // Σ w_out² (NORM).  NOWRITE: w_out is only formed in registers (its dots are the product), nothing
 // is stored — CGS2's second projection c2 = Ṽᵀ(w − Ṽ s²c1) without writing the intermediate.
-template <int NV, int MODE, bool DOTS, bool NORM, bool NOWRITE = false>
+// GDOTS (with NORM): also Ṽᵢᵀ w_out — the Gram row of the new basis vector for Gram CGS2; the fold
+// writes out[0] = Σ w_out², out[1 + i] = Ṽᵢᵀ w_out.
+template <int NV, int MODE, bool DOTS, bool NORM, bool NOWRITE = false, bool GDOTS = false>
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const double* __restrict__ cd,
                                                              const double* __restrict__ scl, const double* w,
                                                              double* wout, size_t n2, double* __restrict__ part,
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
   double coef[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? (cd[i] + (cd2 ? cd2[i] : 0.0)) * scl[i] * scl[i] : cd[i];
-  constexpr int NA = DOTS ? NV : 1;
+  constexpr int NA = DOTS ? NV : GDOTS ? NV + 1 : 1;
   double acc[NA];
 #pragma unroll
   for (int i = 0; i < NA; ++i) acc[i] = 0.0;
@@ -106,13 +108,17 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
       for (int i = 0; i < NV; ++i) acc[i] = fma(v[i].x, x.x, fma(v[i].y, x.y, acc[i]));
     }
     if constexpr (NORM) acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
+    if constexpr (GDOTS) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[1 + i] = fma(v[i].x, x.x, fma(v[i].y, x.y, acc[1 + i]));
+    }
   }
   if constexpr (DOTS) {
     block_reduce_write<NV>(acc, part, stride);
     if (out) grid_fold(part, gridDim.x, stride, NV, out, counter);
   } else if constexpr (NORM) {
-    block_reduce_write<1>(acc, part, stride);
-    if (out && grid_fold(part, gridDim.x, stride, 1, out, counter)) run_post(post);
+    block_reduce_write<NA>(acc, part, stride);
+    if (out && grid_fold(part, gridDim.x, stride, NA, out, counter)) run_post(post);
   }
 }
 
@@ -275,10 +281,15 @@ static void upd_cgs(cnpint_ctx* c, const VPtrs& V, const double* c1, const doubl
   if (phase == 0)  // c2 = Ṽᵀ(w − Ṽ s² c1), nothing written
     k_update<NV, 0, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
         V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, nullptr);
-  else {  // w ← w − Ṽ s² (c1 + c2), ‖w‖², then the pending post-fold step (Arnoldi finalize)
+  else if (phase == 1) {  // w ← w − Ṽ s² (c1 + c2), ‖w‖², then the pending post-fold step (Arnoldi finalize)
     const PostOp post = c->post;
     c->post = PostOp{};
     k_update<NV, 0, false, true, false><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
+        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2, post);
+  } else {  // phase 2 (Gram CGS2): as phase 1, plus the Gram row Ṽᵢᵀ w of the new vector; out = [‖w‖², Ṽᵀw]
+    const PostOp post = c->post;
+    c->post = PostOp{};
+    k_update<NV, 0, false, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
         V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2, post);
   }
 }
@@ -301,7 +312,7 @@ cudaError_t launch_cgs2_pass(cnpint_ctx* c, double* const* Vp, int nv, const dou
     case 8: upd_cgs<8>(c, V, c1, c2, w, part, out, phase); break;
     default: return cudaErrorInvalidValue;
   }
-  cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (phase == 0 ? 1 : 2)));
+  cnp_prof_end(c, KID_UPDATE, 8.0 * cnp_units(c) * (nv + (phase == 0 ? 1 : 2)));  // phase 2: same bytes as 1
   return cudaGetLastError();
 }
 

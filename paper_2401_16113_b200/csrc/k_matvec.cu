@@ -78,7 +78,7 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
 // ------------------------------------------------------------------------------- K1 1D
 // MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  MODE 3: as 2 without storing y (norm
 // only).  NORM: per-block Σ y².
-template <int MODE, bool NORM, int NVD = 0, bool GRAM = false>
+template <int MODE, bool NORM, int NVD = 0>
 __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, const double* __restrict__ lo,
                                                   const double* __restrict__ di, const double* __restrict__ up,
@@ -86,10 +86,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   double* __restrict__ part, double* __restrict__ out,
                                                   unsigned* counter, DotPtrs vd = DotPtrs{},
                                                   const double* __restrict__ dt = nullptr, PostOp post = PostOp{}) {
-  constexpr int ND = NVD > 0 ? (GRAM ? 2 * NVD : NVD) : 1;  // GRAM: Ṽᵀy and the Gram row Ṽᵀ Ṽ_{NVD−1}
-  double dacc[ND];
+  double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
-  for (int i = 0; i < ND; ++i) dacc[i] = 0.0;
+  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
   const bool active = 2 * gx < ld;
@@ -168,25 +167,15 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
       if (NVD > 0 && active) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
 #pragma unroll
         for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
-        if constexpr (GRAM) {
-          const double2 vj = vvb[q][NVD > 0 ? NVD - 1 : 0];
-#pragma unroll
-          for (int i = 0; i < NVD; ++i)
-            dacc[NVD + i] = fma(vvb[q][i].x, vj.x, fma(vvb[q][i].y, vj.y, dacc[NVD + i]));
-        }
       }
       if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
       pv = cv; pl = cl; pr = cr;
     }
   }
   if (NORM) block_partial<128>(acc, part, out, counter, post);
-  if constexpr (NVD > 0 && GRAM) {
-    block_reduce_nv<2 * NVD>(dacc, part, 2 * CNP_MAX_DOT);
-    if (grid_fold<2 * CNP_MAX_DOT>(part, gridDim.x * gridDim.y * gridDim.z, 2 * CNP_MAX_DOT, 2 * NVD, out, counter))
-      run_post(post);
-  } else if constexpr (NVD > 0) {
+  if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+    if (grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter)) run_post(post);
   }
 }
 
@@ -194,7 +183,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
 // Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread walks a
 // chunk of t.  y-neighbours of s = u_t + u_{t-1} are exchanged through a double-buffered shared
 // row array; the edge warps also carry the halo rows y0-1 and y0+8.
-template <int MODE, bool NORM, int NVD = 0, bool GRAM = false>
+template <int MODE, bool NORM, int NVD = 0>
 __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
                                                   double htau, double alpha, double cxs, double cxu, double cys,
@@ -205,10 +194,9 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   // Warp wy of the block owns y row ybase + wy; its y−1 / y+1 neighbours are read straight from
   // global memory through L1 (the block's other warps load the same rows, so most of those reads
   // hit L1) — no shared-memory exchange and no barrier per time row.  x-neighbours by __shfl.
-  constexpr int ND = NVD > 0 ? (GRAM ? 2 * NVD : NVD) : 1;  // GRAM: Ṽᵀy and the Gram row Ṽᵀ Ṽ_{NVD−1}
-  double dacc[ND];
+  double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
-  for (int i = 0; i < ND; ++i) dacc[i] = 0.0;
+  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
   const int yrow = blockIdx.y * 8 + wy;
@@ -291,12 +279,6 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
         if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
 #pragma unroll
           for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
-          if constexpr (GRAM) {
-            const double2 vj = vvb[q][NVD - 1];
-#pragma unroll
-            for (int i = 0; i < NVD; ++i)
-              dacc[NVD + i] = fma(vvb[q][i].x, vj.x, fma(vvb[q][i].y, vj.y, dacc[NVD + i]));
-          }
         }
         if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
       }
@@ -304,13 +286,9 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
     }
   }
   if (NORM) block_partial<256>(acc, part, out, counter, post);
-  if constexpr (NVD > 0 && GRAM) {
-    block_reduce_nv<2 * NVD>(dacc, part, 2 * CNP_MAX_DOT);
-    if (grid_fold<2 * CNP_MAX_DOT>(part, gridDim.x * gridDim.y * gridDim.z, 2 * CNP_MAX_DOT, 2 * NVD, out, counter))
-      run_post(post);
-  } else if constexpr (NVD > 0) {
+  if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+    if (grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter)) run_post(post);
   }
 }
 
@@ -343,26 +321,28 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
   return cudaGetLastError();
 }
 
-template <int NVD, bool GRAM = false>
+template <int NVD>
 static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, const DotPtrs& vd, double* part,
-                                   double* out, const PostOp& post = PostOp{}) {
+                                   double* out) {
   const double htau = 0.5 * c->tau;
+  const PostOp post = c->post;  // pending step run by the folding block (Gram CGS2: c2 from c1 and G̃)
+  c->post = PostOp{};
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec1d<0, false, NVD, GRAM><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N,
-                                                                  c->ld, htau, c->alpha, tchunk, part, out,
-                                                                  c->d_counter, vd, c->d_dt, post);
+    k_matvec1d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N, c->ld,
+                                                            htau, c->alpha, tchunk, part, out, c->d_counter, vd,
+                                                            c->d_dt, post);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec2d<0, false, NVD, GRAM><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
-                                                                  c->alpha, c->xs, c->xu, c->ys, c->yu,
-                                                                  c->xd + c->yd + c->shift, tchunk, part, out,
-                                                                  c->d_counter, vd, c->d_dt, post);
+    k_matvec2d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
+                                                            c->alpha, c->xs, c->xu, c->ys, c->yu,
+                                                            c->xd + c->yd + c->shift, tchunk, part, out,
+                                                            c->d_counter, vd, c->d_dt, post);
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
   return cudaGetLastError();
@@ -381,26 +361,6 @@ cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double
     case 6: return run_matvec_dots<6>(c, u, y, vd, part, out);
     case 7: return run_matvec_dots<7>(c, u, y, vd, part, out);
     case 8: return run_matvec_dots<8>(c, u, y, vd, part, out);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-cudaError_t launch_matvec_dots_gram(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv) {
-  DotPtrs vd{};
-  for (int i = 0; i < nv && i < CNP_MAX_DOT; ++i) vd.p[i] = V[i];
-  const PostOp post = c->post;  // the Gram step, run by the folding block
-  c->post = PostOp{};
-  double* part = c->d_part;
-  double* out = c->d_cg;
-  switch (nv) {
-    case 1: return run_matvec_dots<1, true>(c, u, y, vd, part, out, post);
-    case 2: return run_matvec_dots<2, true>(c, u, y, vd, part, out, post);
-    case 3: return run_matvec_dots<3, true>(c, u, y, vd, part, out, post);
-    case 4: return run_matvec_dots<4, true>(c, u, y, vd, part, out, post);
-    case 5: return run_matvec_dots<5, true>(c, u, y, vd, part, out, post);
-    case 6: return run_matvec_dots<6, true>(c, u, y, vd, part, out, post);
-    case 7: return run_matvec_dots<7, true>(c, u, y, vd, part, out, post);
-    case 8: return run_matvec_dots<8, true>(c, u, y, vd, part, out, post);
     default: return cudaErrorInvalidValue;
   }
 }

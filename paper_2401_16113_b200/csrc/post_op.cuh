@@ -5,8 +5,9 @@
 #include "common.cuh"
 #include "internal.h"
 
-CNP_DEV void cycle_start_dev(double* scl, double* g, double* scal, int first, int rmax) {
+CNP_DEV void cycle_start_dev(double* scl, double* g, double* scal, int first, int rmax, double* G = nullptr) {
   const double beta = sqrt(scal[2]);
+  if (G) G[0] = scal[2];  // Gram CGS2: G̃_00 = ‖Ṽ_0‖²
   if (first) scal[0] = beta;
   scal[4] = beta / scal[0];
   scl[0] = beta > 0.0 ? 1.0 / beta : 0.0;
@@ -42,24 +43,29 @@ CNP_DEV void arnoldi_finalize_dev(int j, int ldh, const double* c1, const double
   if (beta == 0.0) scal[5] = 1.0;  // happy breakdown
 }
 
-// Gram CGS2 step j (op 3).  cg[0..j] = c1 = Ṽᵀw, cg[j+1..2j+1] = Ṽᵢᵀ Ṽ_j (i ≤ j), folded by the
-// matvec.  Stores row/column j of the Gram matrix G̃ (the rows i < j were stored at steps i of this
-// cycle) and forms the second projection without a pass over the vectors:
-//   c2 = Ṽᵀ(w − Ṽ S² c1) = c1 − G̃ S² c1,   S = diag(s_i), v_i = s_i Ṽ_i,
-// the coefficients classic CGS2's second pass reads back (north_star (5); the algebra is exact,
-// rounding differs by O(ε‖c1‖), the size of the classic pass's own rounding).
-CNP_DEV void gram_c2_dev(int j, int ldh, const double* cg, double* G, const double* scl, double* c1, double* c2) {
-  for (int i = 0; i <= j; ++i) {
-    const double gij = cg[j + 1 + i];
-    G[(size_t)j * ldh + i] = gij;
-    G[(size_t)i * ldh + j] = gij;
-    c1[i] = cg[i];
-  }
+// Gram CGS2 (north_star (5): classical Gram-Schmidt with reorthogonalisation).  G̃ = ṼᵀṼ of the
+// cycle's (unnormalised) basis, symmetric, stored at ldh; its row j+1 is reduced by the update that
+// writes Ṽ_{j+1} (op 4) and G̃_00 by the cycle start, so at step j every entry i, k ≤ j is known.
+//   op 3 (after the matvec folded c1 = Ṽᵀw):  c2 = Ṽᵀ(w − Ṽ S² c1) = c1 − G̃ S² c1,  S = diag(s_i)
+// — the coefficients classic CGS2's second pass reads back; the algebra is exact and the rounding
+// differs by O(ε‖c1‖), the size of the classic pass's own rounding.
+CNP_DEV void gram_c2_dev(int j, int ldh, const double* G, const double* scl, const double* c1, double* c2) {
   for (int i = 0; i <= j; ++i) {
     double acc = c1[i];
     for (int k = 0; k <= j; ++k) acc -= G[(size_t)i * ldh + k] * (scl[k] * scl[k] * c1[k]);
     c2[i] = acc;
   }
+}
+//   op 4 (after the update folded cg = [‖Ṽ_{j+1}‖², Ṽ_iᵀṼ_{j+1} (i ≤ j)]): store row/column j+1 of G̃,
+//   scal[2] = ‖Ṽ_{j+1}‖², then the Arnoldi finalize of column j (op 1).
+CNP_DEV void gram_store_dev(int j, int ldh, const double* cg, double* G, double* scal) {
+  const int r = j + 1;
+  for (int i = 0; i <= j; ++i) {
+    G[(size_t)r * ldh + i] = cg[1 + i];
+    G[(size_t)i * ldh + r] = cg[1 + i];
+  }
+  G[(size_t)r * ldh + r] = cg[0];
+  scal[2] = cg[0];
 }
 
 // Called by the whole last block after grid_fold returned true (its thread 0 wrote scal[2]).
@@ -68,7 +74,11 @@ CNP_DEV void run_post(const PostOp& p) {
   __syncthreads();  // the fold's outputs (written by threads < ncols) are visible to thread 0
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     if (p.op == 1) arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
-    else if (p.op == 3) gram_c2_dev(p.j, p.ldh, p.cg, p.G, p.scl, p.c1w, p.c2w);
-    else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax);
+    else if (p.op == 3) gram_c2_dev(p.j, p.ldh, p.G, p.scl, p.c1, p.c2w);
+    else if (p.op == 4) {
+      if (p.j + 1 < p.ldh) gram_store_dev(p.j, p.ldh, p.cg, p.G, p.scal);
+      else p.scal[2] = p.cg[0];
+      arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
+    } else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax, p.G);
   }
 }
