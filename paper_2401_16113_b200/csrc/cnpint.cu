@@ -705,6 +705,7 @@ static PostOp post_cycle_start(const cnpint_ctx* c, int first) {
   PostOp p{};
   p.op = 2; p.first = first; p.rmax = c->restart_max; p.scl = c->d_scl; p.g = c->d_g; p.scal = c->d_scal;
   p.G = c->d_G;  // G̃_00 for Gram CGS2 (null without a GMRES workspace)
+  p.hmap = c->d_hmap; p.status = c->d_status;
   return p;
 }
 static PostOp post_gram_c2(const cnpint_ctx* c, int j) {
@@ -716,6 +717,7 @@ static PostOp post_finalize(const cnpint_ctx* c, int j) {
   PostOp p{};
   p.op = 1; p.j = j; p.ldh = c->restart_max + 1; p.c1 = c->d_c1; p.c2 = c->d_c2; p.scl = c->d_scl; p.H = c->d_H;
   p.cs = c->d_cs; p.sn = c->d_sn; p.g = c->d_g; p.scal = c->d_scal;
+  p.hmap = c->d_hmap; p.status = c->d_status;
   return p;
 }
 static PostOp post_gram_finalize(const cnpint_ctx* c, int j) {
@@ -775,8 +777,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   double* b_nc = const_cast<double*>(d_b);
   V[0] = b_nc;
   c->post = post_cycle_start(c, 1);  // run by launch_norm2's folding block
-  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));
-  CK(launch_scal_to_host(c));
+  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));  // its post op also fills the mapped scalars
   CK(cudaStreamSynchronize(c->stream));
   if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
     CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
@@ -817,7 +818,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
         if (cnpint_status cs = cgs2(c, V.data(), nv, w, nv <= CNP_MAX_DOT)) return cs;
         if (nv > CNP_MAX_DOT) CK(launch_small(c, 1, j, 0));
       }
-      CK(launch_scal_to_host(c));
+      if (nv > CNP_MAX_DOT) CK(launch_scal_to_host(c));  // else the finalize post op wrote them
       CK(cudaStreamSynchronize(c->stream));
       ++its;
       jdone = j + 1;
@@ -845,8 +846,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
     V[0] = c->d_V;
     const bool likely_done = est <= tol;
     c->post = post_cycle_start(c, 0);  // run by the residual matvec's folding block
-    CK(launch_matvec(c, d_u, V[0], likely_done ? 3 : 2, d_b, c->d_part, c->d_scal + 2));
-    CK(launch_scal_to_host(c));
+    CK(launch_matvec(c, d_u, V[0], likely_done ? 3 : 2, d_b, c->d_part, c->d_scal + 2));  // post op writes h
     CK(cudaStreamSynchronize(c->stream));
     relres_true = h[4];
     ++cycles;

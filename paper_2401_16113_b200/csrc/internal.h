@@ -51,6 +51,10 @@ struct PostOp {
   const double* cg;
   double* G;
   double* c2w;
+  // when set: after the step, scal[0..7] and the status word go to the handle's mapped host buffer
+  // (what k_to_host does), so the host's per-step read needs no extra launch
+  volatile double* hmap;
+  const int* status;
 };
 
 struct cnpint_ctx {

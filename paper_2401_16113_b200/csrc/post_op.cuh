@@ -80,5 +80,9 @@ CNP_DEV void run_post(const PostOp& p) {
       else p.scal[2] = p.cg[0];
       arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
     } else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax, p.G);
+    if (p.hmap && p.op != 3) {
+      for (int i = 0; i < 8; ++i) p.hmap[i] = p.scal[i];
+      p.hmap[8] = (double)*p.status;
+    }
   }
 }
