@@ -708,11 +708,6 @@ static PostOp post_cycle_start(const cnpint_ctx* c, int first) {
   p.hmap = c->d_hmap; p.status = c->d_status;
   return p;
 }
-static PostOp post_gram_c2(const cnpint_ctx* c, int j) {
-  PostOp p{};
-  p.op = 3; p.j = j; p.ldh = c->restart_max + 1; p.G = c->d_G; p.c1 = c->d_c1; p.c2w = c->d_c2; p.scl = c->d_scl;
-  return p;
-}
 static PostOp post_finalize(const cnpint_ctx* c, int j) {
   PostOp p{};
   p.op = 1; p.j = j; p.ldh = c->restart_max + 1; p.c1 = c->d_c1; p.c2 = c->d_c2; p.scl = c->d_scl; p.H = c->d_H;
@@ -722,7 +717,7 @@ static PostOp post_finalize(const cnpint_ctx* c, int j) {
 }
 static PostOp post_gram_finalize(const cnpint_ctx* c, int j) {
   PostOp p = post_finalize(c, j);
-  p.op = 4; p.cg = c->d_cg; p.G = c->d_G;
+  p.op = 4; p.cg = c->d_cg; p.G = c->d_G; p.c2w = c->d_c2;
   return p;
 }
 
@@ -799,11 +794,10 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       double* w = V[j + 1];
       const int nv = j + 1;
       if (nv <= CNP_MAX_DOT && !(c->debug & 128)) {
-        // Gram CGS2: w = 𝓜 z_j with c1 = Ṽᵀw; the folding block forms c2 = Ṽᵀ(w − Ṽs²c1) =
-        // c1 − G̃s²c1 from the stored Gram matrix (post op 3); one update w −= Ṽs²(c1 + c2) that also
-        // reduces ‖w‖² and the Gram row Ṽᵀw of the new vector (post op 4 stores it, then the
-        // Arnoldi finalize) — the same two projections as classic CGS2, one reading pass fewer
-        c->post = post_gram_c2(c, j);
+        // Gram CGS2: w = 𝓜 z_j with c1 = Ṽᵀw; one update w −= Ṽs²(c1 + c2) whose blocks form
+        // c2 = Ṽᵀ(w − Ṽs²c1) = c1 − G̃s²c1 from the stored Gram matrix and which also reduces ‖w‖²
+        // and the Gram row Ṽᵀw of the new vector (post op 4 stores it, then the Arnoldi finalize)
+        // — the same two projections as classic CGS2, one reading pass fewer
         CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
         c->post = post_gram_finalize(c, j);
         CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));

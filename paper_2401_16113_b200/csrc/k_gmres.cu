@@ -85,8 +85,20 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
                                                              const double* __restrict__ cd2 = nullptr,
                                                              PostOp post = PostOp{}) {
   double coef[NV];
+  if constexpr (GDOTS) {
+    // Gram CGS2: the second projection from the stored Gram matrix, c2 = c1 − G̃ S² c1 (every block
+    // forms the same NV² products; post_op.cuh gram_c2_dev), coefficient (c1 + c2) s²
 #pragma unroll
-  for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? (cd[i] + (cd2 ? cd2[i] : 0.0)) * scl[i] * scl[i] : cd[i];
+    for (int i = 0; i < NV; ++i) {
+      double c2 = cd[i];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) c2 -= post.G[(size_t)i * post.ldh + k] * (scl[k] * scl[k] * cd[k]);
+      coef[i] = (cd[i] + c2) * scl[i] * scl[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) coef[i] = MODE == 0 ? (cd[i] + (cd2 ? cd2[i] : 0.0)) * scl[i] * scl[i] : cd[i];
+  }
   constexpr int NA = DOTS ? NV : GDOTS ? NV + 1 : 1;
   double acc[NA];
 #pragma unroll

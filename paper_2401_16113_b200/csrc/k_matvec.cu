@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
   if (NORM) block_partial<128>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    if (grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter)) run_post(post);
+    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
   }
 }
 
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   if (NORM) block_partial<256>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
     block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    if (grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter)) run_post(post);
+    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
   }
 }
 
@@ -325,8 +325,6 @@ template <int NVD>
 static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, const DotPtrs& vd, double* part,
                                    double* out) {
   const double htau = 0.5 * c->tau;
-  const PostOp post = c->post;  // pending step run by the folding block (Gram CGS2: c2 from c1 and G̃)
-  c->post = PostOp{};
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
     const int tchunk = c->N >= 4096 ? 32 : 16;
@@ -334,7 +332,7 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     k_matvec1d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N, c->ld,
                                                             htau, c->alpha, tchunk, part, out, c->d_counter, vd,
-                                                            c->d_dt, post);
+                                                            c->d_dt);
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
@@ -342,7 +340,7 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     k_matvec2d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
                                                             c->alpha, c->xs, c->xu, c->ys, c->yu,
                                                             c->xd + c->yd + c->shift, tchunk, part, out,
-                                                            c->d_counter, vd, c->d_dt, post);
+                                                            c->d_counter, vd, c->d_dt);
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
   return cudaGetLastError();

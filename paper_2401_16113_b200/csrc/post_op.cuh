@@ -46,7 +46,8 @@ CNP_DEV void arnoldi_finalize_dev(int j, int ldh, const double* c1, const double
 // Gram CGS2 (north_star (5): classical Gram-Schmidt with reorthogonalisation).  G̃ = ṼᵀṼ of the
 // cycle's (unnormalised) basis, symmetric, stored at ldh; its row j+1 is reduced by the update that
 // writes Ṽ_{j+1} (op 4) and G̃_00 by the cycle start, so at step j every entry i, k ≤ j is known.
-//   op 3 (after the matvec folded c1 = Ṽᵀw):  c2 = Ṽᵀ(w − Ṽ S² c1) = c1 − G̃ S² c1,  S = diag(s_i)
+//   c2 = Ṽᵀ(w − Ṽ S² c1) = c1 − G̃ S² c1,  S = diag(s_i)  (formed by the update kernel's blocks and
+//   again by its folding block for the H column, op 4)
 // — the coefficients classic CGS2's second pass reads back; the algebra is exact and the rounding
 // differs by O(ε‖c1‖), the size of the classic pass's own rounding.
 CNP_DEV void gram_c2_dev(int j, int ldh, const double* G, const double* scl, const double* c1, double* c2) {
@@ -56,8 +57,8 @@ CNP_DEV void gram_c2_dev(int j, int ldh, const double* G, const double* scl, con
     c2[i] = acc;
   }
 }
-//   op 4 (after the update folded cg = [‖Ṽ_{j+1}‖², Ṽ_iᵀṼ_{j+1} (i ≤ j)]): store row/column j+1 of G̃,
-//   scal[2] = ‖Ṽ_{j+1}‖², then the Arnoldi finalize of column j (op 1).
+//   op 4 (after the update folded cg = [‖Ṽ_{j+1}‖², Ṽ_iᵀṼ_{j+1} (i ≤ j)]): c2 as above, store row/column
+//   j+1 of G̃, scal[2] = ‖Ṽ_{j+1}‖², then the Arnoldi finalize of column j (op 1).
 CNP_DEV void gram_store_dev(int j, int ldh, const double* cg, double* G, double* scal) {
   const int r = j + 1;
   for (int i = 0; i <= j; ++i) {
@@ -76,6 +77,7 @@ CNP_DEV void run_post(const PostOp& p) {
     if (p.op == 1) arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
     else if (p.op == 3) gram_c2_dev(p.j, p.ldh, p.G, p.scl, p.c1, p.c2w);
     else if (p.op == 4) {
+      gram_c2_dev(p.j, p.ldh, p.G, p.scl, p.c1, p.c2w);  // the c2 the update used, for the H column
       if (p.j + 1 < p.ldh) gram_store_dev(p.j, p.ldh, p.cg, p.G, p.scal);
       else p.scal[2] = p.cg[0];
       arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);

@@ -14,5 +14,6 @@ bash scripts/gpu_ncu_env.sh c3 "k_tridiag" full_c3_k3 X=1
 bash scripts/gpu_ncu_op.sh c2 "k_update" full_c2_k7 gmres 3
 bash scripts/gpu_ncu_env.sh c3 "k_fstep" full_c3_k2 X=1
 bash scripts/gpu_ncu_op.sh c2 "k_matvec1d" full_c2_k1 A 0
+bash scripts/gpu_ncu_op.sh c2 "k_matvec1d" full_c2_k1g gmres 1
 bash scripts/gpu_ncu_env.sh c4 "k_dst_r" full_c4_k5y X=1
 echo done
