@@ -26,6 +26,19 @@ CNP_DEV double2 crecip(double2 a) {
   double d = 1.0 / fma(a.x, a.x, a.y * a.y);
   return make_double2(a.x * d, -a.y * d);
 }
+// 1/a with a Newton-refined hardware reciprocal of |a|² (two steps: within an ulp of the IEEE
+// quotient, no slow-path branch); zero or non-finite |a|² gives NaN (caught by cfinite).  Used on the
+// critical path of K3's variable-row sweeps and merges.
+CNP_DEV double2 crecip_nr(double2 a) {
+  const double d = fma(a.x, a.x, a.y * a.y);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  return make_double2(a.x * r, -a.y * r);
+}
 // multiply by -i (forward) or +i (inverse)
 template <bool INV>
 CNP_DEV double2 cmul_mi(double2 a) {

@@ -60,7 +60,7 @@ CNP_DEV Seg shfl_seg(const Seg& s, int d) {
 // are written to cf[0..5].  Returns false on a zero / non-finite 2x2 determinant.
 CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf) {
   const double2 det = csub(cmul(A.gb, B.fb), cmul(A.gc, B.fa));
-  const double2 id = crecip(det);
+  const double2 id = crecip_nr(det);
   const double2 P0 = cmul(csub(cmul(B.fb, A.gd), cmul(A.gc, B.fd)), id);
   const double2 P1 = cneg(cmul(cmul(B.fb, A.ga), id));
   const double2 P2 = cmul(cmul(A.gc, B.fc), id);
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           const double a = -tau * lo[i], c = -tau * up[i];
           const double2 bb = make_double2(skk.x - tau * di[i], skk.y);
           const double2 piv = (j == 1) ? bb : crfms(bb, a, gam);
-          const double2 inv = crecip(piv);
+          const double2 inv = crecip_nr(piv);
           ok &= cfinite(inv);
           alp = (j == 1) ? cscale(inv, a) : cscale(cmul(alp, inv), -a);
           gam = cscale(inv, c);
