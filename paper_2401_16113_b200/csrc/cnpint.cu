@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <algorithm>
 #include <complex>
 #include <cmath>
@@ -442,6 +443,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   cnpint_ctx* c = new (std::nothrow) cnpint_ctx;
   if (!c) return CNPINT_EINVAL;
   std::memset(c, 0, sizeof(*c));
+  { const char* e = getenv("CNPINT_PDL"); c->pdl = (e && atoi(e) == 0) ? 0 : 1; }
   c->dim = op->dim; c->nx = op->nx; c->ny = op->dim == 2 ? op->ny : 1; c->N = N; c->H = N / 2;
   c->toeplitz = op->dim == 2 ? 1 : op->toeplitz;
   c->ld = ld_of(op->nx); c->slice = (int64_t)c->ny * c->ld; c->vec = (int64_t)N * c->slice;

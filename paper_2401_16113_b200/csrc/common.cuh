@@ -46,6 +46,16 @@ CNP_DEV double2 cmul_mi(double2 a) {
 }
 CNP_DEV bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute (cnp_launch) may become
+// resident while its predecessor drains; griddepcontrol.wait blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for a plain launch), launch_dependents lets the next
+// kernel's launch begin.  Every kernel calls this before its first access to data another kernel
+// wrote, so the memory semantics are those of plain stream order.
+CNP_DEV void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ reductions
 CNP_DEV double warp_sum(double v) {
 #pragma unroll

@@ -1,5 +1,6 @@
 // Internal (non-ABI) declarations shared by the cnpint host code and kernel launchers.
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
@@ -108,6 +109,7 @@ struct cnpint_ctx {
   double* d_Z;         // [restart_max][vec] z_j = P_α⁻¹ v_j of the current restart cycle
   double* d_G;         // [(restart_max+1)²] Gram matrix Ṽᵢᵀ Ṽₖ of the cycle's basis (Gram CGS2)
   double* d_cg;        // [CNP_MAX_DOT+1] the Gram-CGS2 update's fold [‖w‖², Ṽᵀw]
+  int pdl;              // launch the GMRES-loop kernels with programmatic dependent launch
   double* d_part;      // [CNP_RED_BLOCKS][CNP_MAX_DOT+1]
   double* d_c1;        // [restart_max+1] raw dots (pass 1)
   double* d_c2;        // [restart_max+1] raw dots (pass 2)
@@ -189,6 +191,23 @@ cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg);
 cudaError_t launch_scal_to_host(cnpint_ctx* c);
 
 // profiler hooks (cnpint.cu); no-ops unless cnpint_profile_enable(ctx, 1)
+// Kernel launch on the handle's stream with programmatic dependent launch when c->pdl (CNPINT_PDL=0
+// turns it off): the kernel must start with pdl_enter() before touching data of earlier kernels.
+template <typename... KArgs, typename... Args>
+static inline cudaError_t cnp_launch(const cnpint_ctx* c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 void cnp_prof_begin(cnpint_ctx* c, int kid);
 void cnp_prof_end(cnpint_ctx* c, int kid, double algo_bytes);
 static inline double cnp_units(const cnpint_ctx* c) { return (double)c->N * c->nx * c->ny; }

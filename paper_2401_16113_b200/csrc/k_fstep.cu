@@ -243,6 +243,9 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
   }
   if (MODE == 2)
     for (int q = tid; q <= H; q += NT) { l1s[q] = a.lam1[q]; l2s[q] = a.lam2[q]; }
+  // PDL: the tables above come from create-time constants; everything below may read what the previous
+  // kernel on the stream wrote (the basis scale, the input, the shared ticket counters)
+  pdl_enter();
   const double s = (MODE != 1 && a.vscale) ? *a.vscale : 1.0;
   if (tid == 0) s_tk[0] = atomicAdd(a.ticket, 1u) - a.tick_base;
 
@@ -612,7 +615,8 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   a.skip = 0;
 #endif
   a.cnt = c->d_fscnt; a.ticket = c->d_fscnt + S.nxb; a.tick_base = c->fs_tick; a.base = c->fs_cnt;
-  kern<<<grid, G::NT, G::bytes, c->stream>>>(a, S);
+  cudaError_t le = cnp_launch(c, kern, dim3(grid), dim3(G::NT), G::bytes, a, S);
+  if (le != cudaSuccess) return le;
   c->fs_cnt += (unsigned)(S.n[0] + S.n[1]);  // phases 0 and 1 count per block
   c->fs_tick += S.total + (unsigned)grid;    // every CTA also takes one ticket past the end
   return cudaGetLastError();

@@ -40,6 +40,7 @@ template <int NV>
 __global__ void __launch_bounds__(CNP_RED_THREADS) k_dots(VPtrs V, const double* __restrict__ w, size_t n2,
                                                            double* __restrict__ part, int stride,
                                                            double* __restrict__ out, unsigned* counter) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   double acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = 0.0;
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
                                                             double* __restrict__ part, int stride,
                                                             double* __restrict__ out, unsigned* counter,
                                                             PostOp post) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   double acc[1] = {0.0};
   const double2* w2 = reinterpret_cast<const double2*>(w);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
                                                              int stride, double* __restrict__ out, unsigned* counter,
                                                              const double* __restrict__ cd2 = nullptr,
                                                              PostOp post = PostOp{}) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   double coef[NV];
   if constexpr (GDOTS) {
     // Gram CGS2: the second projection from the stored Gram matrix, c2 = c1 − G̃ S² c1 (every block
@@ -179,8 +182,8 @@ static size_t n2_of(const cnpint_ctx* c) { return (size_t)c->vec / 2; }
 
 template <int NV>
 static void dots_nv(cnpint_ctx* c, const VPtrs& V, const double* w, double* part, double* out) {
-  k_dots<NV><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(V, w, n2_of(c), part, CNP_MAX_DOT + 1, out,
-                                                                c->d_counter);
+  cnp_launch(c, k_dots<NV>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, V, w, n2_of(c), part, CNP_MAX_DOT + 1,
+             out, c->d_counter);
 }
 
 cudaError_t launch_dots(cnpint_ctx* c, double* const* Vp, int nv, const double* w, double* part, double* out) {
@@ -206,8 +209,8 @@ cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* o
   cnp_prof_begin(c, KID_DOTS);
   const PostOp post = c->post;
   c->post = PostOp{};
-  k_norm2<<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
-                                                             post);
+  cnp_launch(c, k_norm2, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, w, n2_of(c), part, CNP_MAX_DOT + 1, out,
+             c->d_counter, post);
   cnp_prof_end(c, KID_DOTS, 8.0 * cnp_units(c));
   return cudaGetLastError();
 }
@@ -226,8 +229,9 @@ cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* 
 template <int NV, int MODE, bool DOTS, bool NORM>
 static void upd(cnpint_ctx* c, const VPtrs& V, const double* cd, const double* w, double* wout, double* part,
                 double* out) {
-  k_update<NV, MODE, DOTS, NORM><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
-      V, cd, c->d_scl, w, wout, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter);
+  cnp_launch(c, k_update<NV, MODE, DOTS, NORM>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, V, cd,
+             (const double*)c->d_scl, w, wout, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
+             (const double*)nullptr, PostOp{});
 }
 
 // Cycle end with the Hessenberg back-substitution folded in: every block solves y = H[0:NV,0:NV]⁻¹g
@@ -239,6 +243,7 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_combine_bs(VPtrs X, const d
                                                                  const double* __restrict__ g,
                                                                  const double* __restrict__ scl, int scaled,
                                                                  const double* u_in, double* u_out, size_t n2) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   __shared__ double cs_[NV];
   if (threadIdx.x == 0) {
     double y[NV];
@@ -277,7 +282,7 @@ cudaError_t launch_combine_backsolve(cnpint_ctx* c, double* const* Xp, int nv, i
   const int ldh = c->restart_max + 1;
   cnp_prof_begin(c, KID_UPDATE);
 #define CB_CASE(K) \
-  case K: k_combine_bs<K><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(X, c->d_H, ldh, c->d_g, c->d_scl, scaled, u_in, u_out, n2_of(c)); break;
+  case K: cnp_launch(c, k_combine_bs<K>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, X, (const double*)c->d_H, ldh, (const double*)c->d_g, (const double*)c->d_scl, scaled, u_in, u_out, n2_of(c)); break;
   switch (nv) {
     CB_CASE(1) CB_CASE(2) CB_CASE(3) CB_CASE(4) CB_CASE(5) CB_CASE(6) CB_CASE(7) CB_CASE(8)
     default: return cudaErrorInvalidValue;
@@ -291,18 +296,21 @@ template <int NV>
 static void upd_cgs(cnpint_ctx* c, const VPtrs& V, const double* c1, const double* c2, double* w, double* part,
                     double* out, int phase) {
   if (phase == 0)  // c2 = Ṽᵀ(w − Ṽ s² c1), nothing written
-    k_update<NV, 0, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
-        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, nullptr);
+    cnp_launch(c, k_update<NV, 0, true, false, true>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, V, c1,
+               (const double*)c->d_scl, (const double*)w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
+               (const double*)nullptr, PostOp{});
   else if (phase == 1) {  // w ← w − Ṽ s² (c1 + c2), ‖w‖², then the pending post-fold step (Arnoldi finalize)
     const PostOp post = c->post;
     c->post = PostOp{};
-    k_update<NV, 0, false, true, false><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
-        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2, post);
+    cnp_launch(c, k_update<NV, 0, false, true, false>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, V, c1,
+               (const double*)c->d_scl, (const double*)w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
+               c2, post);
   } else {  // phase 2 (Gram CGS2): as phase 1, plus the Gram row Ṽᵢᵀ w of the new vector; out = [‖w‖², Ṽᵀw]
     const PostOp post = c->post;
     c->post = PostOp{};
-    k_update<NV, 0, false, true, false, true><<<CNP_RED_BLOCKS, CNP_RED_THREADS, 0, c->stream>>>(
-        V, c1, c->d_scl, w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter, c2, post);
+    cnp_launch(c, k_update<NV, 0, false, true, false, true>, dim3(CNP_RED_BLOCKS), dim3(CNP_RED_THREADS), 0, V, c1,
+               (const double*)c->d_scl, (const double*)w, w, n2_of(c), part, CNP_MAX_DOT + 1, out, c->d_counter,
+               c2, post);
   }
 }
 
@@ -363,12 +371,13 @@ cudaError_t launch_update(cnpint_ctx* c, double* const* Vp, int nv, const double
 // e2e), an 8-byte cudaMemcpyAsync waits behind the other handles' 134-MB vector copies on the shared
 // copy engine (measured: 2.4 ms per wait at c2), this write does not.
 __global__ void k_to_host(const double* __restrict__ scal, const int* __restrict__ status, volatile double* h) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   const int i = threadIdx.x;
   if (i < 8) h[i] = scal[i];
   if (i == 8) h[8] = (double)*status;
 }
 cudaError_t launch_scal_to_host(cnpint_ctx* c) {
-  k_to_host<<<1, 32, 0, c->stream>>>(c->d_scal, c->d_status, c->d_hmap);
+  cnp_launch(c, k_to_host, dim3(1), dim3(32), 0, (const double*)c->d_scal, (const int*)c->d_status, c->d_hmap);
   return cudaGetLastError();
 }
 

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   double* __restrict__ part, double* __restrict__ out,
                                                   unsigned* counter, DotPtrs vd = DotPtrs{},
                                                   const double* __restrict__ dt = nullptr, PostOp post = PostOp{}) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   double dacc[NVD > 0 ? NVD : 1];
 #pragma unroll
   for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
                                                   double* __restrict__ out, unsigned* counter,
                                                   DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr,
                                                   PostOp post = PostOp{}) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   // Warp wy of the block owns y row ybase + wy; its y−1 / y+1 neighbours are read straight from
   // global memory through L1 (the block's other warps load the same rows, so most of those reads
   // hit L1) — no shared-memory exchange and no barrier per time row.  x-neighbours by __shfl.
@@ -306,16 +308,17 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec1d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau,
-                                                         c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt,
-                                                         post);
+    const cudaError_t e = cnp_launch(c, k_matvec1d<MODE, NORM>, grid, block, 0, u, y, b, c->d_lo, c->d_di, c->d_up,
+                                     c->N, c->ld, htau, c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt, post);
+    if (e != cudaSuccess) return e;
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec2d<MODE, NORM><<<grid, block, 0, c->stream>>>(u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
-                                                         c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
-                                                         part, out, c->d_counter, DotPtrs{}, dt, post);
+    const cudaError_t e = cnp_launch(c, k_matvec2d<MODE, NORM>, grid, block, 0, u, y, b, c->N, c->nx, c->ny, c->ld,
+                                     htau, c->alpha, c->xs, c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
+                                     part, out, c->d_counter, DotPtrs{}, dt, post);
+    if (e != cudaSuccess) return e;
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
   return cudaGetLastError();
@@ -330,17 +333,19 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     const int tchunk = c->N >= 4096 ? 32 : 16;
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec1d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->d_lo, c->d_di, c->d_up, c->N, c->ld,
-                                                            htau, c->alpha, tchunk, part, out, c->d_counter, vd,
-                                                            c->d_dt);
+    const cudaError_t e = cnp_launch(c, k_matvec1d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr,
+                                     c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau, c->alpha, tchunk, part, out,
+                                     c->d_counter, vd, c->d_dt, PostOp{});
+    if (e != cudaSuccess) return e;
   } else {
     const int tchunk = 16;
     dim3 block(32, 8);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    k_matvec2d<0, false, NVD><<<grid, block, 0, c->stream>>>(u, y, nullptr, c->N, c->nx, c->ny, c->ld, htau,
-                                                            c->alpha, c->xs, c->xu, c->ys, c->yu,
-                                                            c->xd + c->yd + c->shift, tchunk, part, out,
-                                                            c->d_counter, vd, c->d_dt);
+    const cudaError_t e = cnp_launch(c, k_matvec2d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr,
+                                     c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs, c->xu, c->ys, c->yu,
+                                     c->xd + c->yd + c->shift, tchunk, part, out, c->d_counter, vd, c->d_dt,
+                                     PostOp{});
+    if (e != cudaSuccess) return e;
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
   return cudaGetLastError();

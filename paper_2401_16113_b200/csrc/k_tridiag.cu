@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(MAXT, 2)
               const double2* __restrict__ il2, const double2* __restrict__ tab, int m, int64_t W, int K, int G,
               int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status,
               const double2* __restrict__ lam1, int skip) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   constexpr bool TOEP = MODE != MODE_VAR;
   constexpr bool FAST = MODE == MODE_FAST;
   constexpr int NCF = FAST ? 2 : 6;  // stored coefficients per merge
@@ -418,6 +419,7 @@ __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __res
                                 const double* __restrict__ up, const double2* __restrict__ sk,
                                 const double2* __restrict__ il2, int m, int64_t W, double tau, int K,
                                 int* __restrict__ status, const double2* __restrict__ lam1) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   const double2 s = sk[k], il = il2[k];
@@ -527,10 +529,9 @@ static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what
   const int MP = tri_rows_alloc(c->nx, t.padsh);
   const size_t smem = (size_t)(t.NS * (MODE == MODE_VAR ? 3 * MP : MP + t.tabstride) + nw * 31 * ncf +
                                t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
-  k_tridiag<MODE, L, MAXT><<<grid, 32 * t.G * t.NS, smem, c->stream>>>(
-      what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS,
-      t.padsh, t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1, tri_skip());
-  return cudaGetLastError();
+  return cnp_launch(c, k_tridiag<MODE, L, MAXT>, dim3(grid), dim3(32 * t.G * t.NS), smem, what, zhat, c->d_lo,
+                    c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS, t.padsh,
+                    t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1, tri_skip());
 }
 
 template <int MODE, int L>
