@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256, DST_MINB)
     k_dst(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
           const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
           int nx) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   using LY = DstLayout<LOGE, NC>;
   constexpr int NT = 256;
   constexpr int M = LY::M;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(DstPlan<LOGE>::NT, LOGE <= 9 ? 2 : 1)
     k_dst_r(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
             const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
             int nx) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   using P = DstPlan<LOGE>;
   constexpr int E = P::E, M0 = P::M0, n = M0 - 1;
   constexpr int R1 = P::R1, R2 = P::R2, R3 = P::R3, M = P::M, NC = P::NC, TP = P::TP;
@@ -329,7 +331,7 @@ static cudaError_t run_dst_r(cnpint_ctx* c, const double* in, double* out, const
   const int ld = (int)c->ld;
   const int ntiles = YPASS ? c->N * ((ld / 2 + P::NC - 1) / P::NC) : ((nlines + 1) / 2 + P::NC - 1) / P::NC;
   const int grid = ntiles < grid_max ? ntiles : grid_max;
-  kern<<<grid, P::NT, P::bytes, c->stream>>>(in, out, c->N, c->ny, c->ld, pre, post, accumulate, c->debug & 1, c->nx);
+  cnp_launch(c, kern, dim3(grid), dim3(P::NT), P::bytes, in, out, c->N, c->ny, c->ld, pre, post, accumulate, c->debug & 1, c->nx);
   return cudaGetLastError();
 }
 
@@ -354,8 +356,8 @@ static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const
   const int ld = (int)c->ld;
   const int ntiles = YPASS ? c->N * ((ld / 2 + NC - 1) / NC) : ((nlines + 1) / 2 + NC - 1) / NC;
   const int grid = ntiles < grid_max ? ntiles : grid_max;
-  kern<<<grid, 256, LY::bytes, c->stream>>>(in, out, c->N, c->ny, c->ld, pre, post, accumulate, c->debug & 1,
-                                           c->nx);
+  cnp_launch(c, kern, dim3(grid), dim3(256), LY::bytes, in, out, c->N, c->ny, c->ld, pre, post, accumulate,
+             c->debug & 1, c->nx);
   return cudaGetLastError();
 }
 

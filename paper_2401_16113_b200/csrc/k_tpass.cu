@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(TpPlan<LOGN>::NT, TpPlan<LOGN>::MINB)
               int ld, int nx, const double* __restrict__ gam, const double* __restrict__ igam,
               const double2* __restrict__ lam1, const double2* __restrict__ lam2, const double* __restrict__ ex,
               const double* __restrict__ ey, double tau, double tau_shift, int debug_sign) {
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   using TP = TpPlan<LOGN>;
   using F = typename TP::F;
   using I = typename TP::I;
@@ -206,9 +207,9 @@ static cudaError_t run_tpass(cnpint_ctx* c, const double* in, double* out, const
   }
   const int ntiles = (int)((c->slice / 2 + TP::NC - 1) / TP::NC);
   const int grid = ntiles < grid_max ? ntiles : grid_max;
-  kern<<<grid, TP::NT, TP::bytes, c->stream>>>(in, out, vscale, c->slice, (int)c->ld, c->nx, c->d_gam, c->d_igam,
-                                              c->d_lam1, c->d_lam2, c->d_ex, c->d_ey, c->tau_p,
-                                              c->tau_p * c->shift, c->debug & 1);
+  cnp_launch(c, kern, dim3(grid), dim3(TP::NT), TP::bytes, in, out, vscale, c->slice, (int)c->ld, c->nx,
+             (const double*)c->d_gam, (const double*)c->d_igam, (const double2*)c->d_lam1, (const double2*)c->d_lam2,
+             (const double*)c->d_ex, (const double*)c->d_ey, c->tau_p, c->tau_p * c->shift, c->debug & 1);
   return cudaGetLastError();
 }
 
