@@ -46,7 +46,6 @@ __global__ void __launch_bounds__(256, DST_MINB)
     k_dst(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
           const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
           int nx) {
-  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   using LY = DstLayout<LOGE, NC>;
   constexpr int NT = 256;
   constexpr int M = LY::M;
@@ -60,6 +59,7 @@ __global__ void __launch_bounds__(256, DST_MINB)
   // ---- tables once per CTA: stage twiddles, pre-scaling of the extension (0 at e = 0, M)
   fill_stage_twiddles(stw, LOGE, debug_sign ? -1.0 : 1.0, tid, NT);
   for (int e = tid; e <= M; e += NT) pre_s[e] = (e == 0 || e == M) ? 0.0 : (pre ? pre[e - 1] : 1.0);
+  pdl_enter();  // PDL: tables above are create-time constants; the lines below come from the previous kernel
   // tiles: x pass — NC row pairs; y pass — NC adjacent column pairs of one time slice
   const int nlines = N * ny;
   const int pairs_per_t = ldi / 2;
@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(DstPlan<LOGE>::NT, LOGE <= 9 ? 2 : 1)
     k_dst_r(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
             const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
             int nx) {
-  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   using P = DstPlan<LOGE>;
   constexpr int E = P::E, M0 = P::M0, n = M0 - 1;
   constexpr int R1 = P::R1, R2 = P::R2, R3 = P::R3, M = P::M, NC = P::NC, TP = P::TP;
@@ -188,6 +187,7 @@ __global__ void __launch_bounds__(DstPlan<LOGE>::NT, LOGE <= 9 ? 2 : 1)
   const double sg = debug_sign ? -1.0 : 1.0;
   for (int q = tid; q < E; q += P::NT) { double2 w = expi_neg(q, E); w.y *= sg; twE[q] = w; }
   for (int e = tid; e <= M0; e += P::NT) pre_s[e] = (e == 0 || e == M0) ? 0.0 : (pre ? pre[e - 1] : 1.0);
+  pdl_enter();  // PDL: tables above are create-time constants; the lines below come from the previous kernel
   __syncthreads();
   const int ldi = (int)ld;
   const int nlines = N * ny;
