@@ -774,15 +774,9 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   double* b_nc = const_cast<double*>(d_b);
   V[0] = b_nc;
   c->post = post_cycle_start(c, 1);  // run by launch_norm2's folding block
-  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));  // its post op also fills the mapped scalars
-  CK(cudaStreamSynchronize(c->stream));
-  if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
-    CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (rep) { rep->iterations = 0; rep->restarts = 0; rep->converged = 1; rep->relres_est = 0; rep->relres_true = 0; }
-    return CNPINT_OK;
-  }
-  if (!std::isfinite(h[0])) { seterr(c, "gmres: ||b|| not finite"); return CNPINT_EBREAKDOWN; }
+  CK(launch_norm2(c, d_b, c->d_part, c->d_scal + 2));
+  // no host read here: ‖b‖ (h[0]) arrives with the first Arnoldi step's scalars, where b = 0 (every
+  // quantity of that step is then 0 or NaN and is discarded) and a non-finite b are handled
   std::vector<double*> Z(restart);
   for (int i = 0; i < restart; ++i) Z[i] = c->d_Z + (size_t)i * vec;
   while (true) {
@@ -816,6 +810,15 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       }
       if (nv > CNP_MAX_DOT) CK(launch_scal_to_host(c));  // else the finalize post op wrote them
       CK(cudaStreamSynchronize(c->stream));
+      if (its == 0 && cycles == 0) {  // ‖b‖ of the cycle start
+        if (h[0] == 0.0) {  // b = 0 ⇒ u = 0
+          CK(cudaMemsetAsync(d_u, 0, vec * sizeof(double), c->stream));
+          CK(cudaStreamSynchronize(c->stream));
+          if (rep) { rep->iterations = 0; rep->restarts = 0; rep->converged = 1; rep->relres_est = 0; rep->relres_true = 0; }
+          return CNPINT_OK;
+        }
+        if (!std::isfinite(h[0])) { seterr(c, "gmres: ||b|| not finite"); return CNPINT_EBREAKDOWN; }
+      }
       ++its;
       jdone = j + 1;
       est = h[1];

@@ -468,6 +468,23 @@ def test_zero_rhs_and_determinism():
     assert torch.equal(u1, u2)                # deterministic reductions: bitwise reproducible
 
 
+def test_gmres_nonfinite_rhs_rejected():
+    """‖b‖ is read with the first Arnoldi step's scalars (no separate host read): a NaN or inf in b
+    must still end the solve with CNPINT_EBREAKDOWN (raised by the binding), and the handle must stay
+    usable for a finite b afterwards."""
+    w = SMALL["1d_small"]
+    s = solver_for(w, restart_max=10)
+    b = problems.rhs(w, s)
+    for bad in (float("nan"), float("inf")):
+        bb = b.clone()
+        bb.view(-1)[3] = bad
+        with pytest.raises(Exception):
+            s.gmres(bb, s.empty(), 1e-10, 10)
+    u = s.empty()
+    rep = s.gmres(b, u, 1e-10, 10)
+    assert rep["converged"]
+
+
 # ------------------------------------------------------------------------------ c5 sweep
 @pytest.mark.parametrize("n,N", [(127, 256), (127, 1024)])
 def test_gmres_c5_small_vs_oracle(n, N):
