@@ -65,10 +65,24 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
   pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
   double acc[1] = {0.0};
   const double2* w2 = reinterpret_cast<const double2*>(w);
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+  // four independent loads in flight per thread (a one-load grid-stride loop leaves the HBM idle
+  // between a load and its use); fixed per-thread summation order, so still deterministic
+  const size_t stride_e = (size_t)gridDim.x * blockDim.x;
+  size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (; e + 3 * stride_e < n2; e += 4 * stride_e) {
+    const double2 x0 = ldg_cs2(w2 + e), x1 = ldg_cs2(w2 + e + stride_e);
+    const double2 x2 = ldg_cs2(w2 + e + 2 * stride_e), x3 = ldg_cs2(w2 + e + 3 * stride_e);
+    acc[0] = fma(x0.x, x0.x, fma(x0.y, x0.y, acc[0]));
+    a1 = fma(x1.x, x1.x, fma(x1.y, x1.y, a1));
+    a2 = fma(x2.x, x2.x, fma(x2.y, x2.y, a2));
+    a3 = fma(x3.x, x3.x, fma(x3.y, x3.y, a3));
+  }
+  for (; e < n2; e += stride_e) {
     const double2 x = ldg_cs2(w2 + e);
     acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
   }
+  acc[0] += (a1 + a2) + a3;
   block_reduce_write<1>(acc, part, stride);
   if (grid_fold(part, gridDim.x, stride, 1, out, counter)) run_post(post);
 }
