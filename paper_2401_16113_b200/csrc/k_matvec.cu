@@ -11,6 +11,7 @@
 #include "post_op.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 // ------------------------------------------------------------------------------- K0 stream copy
 __global__ void __launch_bounds__(256) k_stream_copy(const double2* __restrict__ src, double2* __restrict__ dst,
@@ -73,6 +74,17 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
     part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (size_t)blockIdx.z)] = s;
   }
   if (out && grid_fold(part, gridDim.x * gridDim.y * gridDim.z, 1, 1, out, counter)) run_post(post);
+}
+
+// rows of the time chunk a 1D block walks (CNPINT_MV_TCHUNK: tuning override, 8/16/32/64)
+static int mv_tchunk(const cnpint_ctx* c) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CNPINT_MV_TCHUNK");
+    const int t = e ? atoi(e) : 0;
+    v = (t == 8 || t == 16 || t == 32 || t == 64) ? t : 0;
+  }
+  return v ? v : (c->N >= 4096 ? 32 : 16);
 }
 
 // ------------------------------------------------------------------------------- K1 1D
@@ -305,7 +317,7 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
   if (NORM) c->post = PostOp{};
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
-    const int tchunk = c->N >= 4096 ? 32 : 16;
+    const int tchunk = mv_tchunk(c);
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     const cudaError_t e = cnp_launch(c, k_matvec1d<MODE, NORM>, grid, block, 0, u, y, b, c->d_lo, c->d_di, c->d_up,
@@ -330,7 +342,7 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
   const double htau = 0.5 * c->tau;
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
-    const int tchunk = c->N >= 4096 ? 32 : 16;
+    const int tchunk = mv_tchunk(c);
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
     const cudaError_t e = cnp_launch(c, k_matvec1d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr,
@@ -370,7 +382,7 @@ cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double
 
 int matvec_partial_blocks(const cnpint_ctx* c) {
   if (c->dim == 1) {
-    const int tchunk = c->N >= 4096 ? 32 : 16;
+    const int tchunk = mv_tchunk(c);
     return (int)(((c->ld / 2 + 127) / 128) * ((c->N + tchunk - 1) / tchunk));
   }
   return (int)(((c->ld + 63) / 64) * ((c->ny + 7) / 8) * ((c->N + 15) / 16));
