@@ -166,7 +166,7 @@ struct TfftCfg {
   int C, logN2, X, CS, T, ok;
   size_t smem;
 };
-TfftCfg tfft_cfg(int N);
+TfftCfg tfft_cfg(int N, int mode = 0);  // mode: 0/1 1D forward/inverse, 2 the 2D time pass
 cudaError_t launch_tfft_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_tfft_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_tfft_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);

@@ -364,14 +364,15 @@ __global__ void __launch_bounds__(TF_NT, 2)
   if constexpr (C > 1) cg::this_cluster().sync();  // no CTA leaves while others may access its smem
 }
 
-TfftCfg tfft_cfg(int N) {
+TfftCfg tfft_cfg(int N, int mode) {
   TfftCfg f;
   int logN = 0;
   while ((1 << logN) < N) ++logN;
   // default (measured, profiles/r01_tfft_sweep.txt): a pair of CTAs (C = 2) for 1024 <= N <= 4096,
   // C = 8 beyond; tiles of 16 columns (128-B row segments) while N2 <= 512, 8 at N2 = 1024, 4 at
-  // N2 = 2048.
-  f.C = N >= 8192 ? 8 : N >= 1024 ? 2 : 1;
+  // N2 = 2048.  The 2D time pass at N = 1024 (c5 N1024) runs one CTA per tile (C = 1): 200 → 187 µs
+  // at n = 127, 759 → 714 µs at n = 255 (profiles/r01_k6_sweep.txt).
+  f.C = N >= 8192 ? 8 : (N >= 1024 && !(mode == 2 && N == 1024)) ? 2 : 1;
   if (const char* e = getenv("CNPINT_TFFT_C")) {  // tuning override (experiments only)
     const int v = atoi(e);
     if ((v == 1 || v == 2 || v == 4 || v == 8) && N / v >= 2 && N / v <= 2048) f.C = v;
@@ -440,7 +441,7 @@ static cudaError_t dispatch(cnpint_ctx* c, const TfftCfg& f, const double* vin, 
 template <int MODE>
 static cudaError_t run_tfft(cnpint_ctx* c, const double* vin, const double2* spin, double* vout, double2* spout,
                             const double* vscale, int accumulate) {
-  const TfftCfg f = tfft_cfg(c->N);
+  const TfftCfg f = tfft_cfg(c->N, MODE);
   const int kid = MODE == 0 ? KID_FFT_FWD : MODE == 1 ? KID_FFT_INV : KID_TIMEPASS2D;
   const double bytes = MODE == 2 ? 16.0 * cnp_units(c)
                                  : 8.0 * cnp_units(c) * (accumulate ? 2.0 : 1.0) + 16.0 * cnp_spec_units(c);

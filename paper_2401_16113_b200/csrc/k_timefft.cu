@@ -233,6 +233,6 @@ cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int 
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_pass_2d(c, in, out, vscale);
   if (!(c->debug & 8) && tpass_ok(c)) return launch_tpass_2d(c, in, out, vscale);  // N = 256, 512 (bit 64 off)
-  if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_pass_2d(c, in, out, vscale);
+  if (tfft_cfg(c->N, 2).ok && !(c->debug & 8)) return launch_tfft_pass_2d(c, in, out, vscale);
   return run_fft<2>(c, in, nullptr, out, nullptr, vscale, 0);
 }
