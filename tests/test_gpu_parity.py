@@ -468,6 +468,23 @@ def test_zero_rhs_and_determinism():
     assert torch.equal(u1, u2)                # deterministic reductions: bitwise reproducible
 
 
+@pytest.mark.parametrize("name", ["1d_small", "2d_small", "1d_N2048_ragged"])
+def test_pdl_launches_bitwise_equal(name, monkeypatch):
+    """Programmatic dependent launch (default) only changes when a kernel becomes resident, never what
+    it reads: a GMRES solve with PDL on and one with plain launches (CNPINT_PDL=0, read at create)
+    give bitwise identical solutions (the reductions are deterministic)."""
+    w = SMALL[name]
+    out = []
+    for pdl in ("0", "1"):
+        monkeypatch.setenv("CNPINT_PDL", pdl)
+        s = solver_for(w, restart_max=w.restart)
+        u = s.empty()
+        rep = s.gmres(problems.rhs(w, s), u, w.tol, w.restart)
+        assert rep["converged"]
+        out.append(u.clone())
+    assert torch.equal(out[0], out[1])
+
+
 def test_gmres_nonfinite_rhs_rejected():
     """‖b‖ is read with the first Arnoldi step's scalars (no separate host read): a NaN or inf in b
     must still end the solve with CNPINT_EBREAKDOWN (raised by the binding), and the handle must stay
