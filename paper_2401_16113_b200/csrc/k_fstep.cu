@@ -43,6 +43,9 @@
 #ifndef FS_NC7
 #define FS_NC7 16  // pair columns per block when max(N1, N2) >= 128 (16 threads per column)
 #endif
+#ifndef FS_MINB6
+#define FS_MINB6 0  // CTAs per SM for N1, N2 <= 64 (0: 768 threads per SM)
+#endif
 #ifndef FS_MINB7
 #define FS_MINB7 2
 #endif
@@ -133,7 +136,8 @@ struct FsGeo {
   static constexpr int TP1 = RF<LOG1>::R1 > RF<LOG1>::R2 ? RF<LOG1>::R1 : RF<LOG1>::R2;
   static constexpr int TP2 = RF<LOG2>::R1 > RF<LOG2>::R2 ? RF<LOG2>::R1 : RF<LOG2>::R2;
   static constexpr int NT = NC * (TP1 > TP2 ? TP1 : TP2);  // threads: tid = col + NC·j
-  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (NT <= 384 ? 768 / NT / TT : 1) : MODE == 2 ? 2 : FS_MINB7;
+  static constexpr int MINB = (MX <= 6 && MODE != 2) ? (FS_MINB6 > 0 ? FS_MINB6 : NT <= 384 ? 768 / NT / TT : 1)
+                                                   : MODE == 2 ? 2 : FS_MINB7;
   // items per block and phase (see k_fstep); PER = slots per schedule step
   static constexpr int NFAM = 2 * (N2 / 2 + 1);
   static constexpr int NP0 = MODE == 1 ? NFAM : N1 / TT, NP1 = MODE == 2 ? NFAM : 0, NP2 = MODE == 0 ? NFAM : N1 / TT;
