@@ -91,6 +91,9 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_norm2(const double* __restr
 // coef_i = cd[i] (MODE 1, combine, w may be null), optionally fused partial dots with Ṽ (DOTS) or
 // Σ w_out² (NORM).  NOWRITE: w_out is only formed in registers (its dots are the product), nothing
 // is stored — CGS2's second projection c2 = Ṽᵀ(w − Ṽ s²c1) without writing the intermediate.
+#ifndef UPD_REVERSE
+#define UPD_REVERSE 1
+#endif
 // GDOTS (with NORM): also Ṽᵢᵀ w_out — the Gram row of the new basis vector for Gram CGS2; the fold
 // writes out[0] = Σ w_out², out[1 + i] = Ṽᵢᵀ w_out.
 template <int NV, int MODE, bool DOTS, bool NORM, bool NOWRITE = false, bool GDOTS = false>
@@ -122,7 +125,11 @@ __global__ void __launch_bounds__(CNP_RED_THREADS) k_update(VPtrs V, const doubl
   for (int i = 0; i < NA; ++i) acc[i] = 0.0;
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* o2 = reinterpret_cast<double2*>(wout);
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n2; e += (size_t)gridDim.x * blockDim.x) {
+  // GDOTS (Gram update, always right after the matvec that wrote w front to back): walk the vectors
+  // back to front, so the tail of w the matvec left in the 126-MB L2 is read before this kernel's own
+  // traffic evicts it (a front-to-back reader evicts each line just before it needs it)
+  for (size_t e0 = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e0 < n2; e0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = (GDOTS && UPD_REVERSE) ? n2 - 1 - e0 : e0;
     double2 x = w2 ? w2[e] : make_double2(0.0, 0.0);
     double2 v[NV];
 #pragma unroll

@@ -76,6 +76,9 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
   if (out && grid_fold(part, gridDim.x * gridDim.y * gridDim.z, 1, 1, out, counter)) run_post(post);
 }
 
+#ifndef MV_REVERSE
+#define MV_REVERSE 1
+#endif
 // rows of the time chunk a 1D block walks (CNPINT_MV_TCHUNK: tuning override, 8/16/32/64)
 static int mv_tchunk(const cnpint_ctx* c) {
   static int v = -1;
@@ -106,7 +109,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
   const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
   const bool active = 2 * gx < ld;
   const int64_t x0 = active ? 2 * gx : 0;
-  const int t0 = blockIdx.y * tchunk;
+  // residual (MODE >= 2, right after the combine wrote u front to back): time chunks back to front,
+  // so u's tail still in L2 is read first (see k_update's GDOTS walk)
+  const int t0 = ((MODE >= 2 && MV_REVERSE) ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y) * tchunk;
   const int t1 = min(N, t0 + tchunk);
   const bool hasL = active && lane == 0 && x0 > 0;
   const bool hasR = lane == 31 && active && x0 + 2 < ld;
@@ -214,7 +219,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
   const int yrow = blockIdx.y * 8 + wy;
-  const int t0 = blockIdx.z * tchunk;
+  const int t0 = ((MODE >= 2 && MV_REVERSE) ? (int)(gridDim.z - 1 - blockIdx.z) : (int)blockIdx.z) * tchunk;
   const int t1 = min(N, t0 + tchunk);
   const bool colok = x0 < ld;
   const bool rowok = yrow < ny;
