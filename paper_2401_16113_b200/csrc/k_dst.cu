@@ -38,11 +38,17 @@ struct DstLayout {
 
 }  // namespace
 
+#ifndef DST_NC9
+#define DST_NC9 4  // line pairs per Stockham tile at 2(n+1) = 512 (c4 x pass: 241 -> 233 us with 4 CTAs/SM)
+#endif
+#ifndef DST_MINB9
+#define DST_MINB9 4
+#endif
 #ifndef DST_MINB
 #define DST_MINB 2
 #endif
 template <bool YPASS, int LOGE, int NC>
-__global__ void __launch_bounds__(256, DST_MINB)
+__global__ void __launch_bounds__(256, LOGE == 9 ? DST_MINB9 : DST_MINB)
     k_dst(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
           const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
           int nx) {
@@ -338,7 +344,7 @@ static cudaError_t run_dst_r(cnpint_ctx* c, const double* in, double* out, const
 template <bool YPASS, int LOGE>
 static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
                              int accumulate) {
-  constexpr int NC = LOGE <= 9 ? 8 : LOGE == 10 ? 4 : 2;
+  constexpr int NC = LOGE == 9 ? DST_NC9 : LOGE < 9 ? 8 : LOGE == 10 ? 4 : 2;
   using LY = DstLayout<LOGE, NC>;
   auto kern = k_dst<YPASS, LOGE, NC>;
   static int grid_max = 0;
