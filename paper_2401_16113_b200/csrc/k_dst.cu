@@ -41,6 +41,15 @@ struct DstLayout {
 #ifndef DST_NC9
 #define DST_NC9 4  // line pairs per Stockham tile at 2(n+1) = 512 (c4 x pass: 241 -> 233 us with 4 CTAs/SM)
 #endif
+#ifndef DST_NC10
+#define DST_NC10 4
+#endif
+#ifndef DST_MINB10
+#define DST_MINB10 2
+#endif
+#ifndef DST_MINB8
+#define DST_MINB8 4  // 2(n+1) <= 256 (c5 n = 127): 4 CTAs/SM, x 129 -> 119 us, y 130 -> 122 us at N = 1024
+#endif
 #ifndef DST_MINB9
 #define DST_MINB9 4
 #endif
@@ -48,7 +57,7 @@ struct DstLayout {
 #define DST_MINB 2
 #endif
 template <bool YPASS, int LOGE, int NC>
-__global__ void __launch_bounds__(256, LOGE == 9 ? DST_MINB9 : DST_MINB)
+__global__ void __launch_bounds__(256, LOGE <= 8 ? DST_MINB8 : LOGE == 9 ? DST_MINB9 : LOGE == 10 ? DST_MINB10 : DST_MINB)
     k_dst(const double* __restrict__ in, double* __restrict__ out, int N, int ny, int64_t ld,
           const double* __restrict__ pre, const double* __restrict__ post, int accumulate, int debug_sign,
           int nx) {
@@ -344,7 +353,7 @@ static cudaError_t run_dst_r(cnpint_ctx* c, const double* in, double* out, const
 template <bool YPASS, int LOGE>
 static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
                              int accumulate) {
-  constexpr int NC = LOGE == 9 ? DST_NC9 : LOGE < 9 ? 8 : LOGE == 10 ? 4 : 2;
+  constexpr int NC = LOGE == 9 ? DST_NC9 : LOGE < 9 ? 8 : LOGE == 10 ? DST_NC10 : 2;
   using LY = DstLayout<LOGE, NC>;
   auto kern = k_dst<YPASS, LOGE, NC>;
   static int grid_max = 0;
