@@ -60,6 +60,9 @@ CNP_DEV void p3_step3(double2 (&w)[P::R3], const double2* area, int r) {
   dftR<P::R3, INV>(w);
 }
 
+#ifndef TP_MINB
+#define TP_MINB 2
+#endif
 template <int LOGN>
 struct TpPlan {
   static constexpr int N = 1 << LOGN, H = N / 2;
@@ -67,7 +70,7 @@ struct TpPlan {
   using I = P3<N / 64, 8, 8>;           // inverse (transposed)
   static constexpr int TP = N >= 1024 ? N / 8 : 64;  // max role count of both plans
   static constexpr int NC = 512 / TP;   // column pairs per tile (8: 128-B row segments; 4 at N = 1024)
-  static constexpr int MINB = N >= 1024 ? 1 : 2;
+  static constexpr int MINB = N >= 1024 ? 1 : TP_MINB;
   static constexpr int NT = NC * TP;
   static constexpr int AREA = (F::AREA > I::AREA ? F::AREA : I::AREA) | 1;
   static constexpr int HI = N / 64;
