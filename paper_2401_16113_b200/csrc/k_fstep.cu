@@ -596,7 +596,9 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   const int grid_max = per_sm * c->num_sms;
   // lag: enough steps between a block's phases that the CTAs in flight (≈ grid) finish the earlier
   // phase first
-  int L = 2 * ((grid_max + per - 1) / per) + 1;
+  // (measured, profiles/r01_fs_sweep.txt: c2 (c = 7) best near 21, c3 (c = 2) at 5)
+  const int cpl = (grid_max + per - 1) / per;  // schedule steps the resident CTAs span
+  int L = cpl <= 2 ? 2 * cpl + 1 : (3 * cpl < 21 ? 3 * cpl : 21);
   if (const char* e = getenv("CNPINT_FS_LAG")) L = atoi(e) > 0 ? atoi(e) : L;
   S.lag[0] = 0;
   S.lag[1] = L;
