@@ -1,17 +1,19 @@
 #!/usr/bin/env python
 """bench.py — the driver's benchmark contract for cnpint (arxiv 2401.16113 hot path on B200).
 
-Workload (N=1): BASELINE.json configs[1] ("c2"): 1D Black–Scholes in log price, m = 4095, N = 4096
-(16.8 M fp64 unknowns), α = 0.01 (the middle of the config's α set), GMRES(restart 30), tol 1e-10,
-zero initial guess, manufactured-solution right-hand side b (synthetic, resident in HBM).
+Workload (N=1): BASELINE.json's metric names no config, so the headline is the largest single-GPU
+configuration: configs[4] at n = 511, N = 1024 ("c5_n511_N1024": 2D Black–Scholes, 261,121 spatial
+unknowns x 1024 steps = 267 M fp64 unknowns), α = 0.01, GMRES(20), tol 1e-10, zero initial guess,
+manufactured-solution right-hand side b (synthetic, resident in HBM).
 
 Step = one full right-preconditioned GMRES solve to tolerance — every row of SURVEY.md §8(a):
-K1 AaO matvec, K2/K3/K4 P_α⁻¹ (Γ-scaled time FFT, batched complex tridiagonal solves, inverse FFT),
-K7 CGS2 Arnoldi passes, K8 Givens/Hessenberg on device, K9 cycle end (GEMV, P⁻¹, true residual).
-value = GMRES solves/s (time-to-tolerance⁻¹), whole job over all ranks.  Alongside: P_α⁻¹ applies/s,
-AaO matvec GB/s and their fraction of the measured HBM peak, K0 stream-copy GB/s, the per-kernel
-breakdown (CUDA events on the launch stream), the live roofline of the dominant kernel, the
-end-to-end number through the host-buffer C-ABI call, and the CPU oracle on the same box.
+K1 AaO matvec, P_α⁻¹ (2D: K5 sine passes + K6 fused time pass; 1D: K2/K3/K4), K7 CGS2 Arnoldi
+passes, K8 Givens/Hessenberg on device, K9 cycle end.  value = GMRES solves/s (time-to-tolerance⁻¹),
+whole job over all ranks.  Alongside: P_α⁻¹ applies/s, AaO matvec GB/s and their fraction of the
+measured HBM peak, K0 stream-copy GB/s, same-run fp64 FMA / DMMA ceilings, the per-kernel breakdown
+(CUDA events on the launch stream), the live roofline of the dominant kernel, the end-to-end number
+through the host-buffer C-ABI call, a per-workload table of every other BASELINE config (c1, c2 at
+three α, c3, c4, the other c5 sizes) and the CPU oracle on the same box.
 
 Multi-GPU: replicas only: each rank solves its own copy; no data-path collective.
 `--impl reference` times the CPU oracle (oracle/, numpy) on the same workload and metric.
@@ -154,6 +156,14 @@ def ncu_traffic(kernel: str, workload: str):
 
 
 # ----------------------------------------------------------------------------------- workload
+HEADLINE = "c5_n511_N1024"   # BASELINE.json configs[4] at its largest size (267 M unknowns, one GPU)
+UNIT = "GMRES solves/s (time-to-tol^-1, whole job)"
+# the per-workload table (same run): every other BASELINE config
+TABLE = [("c1", None), ("c2", 0.1), ("c2", 0.01), ("c2", 0.001), ("c3", None), ("c4", None),
+         ("c5_n127_N256", None), ("c5_n127_N1024", None), ("c5_n255_N256", None), ("c5_n255_N1024", None),
+         ("c5_n511_N256", None)]
+
+
 def workload(name: str, alpha: float | None):
     import synth
     w = synth.WORKLOADS[name]
@@ -165,6 +175,74 @@ def describe(w):
             f"({w.unknowns:,} fp64), T={w.T}, alpha={w.alpha}, GMRES({w.restart}) tol {w.tol}, x0=0")
 
 
+def pinv_structured_bytes(w):
+    """Algorithmic bytes of one P_α⁻¹ as structured: 1D K2 + K3 + K4 (8 B in, 16 B per
+    half-spectrum complex out / in + out / in, 8 B out); 2D W⁻¹ (x, y), time pass, W (y, x): 5 × 16 B."""
+    if w.dim == 1:
+        return 16.0 * w.unknowns + 32.0 * (w.N // 2 + 1) * w.m + 16.0 * w.unknowns
+    return 80.0 * w.unknowns
+
+
+def time_ops(s, w, stream, nvec, reps):
+    """Standalone P⁻¹ and 𝓜 rates on nvec seeded N(0,1) vectors (each > L2 at the large configs)."""
+    import torch
+    import synth
+    V = synth.random_vectors(w, nvec, w.rand_seed)
+    dv = [s.to_device(v) for v in V]
+    del V
+    out = [s.empty() for _ in range(2)]
+    for i in range(3):
+        s.apply_Pinv(dv[i % nvec], out[0])
+        s.apply_A(dv[i % nvec], out[1])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(reps):
+        s.apply_Pinv(dv[i % nvec], out[i % 2])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pinv_s = e0.elapsed_time(e1) * 1e-3 / reps
+    e0.record(stream)
+    for i in range(reps):
+        s.apply_A(dv[i % nvec], out[i % 2])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    mv_s = e0.elapsed_time(e1) * 1e-3 / reps
+    del dv, out
+    return pinv_s, mv_s
+
+
+def op_rates(w, pinv_s, mv_s, peak):
+    st = pinv_structured_bytes(w) / pinv_s / 1e9
+    mv = 16.0 * w.unknowns / mv_s / 1e9
+    return ({"applies_per_s": 1.0 / pinv_s, "ms": 1e3 * pinv_s, "effective_GBps": 16.0 * w.unknowns / pinv_s / 1e9,
+             "structured_GBps": st, "structured_frac": st / peak},
+            {"ms": 1e3 * mv_s, "GBps": mv, "frac": mv / peak})
+
+
+def peak_ceilings(dev):
+    """Same-run fp64 compute ceilings: dependent-FMA and mma.sync f64 (DMMA) loops."""
+    import torch
+    from paper_2401_16113_b200.cnpint import peak_kernel
+    out = torch.empty(8 * 148 * 256 * 2, dtype=torch.float64, device=dev)
+    res = {}
+    stream = torch.cuda.current_stream()
+    for kind, name in ((0, "fp64_fma_TFLOPs"), (1, "fp64_dmma_TFLOPs")):
+        best = 0.0
+        peak_kernel(kind, out, 256)
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fl = peak_kernel(kind, out, 4096)
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, fl / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        res[name] = best
+    res["how"] = ("cnpint_peak_kernel: 8 CTAs x 256 threads per SM, 4096 rounds of 8 dependent-FMA chains per "
+                  "thread / 4 mma.sync.m8n8k4 f64 accumulators per warp; best of 5, CUDA events")
+    return res
+
+
 # ----------------------------------------------------------------------------------- GPU arm
 def run_gpu(args, rank, world, local):
     import numpy as np
@@ -172,16 +250,12 @@ def run_gpu(args, rank, world, local):
 
     from paper_2401_16113_b200 import problems
     from paper_2401_16113_b200.cnpint import stream_copy
-    import synth
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     w = workload(args.workload, args.alpha)
-    s = problems.make_solver(w, restart_max=w.restart)
-    b = problems.rhs(w, s)
-    u = s.empty()
+    peak, peak_src = measured_hbm_peak()
     stream = torch.cuda.current_stream()
-    vec_bytes = s.vec_elems * 8
 
     # K0: same-run stream copy (HBM reference), 2 x 1 GiB buffers, best of 10
     n = (1 << 30) // 8
@@ -197,15 +271,20 @@ def run_gpu(args, rank, world, local):
         copy_best = max(copy_best, 2 * n * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9)
     del a0, a1
     torch.cuda.empty_cache()
+    ceilings = peak_ceilings(dev)
+
+    s = problems.make_solver(w, restart_max=w.restart)
+    b = problems.rhs(w, s)
+    u = s.empty()
+    vec_bytes = s.vec_elems * 8
 
     clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
-    # warm-up solves
     for _ in range(args.warmup):
         rep = s.gmres(b, u, w.tol, w.restart)
     torch.cuda.synchronize()
-    # ---------------- timed region: K full GMRES solves
+    # ---------------- timed region: K full GMRES solves (inputs resident in HBM)
     barrier(world)
     torch.cuda.synchronize()
     l0 = s.launch_count()
@@ -227,7 +306,6 @@ def run_gpu(args, rank, world, local):
 
     # ---------------- per-kernel breakdown: the same K solves again with the event profiler on
     s.profile_enable(True)
-    p0 = time.perf_counter()
     for _ in range(args.steps):
         s.gmres(b, u, w.tol, w.restart)
     torch.cuda.synchronize()
@@ -237,110 +315,33 @@ def run_gpu(args, rank, world, local):
     for name, (ms, cnt, by) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps,
                          "avg_launch_us": 1e3 * ms / cnt, "algo_GBps": (by / (ms * 1e-3) / 1e9) if by else None}
+    for k in kernels.values():
+        k["frac"] = k["algo_GBps"] / peak if k["algo_GBps"] else None
     dominant = max(prof.items(), key=lambda kv: kv[1][0] if kv[1][2] > 0 else -1)[0]
     d_ms, d_cnt, d_by = prof[dominant]
-    peak, peak_src = measured_hbm_peak()
-    for k in kernels.values():  # every kernel's fraction of the same HBM peak
-        k["frac"] = k["algo_GBps"] / peak if k["algo_GBps"] else None
     achieved = d_by / (d_ms * 1e-3) / 1e9
     total_prof_ms = sum(v[0] for v in prof.values())
     traffic = ncu_traffic(dominant, w.name)
 
-    # ---------------- standalone P⁻¹ applies/s and matvec GB/s on 4 seeded N(0,1) vectors (> L2)
-    V = synth.random_vectors(w, 4, w.rand_seed)
-    dv = [s.to_device(v) for v in V]
-    out = [s.empty() for _ in range(2)]
-    for i in range(3):
-        s.apply_Pinv(dv[i % 4], out[0])
-        s.apply_A(dv[i % 4], out[1])
-    torch.cuda.synchronize()
-    reps_p = max(20, args.steps)
-    e0.record(stream)
-    for i in range(reps_p):
-        s.apply_Pinv(dv[i % 4], out[i % 2])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    pinv_s = e0.elapsed_time(e1) * 1e-3 / reps_p
-    e0.record(stream)
-    for i in range(reps_p):
-        s.apply_A(dv[i % 4], out[i % 2])
-    e1.record(stream)
-    torch.cuda.synchronize()
-    mv_s = e0.elapsed_time(e1) * 1e-3 / reps_p
-    unknowns = w.unknowns
-    mv_gbps = 16.0 * unknowns / mv_s / 1e9
-    if w.dim == 1:  # K2 (8 B in, 16 B/complex out), K3 (in + out), K4: three passes
-        pinv_gbps_structured = (16.0 * unknowns + 32.0 * (w.N // 2 + 1) * w.m + 16.0 * unknowns) / pinv_s / 1e9
-    else:  # 2D: DST x, DST y, time pass, DST y, DST x — five real passes of 16 B per unknown
-        pinv_gbps_structured = 80.0 * unknowns / pinv_s / 1e9
-    del dv, out
+    # ---------------- standalone P⁻¹ applies/s and matvec GB/s
+    pinv_s, mv_s = time_ops(s, w, stream, 2 if w.unknowns > 1e8 else 4, max(10, args.steps))
+    pinv_d, mv_d = op_rates(w, pinv_s, mv_s, peak)
 
-    # ---------------- end to end through the host-buffer C-ABI call (pinned host memory)
-    hshape = synth.shape_of(w)  # packed host layout: (N, m) in 1D, (N, n, n) in 2D
+    # ---------------- end to end through the host-buffer C-ABI call (pinned host memory): every step
+    # copies its b in (H2D) and its u out (D2H) inside the timed region
+    import synth
+    hshape = synth.shape_of(w)
     bh = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
     bh.copy_(b[..., : w.n].cpu())
     uh = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
     bnp, unp = bh.numpy(), uh.numpy()
-    s.gmres_host(bnp, w.tol, w.restart, u=unp)
-    torch.cuda.synchronize()
-    barrier(world)
-    h0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(args.steps):
-        s.gmres_host(bnp, w.tol, w.restart, u=unp)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_t = e0.elapsed_time(e1) * 1e-3
-    e2e_wall = time.perf_counter() - h0
-    e2e_single = whole_job_throughput(args.steps, max(e2e_t, 1e-12), world)
-
-    # ---------------- the same, with E handles on E CUDA streams driven by E host threads: one solve's
-    # PCIe copies (H2D of b, D2H of u, ≈ 2.4 ms each way at c2) overlap another solve's GPU work.
-    # Every step still copies its own input in and its result out; value = solves / wall time.
-    import threading
-    ne = max(1, args.e2e_streams)
-    handles = [(s, stream, bnp, unp)]
-    for _ in range(ne - 1):
-        st_i = torch.cuda.Stream()
-        with torch.cuda.stream(st_i):
-            s_i = problems.make_solver(w, restart_max=w.restart)
-        bh_i = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
-        bh_i.copy_(bh)
-        uh_i = torch.empty(hshape, dtype=torch.float64, pin_memory=True)
-        handles.append((s_i, st_i, bh_i.numpy(), uh_i.numpy()))
-    counts = [args.steps // ne + (1 if i < args.steps % ne else 0) for i in range(ne)]
-    reps_e2e = [None] * ne
-
-    def drive(i):
-        s_i, st_i, b_i, u_i = handles[i]
-        with torch.cuda.stream(st_i):
-            for _ in range(counts[i]):
-                _, reps_e2e[i] = s_i.gmres_host(b_i, w.tol, w.restart, u=u_i)
-
-    for i in range(ne):  # warm-up of every handle
-        s_i, st_i, b_i, u_i = handles[i]
-        with torch.cuda.stream(st_i):
-            s_i.gmres_host(b_i, w.tol, w.restart, u=u_i)
-    torch.cuda.synchronize()
-    barrier(world)
-    h1 = time.perf_counter()
-    threads = [threading.Thread(target=drive, args=(i,)) for i in range(ne)]
-    for t_ in threads:
-        t_.start()
-    for t_ in threads:
-        t_.join()
-    torch.cuda.synchronize()
-    e2e_multi_wall = time.perf_counter() - h1
-    assert all(r is None or r["converged"] for r in reps_e2e)
-    assert all(np.array_equal(handles[i][3], unp) for i in range(1, ne))  # same solution on every handle
-    e2e_value = whole_job_throughput(args.steps, max(e2e_multi_wall, 1e-12), world)
-    del handles
-    err_seq = None
-
+    ne = max(1, args.e2e_streams if args.e2e_streams > 0 else (1 if w.unknowns > 1e8 else 4))
+    e2e = run_e2e(s, w, stream, bnp, unp, ne, args.steps, world)
+    del bh, uh, u
     result = {
         "metric": METRIC,
         "value": value,
-        "unit": "GMRES solves/s (time-to-tol^-1, whole job)",
+        "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -350,18 +351,17 @@ def run_gpu(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (manufactured-solution rhs; seeded N(0,1) vectors, numpy default_rng)",
-        "config": {"workload": describe(w), "N": w.N, "m": w.m, "alpha": w.alpha, "restart": w.restart,
-                   "tol": w.tol, "parallelism": f"replicas x{world} (no data-path collective)",
-                   "l2": "inputs larger than L2: one vector is %.0f MB; a solve streams ~%d vectors" %
-                         (vec_bytes / 1e6, 50)},
+        "config": {"workload": describe(w), "name": w.name, "N": w.N, "m": w.m, "alpha": w.alpha,
+                   "restart": w.restart, "tol": w.tol,
+                   "parallelism": f"replicas x{world} (no data-path collective)",
+                   "l2": "inputs larger than L2: one vector is %.0f MB (L2 126 MB); a solve streams ~50 vectors" %
+                         (vec_bytes / 1e6)},
         "gmres": {"iterations": its[-1], "relres_true": reps[-1]["relres_true"],
                   "time_to_tol_ms": 1e3 * t_max / args.steps, "history": reps[-1]["history"]},
-        "pinv": {"applies_per_s": 1.0 / pinv_s, "ms": 1e3 * pinv_s,
-                 "effective_GBps": 16.0 * unknowns / pinv_s / 1e9,
-                 "structured_GBps": pinv_gbps_structured,
-                 "structured_frac": pinv_gbps_structured / peak},
-        "matvec": {"ms": 1e3 * mv_s, "GBps": mv_gbps, "frac": mv_gbps / peak},
+        "pinv": pinv_d,
+        "matvec": mv_d,
         "stream_copy_GBps": copy_best,
+        "compute_ceilings": ceilings,
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic[0],
                      "traffic_launch": {"algo_bytes": traffic[1], "which": traffic[2]},
@@ -370,21 +370,154 @@ def run_gpu(args, rank, world, local):
                      "frac_of_same_run_copy": achieved / copy_best if copy_best else None},
         "kernels": kernels,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_value, "unit": "GMRES solves/s (host buffers, pinned)",
-                "streams": ne, "single_stream_value": e2e_single,
-                "method": (f"cnpint_gmres_host on {ne} handles (own CUDA stream and workspace each) driven by "
-                           f"{ne} host threads; each solve copies its b in and its u out inside the timed "
-                           f"region; wall clock"),
-                "h2d_bytes_per_step": int(w.unknowns * 8), "d2h_bytes_per_step": int(w.unknowns * 8),
-                "wall_s": e2e_wall},
+        "e2e": e2e,
         "clocks": clk,
     }
+    del s, b
+    torch.cuda.empty_cache()
+    if not args.no_table:
+        result["workloads"] = workload_table(args, peak, stream)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(w)
     return result
 
 
+def run_e2e(s, w, stream, bnp, unp, ne, steps, world):
+    """E2E through cnpint_gmres_host: ne handles (own CUDA stream and workspace each) driven by ne host
+    threads, so one solve's PCIe copies overlap another's kernels; ne = 1 at the headline (a second
+    100-GB workspace does not fit).  value = solves / wall time."""
+    import threading
+
+    import numpy as np
+    import torch
+
+    from paper_2401_16113_b200 import problems
+    s.gmres_host(bnp, w.tol, w.restart, u=unp)   # warm-up
+    torch.cuda.synchronize()
+    handles = [(s, stream, bnp, unp)]
+    for _ in range(ne - 1):
+        st_i = torch.cuda.Stream()
+        with torch.cuda.stream(st_i):
+            s_i = problems.make_solver(w, restart_max=w.restart)
+        bh_i = torch.empty(bnp.shape, dtype=torch.float64, pin_memory=True)
+        bh_i.copy_(torch.from_numpy(bnp))
+        uh_i = torch.empty(bnp.shape, dtype=torch.float64, pin_memory=True)
+        handles.append((s_i, st_i, bh_i.numpy(), uh_i.numpy()))
+    counts = [steps // ne + (1 if i < steps % ne else 0) for i in range(ne)]
+    reps = [None] * ne
+
+    def drive(i):
+        s_i, st_i, b_i, u_i = handles[i]
+        with torch.cuda.stream(st_i):
+            for _ in range(counts[i]):
+                _, reps[i] = s_i.gmres_host(b_i, w.tol, w.restart, u=u_i)
+
+    for i in range(1, ne):
+        s_i, st_i, b_i, u_i = handles[i]
+        with torch.cuda.stream(st_i):
+            s_i.gmres_host(b_i, w.tol, w.restart, u=u_i)
+    torch.cuda.synchronize()
+    barrier(world)
+    h1 = time.perf_counter()
+    if ne == 1:
+        drive(0)
+    else:
+        threads = [threading.Thread(target=drive, args=(i,)) for i in range(ne)]
+        for t_ in threads:
+            t_.start()
+        for t_ in threads:
+            t_.join()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - h1
+    assert all(r is None or r["converged"] for r in reps)
+    assert all(np.array_equal(handles[i][3], unp) for i in range(1, ne))
+    del handles
+    return {"value": whole_job_throughput(steps, max(wall, 1e-12), world), "unit": UNIT, "streams": ne,
+            "method": (f"cnpint_gmres_host on {ne} handle(s) (own CUDA stream and workspace each) driven by "
+                       f"{ne} host thread(s); each solve copies its b in and its u out inside the timed region "
+                       f"(pinned host buffers); wall clock"),
+            "h2d_bytes_per_step": int(w.unknowns * 8), "d2h_bytes_per_step": int(w.unknowns * 8),
+            "wall_s": wall}
+
+
+def workload_table(args, peak, stream):
+    """Every other BASELINE config in the same run: GMRES time-to-tol (5 solves, CUDA events), P⁻¹
+    applies/s and structured GB/s, matvec GB/s, kernel breakdown of one solve."""
+    import torch
+
+    from paper_2401_16113_b200 import problems
+    rows = []
+    for name, alpha in TABLE:
+        w = workload(name, alpha)
+        s = problems.make_solver(w, restart_max=w.restart)
+        b = problems.rhs(w, s)
+        u = s.empty()
+        for _ in range(3):
+            s.gmres(b, u, w.tol, w.restart)
+        torch.cuda.synchronize()
+        nrep = 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(nrep):
+            rep = s.gmres(b, u, w.tol, w.restart)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3 / nrep
+        s.profile_enable(True)
+        s.gmres(b, u, w.tol, w.restart)
+        prof = s.profile_read()
+        s.profile_enable(False)
+        pinv_s, mv_s = time_ops(s, w, stream, 4 if w.unknowns < 1e8 else 2, 10)
+        pd, md = op_rates(w, pinv_s, mv_s, peak)
+        rows.append({"workload": w.name, "alpha": w.alpha, "N": w.N, "m": w.m, "unknowns": w.unknowns,
+                     "iterations": rep["iterations"], "relres_true": rep["relres_true"],
+                     "time_to_tol_ms": 1e3 * t, "solves_per_s": 1.0 / t,
+                     "pinv_applies_per_s": pd["applies_per_s"], "pinv_structured_GBps": pd["structured_GBps"],
+                     "pinv_structured_frac": pd["structured_frac"], "matvec_GBps": md["GBps"],
+                     "matvec_frac": md["frac"],
+                     "kernels_us": {k: {"us_per_launch": 1e3 * ms / cnt, "launches": cnt,
+                                        "frac": (by / (ms * 1e-3) / 1e9 / peak) if by else None}
+                                    for k, (ms, cnt, by) in prof.items()}})
+        del s, b, u
+        torch.cuda.empty_cache()
+    return rows
+
+
 # ----------------------------------------------------------------------------------- CPU oracle
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return sorted({(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()})
+    except Exception:
+        return None
+
+
+def time_slab(w, n_slab=32):
+    """The bounded sample of a workload: the same operator, mesh, τ, α and GMRES settings on the first
+    n_slab of its N time steps (T scaled so τ is unchanged).  A solve's oracle work is linear in N up to
+    the FFT's log factor, so (N / n_slab) × the sample's time ≈ (slightly under) the full solve's."""
+    if w.N <= n_slab:
+        return w, 1.0
+    return w.with_(name=f"{w.name}_slab{n_slab}", N=n_slab, T=w.T * n_slab / w.N), w.N / n_slab
+
+
 def oracle_solve(w):
     from oracle import aao, gmres, precond, problem
     op = problem.build_operator(w)
@@ -395,46 +528,67 @@ def oracle_solve(w):
     return time.perf_counter() - t0, rep
 
 
-def cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count()
-
-
 def cpu_baseline(w):
-    dt, rep = oracle_solve(w)
-    return {"value": 1.0 / dt, "unit": "GMRES solves/s", "cores": cores(), "kind": "oracle",
-            "sample": f"1 full oracle GMRES({w.restart}) solve of {w.name} (numpy FFT + vectorised Thomas, MGS),"
-                      f" {rep.iterations} its, {dt:.1f} s",
-            "threads_note": "numpy/BLAS default threading (FFT and Thomas single-threaded)"}
+    """The oracle as it stands on the host cores: one GMRES solve of the bounded sample (time_slab),
+    scaled to the full workload, plus the oracle's 𝓜u (median of 3) and P⁻¹ (once; ~30-60 s at the
+    headline size) on full-size vectors (the per-operation baseline SURVEY.md §8(d) asks for)."""
+    import numpy as np
+
+    import synth
+    from oracle import aao, precond, problem
+    ws, scale = time_slab(w)
+    dt, rep = oracle_solve(ws)
+    res = {"value": 1.0 / (dt * scale), "unit": UNIT, "cores": cores(), "kind": "oracle",
+           "cpu_model": cpu_model(), "blas_threads": str(blas_threads()),
+           "sample": (f"1 oracle GMRES({ws.restart}) solve of {ws.name} (the headline operator, mesh, tau, alpha "
+                      f"on {ws.N} of its {w.N} time steps; numpy FFT + dense-DST / Thomas shifted solves, "
+                      f"MGS), {rep.iterations} its, {dt:.1f} s, scaled x{scale:g} to the full workload")}
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 1)[0]
+    tm = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        aao.apply_M(w, op, v)
+        tm.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    precond.pinv_dft(w, op, v)
+    tp = time.perf_counter() - t0
+    res["per_op_full_size"] = {"apply_M_s_median_of_3": float(np.median(tm)), "apply_Pinv_s_1_run": tp,
+                               "workload": w.name, "unknowns": w.unknowns}
+    return res
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle (oracle/, numpy) on the GPU arm's workload, metric and unit —
+    each step one oracle GMRES solve of the bounded sample (time_slab), scaled to the full workload
+    (steps and warm-up exactly as given); rank 0 only."""
     if rank != 0:
         return None
     w = workload(args.workload, args.alpha)
-    for _ in range(min(args.warmup, 1)):
-        oracle_solve(w)
+    ws, scale = time_slab(w)
+    for _ in range(args.warmup):
+        oracle_solve(ws)
     times, its = [], []
-    budget = 150.0  # seconds: keep the reference arm within a few minutes (each solve ~20 s at c2)
     for _ in range(args.steps):
-        dt, rep = oracle_solve(w)
-        times.append(dt)
+        dt, rep = oracle_solve(ws)
+        times.append(dt * scale)
         its.append(rep.iterations)
-        if sum(times) > budget:
-            break
     tot = sum(times)
-    args.steps = len(times)
     v = args.steps / tot
-    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "GMRES solves/s (time-to-tol^-1, whole job)",
-            "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot / args.steps,
+    sample = (f"each step: 1 oracle GMRES({ws.restart}) solve of {ws.name} ({ws.N} of the {w.N} time steps, "
+              f"same operator/mesh/tau/alpha), its time x{scale:g}")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": describe(w), "N": w.N, "m": w.m, "alpha": w.alpha},
+            "data": "synthetic (manufactured-solution rhs)",
+            "config": {"workload": describe(w), "name": w.name, "N": w.N, "m": w.m, "alpha": w.alpha,
+                       "restart": w.restart, "tol": w.tol,
+                       "parallelism": f"replicas x{world} (no data-path collective)",
+                       "l2": "n/a (CPU)"},
             "gmres": {"iterations": its[-1]},
-            "cpu_baseline": {"value": v, "unit": "GMRES solves/s", "cores": cores(), "kind": "oracle",
-                             "sample": f"{args.steps} full oracle GMRES solves of {w.name}"},
-            "e2e": {"value": v, "unit": "GMRES solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores(), "kind": "oracle", "cpu_model": cpu_model(),
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def main(argv=None):
@@ -443,10 +597,12 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cnpint", choices=["cnpint", "reference"])
-    ap.add_argument("--workload", default="c2")
-    ap.add_argument("--alpha", type=float, default=0.01)
+    ap.add_argument("--workload", default=HEADLINE)
+    ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-streams", type=int, default=4, help="concurrent handles for the e2e measurement")
+    ap.add_argument("--no-table", action="store_true", help="skip the per-workload table")
+    ap.add_argument("--e2e-streams", type=int, default=0,
+                    help="concurrent handles for the e2e measurement (0: 1 at > 1e8 unknowns, else 4)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "cnpint":
         args.warmup = 3  # timing rule: at least 3 warm-up steps

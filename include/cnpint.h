@@ -214,6 +214,21 @@ const char* cnpint_kernel_name(int kernel_class);
  * bandwidth reference.  Enqueued on cuda_stream. */
 cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, void* cuda_stream);
 
+/* Test hook (orthogonality measurements of the Arnoldi basis, K7): vector i of the LAST
+ * restart cycle of the most recent cnpint_gmres call, v_i = s_i·Ṽ_i with 0 <= i < *count (count may
+ * be read with i = 0 even when the call fails).  *d_vec = Ṽ_i (device, the vector layout above; the
+ * first cycle's Ṽ_0 is the caller's b; valid until the next call on the handle), *scale = s_i (host
+ * copy; synchronises the stream).  Any out pointer may be NULL.  EINVAL for i out of range. */
+cnpint_status cnpint_krylov_basis(cnpint_ctx* ctx, int i, const double** d_vec, double* scale, int* count);
+
+/* Same-run compute ceilings: enqueues on cuda_stream a kernel of 8 CTAs x 256
+ * threads per SM doing `iters` rounds of dependent fp64 FMAs (kind 0, 8 chains per thread) or of
+ * mma.sync.m8n8k4 f64 DMMA (kind 1, 4 accumulators per warp).  d_out: device scratch of
+ * >= 8·SMs·256 doubles (one result per thread, so no work is eliminated).  *flops = the floating-point
+ * operations one launch performs (FMA = 2; one m8n8k4 = 512); the caller times the launch with
+ * events on the same stream.  EINVAL for bad arguments, ECUDA on launch failure. */
+cnpint_status cnpint_peak_kernel(int kind, double* d_out, int iters, void* cuda_stream, double* flops);
+
 /* Test hook (negative controls): 0 = none, 1 = flip the sign of the FFT twiddles,
  * 2 = use the printed Eq. eigCx ordering λ1_k = 1 − a e^{+2πik/N} (R3).
  * The parity suite must fail with either set.  Kernel-variant bits (not negative controls; the

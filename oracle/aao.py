@@ -91,10 +91,23 @@ def spatial_sparse(op) -> sp.csr_matrix:
 
 
 class Q1Solver:
-    """Solves Q1 x = r = (I − ½τL_h) x = r.  1D: banded LU (solve_banded); 2D: sparse LU."""
+    """Solves Q1 x = r = (I − ½τL_h) x = r.  1D: banded LU (solve_banded); 2D: sparse LU, or for
+    n ≥ dst_min the fast diagonalisation with dense DST-I matrices:
+    L_h = W diag(μ) W⁻¹, W = (D_yS) ⊗ (D_xS), so x = W[(1 − ½τμ)⁻¹ ∘ (W⁻¹r)] — four dense n×n
+    products per solve instead of sparse triangular solves with nested fill (pinned against the
+    sparse LU in tests/test_oracle_pins.py)."""
 
-    def __init__(self, op, tau):
+    def __init__(self, op, tau, dst_min: int = 256):
         self.op, self.tau = op, tau
+        self.dst = None
+        if not isinstance(op, Operator1D) and op.n >= dst_min:
+            from .precond import dst1_matrix, toeplitz_eig
+            S = dst1_matrix(op.n)
+            Dx, ex = toeplitz_eig(op.n, op.xs, op.xd, op.xu)
+            Dy, ey = toeplitz_eig(op.n, op.ys, op.yd, op.yu)
+            mu = ey[:, None] + ex[None, :] + op.shift        # eigenvalues of L_h, [y][x]
+            self.dst = (S, Dx, Dy, 1.0 / (1.0 - 0.5 * tau * mu))
+            return
         if isinstance(op, Operator1D):
             m = op.m
             ab = np.zeros((3, m))
@@ -108,6 +121,12 @@ class Q1Solver:
             self.lu = spla.splu(Q.tocsc())
 
     def __call__(self, r: np.ndarray) -> np.ndarray:
+        if self.dst is not None:
+            S, Dx, Dy, inv = self.dst
+            n = self.op.n
+            R = r.reshape(n, n)
+            Rh = S @ ((R / Dy[:, None]) / Dx[None, :]) @ S        # W⁻¹ r
+            return (Dy[:, None] * (S @ (inv * Rh) @ S) * Dx[None, :]).reshape(r.shape)   # W (…)
         if self.lu is None:
             return sla.solve_banded((1, 1), self.ab, r)
         shp = r.shape

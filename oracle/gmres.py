@@ -31,12 +31,15 @@ class GmresReport:
 
 
 def gmres_right(A, Pinv, b: np.ndarray, tol: float, restart: int, maxit: int = 1000,
-                reorth: bool = True):
+                reorth: bool = True, iterates: list | None = None):
     """Right-preconditioned restarted GMRES(restart) with x0 = 0.
 
     A, Pinv: callables on arrays shaped like b.  Returns (u, GmresReport).  If maxit is reached
     inside a cycle, the cycle is closed (u updated) and the report says converged=False — so
-    gmres_right(..., maxit=j) returns the j-th GMRES iterate for j ≤ restart."""
+    gmres_right(..., maxit=j) returns the j-th GMRES iterate for j ≤ restart.
+    iterates (test mode): if a list is given, the iterate
+    x_j = u0 + P⁻¹V_j y_j of every inner step j is formed (one extra P⁻¹ per step, by the same
+    back substitution as the cycle end) and appended — the same vectors maxit=j would return."""
     shape = b.shape
     bv = b.reshape(-1)
     bnorm = float(np.linalg.norm(bv))
@@ -48,9 +51,22 @@ def gmres_right(A, Pinv, b: np.ndarray, tol: float, restart: int, maxit: int = 1
     Af = lambda x: A(x.reshape(shape)).reshape(-1)
     Pf = lambda x: Pinv(x.reshape(shape)).reshape(-1)
     r = bv.copy()                      # x0 = 0 ⇒ r0 = b
+
+    def backsolve(H, g, k):                             # y = H[:k,:k]⁻¹ g[:k] (upper triangular)
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+        return y
+
+    def combine(V, y):                                  # V_k y, basis rows kept as a list
+        s = np.zeros_like(bv)
+        for i in range(y.size):
+            s += y[i] * V[i]
+        return s
+
     while True:
         beta = float(np.linalg.norm(r))
-        V = np.zeros((restart + 1, bv.size))
+        V = [None] * (restart + 1)                      # basis vectors (allocated as produced)
         H = np.zeros((restart + 1, restart))
         cs = np.zeros(restart)
         sn = np.zeros(restart)
@@ -87,12 +103,12 @@ def gmres_right(A, Pinv, b: np.ndarray, tol: float, restart: int, maxit: int = 1
             est = abs(g[j + 1]) / bnorm
             rep.history.append(est)
             j_done = j + 1
+            if iterates is not None:
+                iterates.append((u + Pf(combine(V, backsolve(H, g, j_done)))).reshape(shape))
             if est <= tol or breakdown or rep.iterations >= maxit:
                 break
-        y = np.zeros(j_done)                             # back substitution H y = g
-        for i in range(j_done - 1, -1, -1):
-            y[i] = (g[i] - H[i, i + 1:j_done] @ y[i + 1:j_done]) / H[i, i]
-        u = u + Pf(V[:j_done].T @ y)                     # u = u0 + P⁻¹ V y
+        y = backsolve(H, g, j_done)                      # back substitution H y = g
+        u = u + Pf(combine(V, y))                        # u = u0 + P⁻¹ V y
         r = bv - Af(u)
         rep.relres_est = est
         rep.relres_true = float(np.linalg.norm(r)) / bnorm

@@ -107,12 +107,15 @@ def dst1_matrix(n: int) -> np.ndarray:
 
 def toeplitz_eig(n: int, s: float, d: float, u: float):
     """Eigen-decomposition of tridiag(s, d, u) (s·u > 0): L = (D S) diag(e) (S D⁻¹) with
-    D = diag(ρ^i), ρ = √(s/u), e_j = d + 2√(s u) cos(jπ/(n+1)) (the similarity D⁻¹ L D is the
-    symmetric Toeplitz tridiag(√(su), d, √(su)) diagonalised by DST-I)."""
+    D = diag(ρ^i), ρ = √(s/u), e_j = d + 2σ cos(jπ/(n+1)), σ = sgn(s)·√(s u): the similarity
+    D⁻¹ L D has off-diagonals s/ρ = uρ = σ, i.e. it is the symmetric Toeplitz tridiag(σ, d, σ),
+    diagonalised by DST-I.  For s, u < 0 the sign matters: without it mode j
+    would carry the eigenvalue of mode n+1−j."""
     assert s * u > 0
     rho = math.sqrt(s / u)
+    sigma = math.copysign(math.sqrt(s * u), s)
     Dg = rho ** np.arange(1, n + 1)
-    e = d + 2.0 * math.sqrt(s * u) * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
+    e = d + 2.0 * sigma * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
     return Dg, e
 
 

@@ -28,7 +28,8 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_apply_Pinv", "cnpint_time_fft", "cnpint_shifted_solve", "cnpint_time_ifft", "cnpint_gmres",
            "cnpint_apply_Pinv_host", "cnpint_apply_A_host", "cnpint_gmres_host", "cnpint_device_status",
            "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug", "cnpint_profile_enable",
-           "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence", "cnpint_gmres_left"]
+           "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence", "cnpint_gmres_left",
+           "cnpint_krylov_basis", "cnpint_peak_kernel"]
 
 
 class CnpintError(RuntimeError):
@@ -84,6 +85,8 @@ def load_library(path: str = LIB_PATH):
         "cnpint_profile_read": (C.c_int, [vp, C.c_int, dp, C.POINTER(C.c_int64), dp]),
         "cnpint_kernel_name": (C.c_char_p, [C.c_int]),
         "cnpint_set_time_dependence": (C.c_int, [vp, dp]),
+        "cnpint_krylov_basis": (C.c_int, [vp, C.c_int, C.POINTER(C.c_void_p), dp, C.POINTER(C.c_int)]),
+        "cnpint_peak_kernel": (C.c_int, [C.c_int, vp, C.c_int, vp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -97,9 +100,9 @@ def _ptr(t) -> int:
     return int(t.data_ptr())
 
 
-def _stream():
+def _stream(device=None):
     import torch
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 @dataclass
@@ -141,7 +144,11 @@ class Solver:
             raise RuntimeError("cnpint needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
         self.N, self.T, self.alpha, self.op, self.restart_max = N, T, alpha, op, restart_max
-        self.device = torch.device("cuda") if device is None else torch.device(device)
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if dev.type != "cuda":
+            raise ValueError(f"cnpint needs a CUDA device, got {dev}")
+        # a concrete index: the handle lives on one device (its stream, workspace and kernel attributes)
+        self.device = torch.device("cuda", torch.cuda.current_device() if dev.index is None else dev.index)
         cop, self._keep = op.to_c()
         nbytes = self.lib.cnpint_workspace_bytes(N, C.byref(cop), restart_max)
         if nbytes == 0:
@@ -150,8 +157,9 @@ class Solver:
         base = _ptr(self.workspace)
         aligned = (base + 255) // 256 * 256
         h = C.c_void_p()
-        st = self.lib.cnpint_create(C.byref(h), N, T, alpha, C.byref(cop), restart_max, C.c_void_p(aligned),
-                                    nbytes, _stream())
+        with torch.cuda.device(self.device):
+            st = self.lib.cnpint_create(C.byref(h), N, T, alpha, C.byref(cop), restart_max, C.c_void_p(aligned),
+                                        nbytes, _stream(self.device))
         if st != OK:
             raise CnpintError(st, "cnpint_create failed")
         self.h = h
@@ -174,7 +182,55 @@ class Solver:
             raise CnpintError(st, f"{what}: {msg.decode() if msg else ''}")
 
     def _sync_stream(self):
-        self.lib.cnpint_set_stream(self.h, _stream())
+        self.lib.cnpint_set_stream(self.h, _stream(self.device))
+
+    def _on_device(self):
+        """Every ABI call runs with the handle's device current (kernels launch on its stream)."""
+        import torch
+        return torch.cuda.device(self.device)
+
+    def _dev(self, t, name: str, elems: int):
+        """Device pointer of t after checking what the C side cannot: a contiguous float64 CUDA
+        tensor on the handle's device holding at least `elems` doubles (the padded layout)."""
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+        if t.dtype != torch.float64:
+            raise CnpintError(EINVAL, f"{name} must be float64, got {t.dtype}")
+        if t.device != self.device:
+            raise CnpintError(EINVAL, f"{name} is on {t.device}, the handle on {self.device}")
+        if not t.is_contiguous():
+            raise CnpintError(EINVAL, f"{name} must be contiguous")
+        if t.numel() < elems:
+            raise CnpintError(EINVAL, f"{name} holds {t.numel()} doubles < {elems} (padded shape "
+                                      f"{self.padded_shape})")
+        return C.c_void_p(_ptr(t))
+
+    def _vec(self, t, name: str):
+        return self._dev(t, name, self.vec_elems)
+
+    def _spec(self, t, name: str):
+        return self._dev(t, name, 2 * self.spec_elems)
+
+    def _host_in(self, a, name: str) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.shape != self.host_shape:
+            raise CnpintError(EINVAL, f"{name} has shape {a.shape}, expected {self.host_shape}")
+        return a
+
+    def _host_out(self, a, name: str) -> np.ndarray:
+        if a is None:
+            return np.empty(self.host_shape, dtype=np.float64)
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.shape != self.host_shape \
+                or not a.flags.c_contiguous or not a.flags.writeable:
+            raise CnpintError(EINVAL, f"{name} must be a writeable C-contiguous float64 array of shape "
+                                      f"{self.host_shape}")
+        return a
+
+    @property
+    def host_shape(self):
+        """Packed host layout of the *_host calls: (N, nx) in 1D, (N, ny, nx) in 2D."""
+        return (self.N, self.nx) if self.op.dim == 1 else (self.N, self.ny, self.nx)
 
     @property
     def padded_shape(self):
@@ -200,29 +256,40 @@ class Solver:
 
     # ---------------------------------------------------------------- ABI calls
     def apply_A(self, u, y):
-        self._sync_stream()
-        self._check(self.lib.cnpint_apply_A(self.h, C.c_void_p(_ptr(u)), C.c_void_p(_ptr(y))), "apply_A")
+        pa, pb = self._vec(u, "u"), self._vec(y, "y")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_apply_A(self.h, pa, pb), "apply_A")
 
     def apply_P(self, z, v):
-        self._sync_stream()
-        self._check(self.lib.cnpint_apply_P(self.h, C.c_void_p(_ptr(z)), C.c_void_p(_ptr(v))), "apply_P")
+        pa, pb = self._vec(z, "z"), self._vec(v, "v")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_apply_P(self.h, pa, pb), "apply_P")
 
     def apply_Pinv(self, v, z):
-        self._sync_stream()
-        self._check(self.lib.cnpint_apply_Pinv(self.h, C.c_void_p(_ptr(v)), C.c_void_p(_ptr(z))), "apply_Pinv")
+        pa, pb = self._vec(v, "v"), self._vec(z, "z")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_apply_Pinv(self.h, pa, pb), "apply_Pinv")
 
     def time_fft(self, v, what):
-        self._sync_stream()
-        self._check(self.lib.cnpint_time_fft(self.h, C.c_void_p(_ptr(v)), C.c_void_p(_ptr(what))), "time_fft")
+        pa, pb = self._vec(v, "v"), self._spec(what, "what")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_time_fft(self.h, pa, pb), "time_fft")
 
     def shifted_solve(self, what, zhat):
-        self._sync_stream()
-        self._check(self.lib.cnpint_shifted_solve(self.h, C.c_void_p(_ptr(what)), C.c_void_p(_ptr(zhat))),
-                    "shifted_solve")
+        pa, pb = self._spec(what, "what"), self._spec(zhat, "zhat")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_shifted_solve(self.h, pa, pb), "shifted_solve")
 
     def time_ifft(self, zhat, z):
-        self._sync_stream()
-        self._check(self.lib.cnpint_time_ifft(self.h, C.c_void_p(_ptr(zhat)), C.c_void_p(_ptr(z))), "time_ifft")
+        pa, pb = self._spec(zhat, "zhat"), self._vec(z, "z")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_time_ifft(self.h, pa, pb), "time_ifft")
 
     def gmres(self, b, u, tol: float, restart: int, maxit: int = 1000, history_cap: int = 1000,
               side: str = "right"):
@@ -230,11 +297,13 @@ class Solver:
         §4 / Theorem 4.5 setting; the report adds relres_prec = ||P⁻¹(b − 𝓜u)||/||P⁻¹b||)."""
         if side not in ("right", "left"):
             raise ValueError(f"side must be 'right' or 'left', got {side!r}")
-        self._sync_stream()
+        pb, pu = self._vec(b, "b"), self._vec(u, "u")
         hist = (C.c_double * history_cap)()
         rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, C.cast(hist, C.POINTER(C.c_double)), history_cap, float("nan"))
         fn = self.lib.cnpint_gmres if side == "right" else self.lib.cnpint_gmres_left
-        st = fn(self.h, C.c_void_p(_ptr(b)), C.c_void_p(_ptr(u)), tol, restart, maxit, C.byref(rep))
+        with self._on_device():
+            self._sync_stream()
+            st = fn(self.h, pb, pu, tol, restart, maxit, C.byref(rep))
         if st not in (OK, ENOCONV):
             self._check(st, "gmres" if side == "right" else "gmres_left")
         out = {"status": STATUS[st], "iterations": rep.iterations, "restarts": rep.restarts,
@@ -246,43 +315,49 @@ class Solver:
 
     # host-buffer (end-to-end) variants: packed numpy arrays
     def apply_Pinv_host(self, v: np.ndarray, z: Optional[np.ndarray] = None) -> np.ndarray:
-        v = np.ascontiguousarray(v, dtype=np.float64)
-        z = np.empty_like(v) if z is None else z
-        self._sync_stream()
-        self._check(self.lib.cnpint_apply_Pinv_host(self.h, v.ctypes.data_as(C.POINTER(C.c_double)),
-                                                    z.ctypes.data_as(C.POINTER(C.c_double))), "apply_Pinv_host")
+        v = self._host_in(v, "v")
+        z = self._host_out(z, "z")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_apply_Pinv_host(self.h, v.ctypes.data_as(C.POINTER(C.c_double)),
+                                                        z.ctypes.data_as(C.POINTER(C.c_double))), "apply_Pinv_host")
         return z
 
     def apply_A_host(self, u: np.ndarray, y: Optional[np.ndarray] = None) -> np.ndarray:
-        u = np.ascontiguousarray(u, dtype=np.float64)
-        y = np.empty_like(u) if y is None else y
-        self._sync_stream()
-        self._check(self.lib.cnpint_apply_A_host(self.h, u.ctypes.data_as(C.POINTER(C.c_double)),
-                                                 y.ctypes.data_as(C.POINTER(C.c_double))), "apply_A_host")
+        u = self._host_in(u, "u")
+        y = self._host_out(y, "y")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_apply_A_host(self.h, u.ctypes.data_as(C.POINTER(C.c_double)),
+                                                     y.ctypes.data_as(C.POINTER(C.c_double))), "apply_A_host")
         return y
 
     def gmres_host(self, b: np.ndarray, tol: float, restart: int, maxit: int = 1000, u: Optional[np.ndarray] = None):
-        b = np.ascontiguousarray(b, dtype=np.float64)
-        u = np.empty_like(b) if u is None else u
-        self._sync_stream()
+        b = self._host_in(b, "b")
+        u = self._host_out(u, "u")
         rep = GmresReport(0, 0, 0, 0.0, 0.0, 0.0, None, 0, float("nan"))
-        st = self.lib.cnpint_gmres_host(self.h, b.ctypes.data_as(C.POINTER(C.c_double)),
-                                        u.ctypes.data_as(C.POINTER(C.c_double)), tol, restart, maxit, C.byref(rep))
+        with self._on_device():
+            self._sync_stream()
+            st = self.lib.cnpint_gmres_host(self.h, b.ctypes.data_as(C.POINTER(C.c_double)),
+                                            u.ctypes.data_as(C.POINTER(C.c_double)), tol, restart, maxit,
+                                            C.byref(rep))
         if st not in (OK, ENOCONV):
             self._check(st, "gmres_host")
         return u, {"status": STATUS[st], "iterations": rep.iterations, "converged": bool(rep.converged),
                    "relres_true": rep.relres_true, "seconds": rep.seconds}
 
     def device_status(self) -> int:
-        self._sync_stream()
-        return int(self.lib.cnpint_device_status(self.h))
+        with self._on_device():
+            self._sync_stream()
+            return int(self.lib.cnpint_device_status(self.h))
 
     def launch_count(self) -> int:
         return int(self.lib.cnpint_launch_count(self.h))
 
     def profile_enable(self, on: bool = True):
-        self._sync_stream()
-        self._check(self.lib.cnpint_profile_enable(self.h, int(on)), "profile_enable")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_profile_enable(self.h, int(on)), "profile_enable")
 
     def profile_read(self):
         """{kernel class: (ms_total, launches, algorithmic_bytes)} for classes with launches."""
@@ -302,19 +377,53 @@ class Solver:
 
     def set_time_dependence(self, d_half: Optional[np.ndarray]):
         """𝓛(t) = d(t)𝓛 with the N values d(t_{t+½}) (None: constant operator)."""
-        self._sync_stream()
-        if d_half is None:
-            self._check(self.lib.cnpint_set_time_dependence(self.h, None), "set_time_dependence")
-            return
-        d = np.ascontiguousarray(d_half, dtype=np.float64)
-        if d.shape != (self.N,):
-            raise CnpintError(EINVAL, f"d_half must have shape ({self.N},)")
-        self._check(self.lib.cnpint_set_time_dependence(self.h, d.ctypes.data_as(C.POINTER(C.c_double))),
-                    "set_time_dependence")
+        d = None
+        if d_half is not None:
+            d = np.ascontiguousarray(d_half, dtype=np.float64)
+            if d.shape != (self.N,):
+                raise CnpintError(EINVAL, f"d_half must have shape ({self.N},)")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_set_time_dependence(
+                self.h, None if d is None else d.ctypes.data_as(C.POINTER(C.c_double))), "set_time_dependence")
+
+    def krylov_basis(self):
+        """The last GMRES cycle's basis as (list of torch views Ṽ_i, list of scales s_i), v_i = s_iṼ_i
+        (test hook for orthogonality measurements; the views alias the workspace / the caller's b)."""
+        import torch
+        cnt = C.c_int(0)
+        with self._on_device():
+            self._sync_stream()
+            self.lib.cnpint_krylov_basis(self.h, 0, None, None, C.byref(cnt))
+            vecs, scales = [], []
+            for i in range(cnt.value):
+                p, s = C.c_void_p(), C.c_double()
+                self._check(self.lib.cnpint_krylov_basis(self.h, i, C.byref(p), C.byref(s), None), "krylov_basis")
+                base = _ptr(self.workspace)
+                if p.value >= base and p.value < base + self.workspace.numel():
+                    off = (p.value - base) // 8
+                    ws = self.workspace.view(torch.float64) if (base % 8 == 0) else None
+                    vecs.append(ws[off:off + self.vec_elems].view(self.padded_shape))
+                else:
+                    vecs.append(None)   # the caller's b (first cycle): the caller holds it
+                scales.append(s.value)
+        return vecs, scales
 
     def set_debug(self, flags: int):
-        self._sync_stream()
-        self._check(self.lib.cnpint_set_debug(self.h, flags), "set_debug")
+        with self._on_device():
+            self._sync_stream()
+            self._check(self.lib.cnpint_set_debug(self.h, flags), "set_debug")
+
+
+def peak_kernel(kind: int, out, iters: int) -> float:
+    """Enqueue the fp64 FMA (kind 0) / DMMA (kind 1) ceiling kernel on torch's current stream; returns
+    the flops of the launch (the caller times it with CUDA events)."""
+    lib = load_library()
+    fl = C.c_double()
+    st = lib.cnpint_peak_kernel(kind, C.c_void_p(_ptr(out)), iters, _stream(), C.byref(fl))
+    if st != OK:
+        raise CnpintError(st, "peak_kernel")
+    return fl.value
 
 
 def stream_copy(src, dst):

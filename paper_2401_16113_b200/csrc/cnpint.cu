@@ -10,7 +10,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "internal.h"
@@ -62,6 +65,27 @@ static void prof_free(cnpint_ctx* c) {
   delete p;
   c->prof = nullptr;
 }
+// ------------------------------------------------------------------------------ per-device cache
+static std::mutex g_cache_mu;
+static std::map<std::pair<const void*, int>, int> g_cache;
+
+bool cnp_dev_cache_get(const void* key, int* val) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.find({key, dev});
+  if (it == g_cache.end()) return false;
+  *val = it->second;
+  return true;
+}
+
+void cnp_dev_cache_put(const void* key, int val) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache[{key, dev}] = val;
+}
+
 cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out);
 cudaError_t launch_dst_x_acc(cnpint_ctx* c, const double* in, double* out);
 
@@ -338,8 +362,10 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
     auto axis = [&](int n, double s, double d, double u, size_t offi, size_t offd, size_t offe, size_t offtw,
                     int64_t elen) {
       std::vector<double> Di(n), Dd(n), e(elen, 0.0);
+      // D⁻¹ tridiag(s, d, u) D with D = diag(ρ^j), ρ = √(s/u) is the symmetric Toeplitz
+      // tridiag(σ, d, σ), σ = sgn(s)·√(su) (s·u > 0): eigenvalues d + 2σ cos(jπ/(n+1)), DST-I modes
       long double rho = sqrtl((long double)s / (long double)u);
-      long double sq = sqrtl((long double)s * (long double)u);
+      long double sq = (s < 0.0 ? -1.0L : 1.0L) * sqrtl((long double)s * (long double)u);
       for (int j = 1; j <= n; ++j) {
         Di[j - 1] = (double)powl(rho, -(long double)j);
         Dd[j - 1] = (double)(powl(rho, (long double)j) * 2.0L / (long double)(n + 1));
@@ -817,13 +843,20 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
           if (rep) { rep->iterations = 0; rep->restarts = 0; rep->converged = 1; rep->relres_est = 0; rep->relres_true = 0; }
           return CNPINT_OK;
         }
-        if (!std::isfinite(h[0])) { seterr(c, "gmres: ||b|| not finite"); return CNPINT_EBREAKDOWN; }
+        if (!std::isfinite(h[0])) {
+          if (cnpint_status ds = cnpint_device_status(c)) return ds;
+          seterr(c, "gmres: ||b|| not finite");
+          return CNPINT_EBREAKDOWN;
+        }
       }
       ++its;
       jdone = j + 1;
       est = h[1];
       if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
       if (h[3] != 0.0) {
+        // a singular shifted solve (zero / non-finite pivot, e.g. P_1 with a singular variable-row Ã)
+        // poisons P⁻¹ first: report it as such (and clear the status word) before calling it breakdown
+        if (cnpint_status ds = cnpint_device_status(c)) return ds;
         seterr(c, "gmres: non-finite scalar in the Arnoldi process");
         return CNPINT_EBREAKDOWN;
       }
@@ -840,6 +873,8 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
         CK(launch_update(c, Z.data() + g0, ng, c->d_y + g0, 1, fresh ? nullptr : d_u, d_u, 0, 0, c->d_part, nullptr));
       }
     }
+    c->last_v0 = V[0];     // cnpint_krylov_basis (test hook): this cycle's basis
+    c->last_nv = jdone + 1;
     // true residual ‖b − 𝓜u‖: when the estimate says converged only its norm is needed (mode 3, no
     // store); otherwise r is written into the workspace slot of Ṽ_0 for the next cycle (b is kept)
     V[0] = c->d_V;
@@ -928,6 +963,7 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
       est = h[1];
       if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
       if (h[3] != 0.0) {
+        if (cnpint_status ds = cnpint_device_status(c)) return ds;  // singular pivot first (see cnpint_gmres)
         seterr(c, "gmres_left: non-finite scalar in the Arnoldi process");
         return CNPINT_EBREAKDOWN;
       }
@@ -974,6 +1010,18 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
   if (result == CNPINT_ENOCONV)
     seterr(c, "gmres_left: maxit reached (preconditioned relres %.3e > tol %.3e)", relres_prec, tol);
   return result;
+}
+
+cnpint_status cnpint_krylov_basis(cnpint_ctx* c, int i, const double** d_vec, double* scale, int* count) {
+  if (!c) return CNPINT_EINVAL;
+  if (count) *count = c->last_nv;
+  if (i < 0 || i >= c->last_nv || !c->last_v0) { seterr(c, "krylov_basis: no such vector"); return CNPINT_EINVAL; }
+  if (d_vec) *d_vec = i == 0 ? c->last_v0 : c->d_V + (size_t)i * c->vec;
+  if (scale) {
+    CK(cudaMemcpyAsync(scale, c->d_scl + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return CNPINT_OK;
 }
 
 // ------------------------------------------------------------------------------ host variants

@@ -126,6 +126,8 @@ struct cnpint_ctx {
   double* h_pinned;    // mapped pinned host scalars [16]: d_scal[0..7], status at [8]
   double* d_hmap;      // its device alias
   PostOp post;         // pending post-fold operation for the next reducing launch (op 0 = none)
+  const double* last_v0;  // Ṽ_0 of the last completed GMRES cycle (b itself in the first), test hook
+  int last_nv;            // basis vectors Ṽ_0..Ṽ_{last_nv−1} of that cycle
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
   void* prof;          // CnpProf* (host event pools), null when profiling is off
@@ -209,6 +211,19 @@ static inline cudaError_t cnp_launch(const cnpint_ctx* c, void (*k)(KArgs...), d
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 void cnp_prof_begin(cnpint_ctx* c, int kid);
+// Per-(key, CUDA device) cache of a launcher's one-time setup (cudaFuncSetAttribute is per-device
+// state; occupancy-derived grid sizes depend on the device): compute(&v) runs until it succeeds once
+// for the current device, under no lock (it must be idempotent); lookups and stores are mutex-guarded,
+// so handles on several devices and host threads are safe.  key = the kernel's address.
+bool cnp_dev_cache_get(const void* key, int* val);
+void cnp_dev_cache_put(const void* key, int val);
+template <class F>
+static inline cudaError_t cnp_dev_cached(const void* key, int* out, F&& compute) {
+  if (cnp_dev_cache_get(key, out)) return cudaSuccess;
+  cudaError_t e = compute(out);
+  if (e == cudaSuccess) cnp_dev_cache_put(key, *out);
+  return e;
+}
 void cnp_prof_end(cnpint_ctx* c, int kid, double algo_bytes);
 static inline double cnp_units(const cnpint_ctx* c) { return (double)c->N * c->nx * c->ny; }
 static inline double cnp_spec_units(const cnpint_ctx* c) { return (double)(c->H + 1) * c->nx * c->ny; }

@@ -333,15 +333,17 @@ static cudaError_t run_dst_r(cnpint_ctx* c, const double* in, double* out, const
                              int accumulate) {
   using P = DstPlan<LOGE>;
   auto kern = k_dst_r<YPASS, LOGE>;
-  static int grid_max = 0;
-  if (!grid_max) {
+  int grid_max = 0;
+  cudaError_t ce = cnp_dev_cached((const void*)kern, &grid_max, [&](int* v) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::NT, P::bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-    grid_max = per_sm * c->num_sms;
-  }
+    *v = per_sm * c->num_sms;
+    return cudaSuccess;
+  });
+  if (ce != cudaSuccess) return ce;
   const int nlines = c->N * c->ny;
   const int ld = (int)c->ld;
   const int ntiles = YPASS ? c->N * ((ld / 2 + P::NC - 1) / P::NC) : ((nlines + 1) / 2 + P::NC - 1) / P::NC;
@@ -356,15 +358,17 @@ static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const
   constexpr int NC = LOGE == 9 ? DST_NC9 : LOGE < 9 ? 8 : LOGE == 10 ? DST_NC10 : 2;
   using LY = DstLayout<LOGE, NC>;
   auto kern = k_dst<YPASS, LOGE, NC>;
-  static int grid_max = 0;
-  if (!grid_max) {
+  int grid_max = 0;
+  cudaError_t ce = cnp_dev_cached((const void*)kern, &grid_max, [&](int* v) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY::bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, LY::bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-    grid_max = per_sm * c->num_sms;
-  }
+    *v = per_sm * c->num_sms;
+    return cudaSuccess;
+  });
+  if (ce != cudaSuccess) return ce;
   const int n = YPASS ? c->ny : c->nx;
   (void)n;
   const int nlines = c->N * c->ny;

@@ -552,8 +552,7 @@ static void fs_logs(int N, int& l1, int& l2) {
 // items of the three-phase pass are 8–16 KB and the cluster kernel measured faster (c4: 326 vs 781
 // µs, profiles/r01_k6_sweep.txt)
 static int fs_min2d() {  // CNPINT_FS_2D_MIN: tuning experiments only
-  static int v = -1;
-  if (v < 0) v = getenv("CNPINT_FS_2D_MIN") ? atoi(getenv("CNPINT_FS_2D_MIN")) : 2048;
+  static const int v = getenv("CNPINT_FS_2D_MIN") ? atoi(getenv("CNPINT_FS_2D_MIN")) : 2048;
   return v;
 }
 static bool fs_shape_ok(int dim, int N) {
@@ -579,13 +578,15 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
                              const double* vscale, int accumulate) {
   using G = FsGeo<MODE, LOG1, LOG2>;
   auto kern = k_fstep<MODE, LOG1, LOG2>;
-  static int per_sm = 0;
-  if (!per_sm) {
+  int per_sm = 0;
+  cudaError_t ce = cnp_dev_cached((const void*)kern, &per_sm, [&](int* v) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::bytes);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::NT, G::bytes);
-    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-  }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(v, kern, G::NT, G::bytes);
+    if (e != cudaSuccess || *v < 1) *v = 1;
+    return cudaSuccess;
+  });
+  if (ce != cudaSuccess) return ce;
   const int W = (int)c->slice;  // real columns per time row
   FsSched S;
   S.nxb = (W + 2 * G::NC - 1) / (2 * G::NC);
@@ -605,8 +606,7 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   S.lag[2] = MODE == 2 ? 2 * L : L;
   S.total = (unsigned)(S.nxb + S.lag[2]) * (unsigned)per;  // including the empty edge slots
   const int grid = (int)(S.total < (unsigned)grid_max ? S.total : (unsigned)grid_max);
-  static int no_discard = -1;
-  if (no_discard < 0) no_discard = getenv("CNPINT_FS_NODISCARD") ? 1 : 0;
+  static const int no_discard = getenv("CNPINT_FS_NODISCARD") ? 1 : 0;  // tuning knob, read once
   FsArgs a;
   a.vin = vin; a.spin = spin; a.vout = vout; a.spout = spout; a.Y = (double2*)c->d_fsY; a.vscale = vscale;
   a.gam = c->d_gam; a.igam = c->d_igam; a.twN = c->d_tw; a.lam1 = c->d_lam1; a.lam2 = c->d_lam2; a.ex = c->d_ex; a.ey = c->d_ey;
@@ -614,8 +614,7 @@ static cudaError_t fs_launch(cnpint_ctx* c, const double* vin, const double2* sp
   a.W = W; a.ld = (int)c->ld; a.nx = c->nx; a.accumulate = accumulate; a.debug_sign = c->debug & 1;
   a.no_discard = no_discard;
 #ifdef CNPINT_EXPERIMENTS  // result-corrupting timing knob: only in experiment builds
-  static int skip = -1;
-  if (skip < 0) skip = getenv("CNPINT_FS_SKIP") ? atoi(getenv("CNPINT_FS_SKIP")) : 0;
+  static const int skip = getenv("CNPINT_FS_SKIP") ? atoi(getenv("CNPINT_FS_SKIP")) : 0;
   a.skip = skip;
 #else
   a.skip = 0;

@@ -81,12 +81,11 @@ CNP_DEV void block_partial(double v, double* part, double* out = nullptr, unsign
 #endif
 // rows of the time chunk a 1D block walks (CNPINT_MV_TCHUNK: tuning override, 8/16/32/64)
 static int mv_tchunk(const cnpint_ctx* c) {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {  // read once (thread-safe static initialisation)
     const char* e = getenv("CNPINT_MV_TCHUNK");
     const int t = e ? atoi(e) : 0;
-    v = (t == 8 || t == 16 || t == 32 || t == 64) ? t : 0;
-  }
+    return (t == 8 || t == 16 || t == 32 || t == 64) ? t : 0;
+  }();
   return v ? v : (c->N >= 4096 ? 32 : 16);
 }
 

@@ -393,7 +393,7 @@ static cudaError_t launch_c(cnpint_ctx* c, const TfftCfg& f, const double* vin, 
   constexpr int NC = LOGN2 <= 9 ? 8 : LOGN2 == 10 ? 4 : 2;
   using LY = TfLayout<MODE, C, LOGN2, NC>;
   auto kern = k_tfft<MODE, C, LOGN2, NC>;
-  static int max_clusters = 0;
+  int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(TF_NT);
   cfg.dynamicSmemBytes = LY::bytes;
@@ -405,14 +405,18 @@ static cudaError_t launch_c(cnpint_ctx* c, const TfftCfg& f, const double* vin, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (!max_clusters) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY::bytes);
-    if (e != cudaSuccess) return e;
-    cfg.gridDim = dim3(C * c->num_sms);
-    int n = 0;
-    e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-    if (e != cudaSuccess || n < 1) n = c->num_sms / C;
-    max_clusters = n < 1 ? 1 : n;
+  {
+    cudaError_t ce = cnp_dev_cached((const void*)kern, &max_clusters, [&](int* v) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LY::bytes);
+      if (e != cudaSuccess) return e;
+      cfg.gridDim = dim3(C * c->num_sms);
+      int n = 0;
+      e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+      if (e != cudaSuccess || n < 1) n = c->num_sms / C;
+      *v = n < 1 ? 1 : n;
+      return cudaSuccess;
+    });
+    if (ce != cudaSuccess) return ce;
   }
   const int64_t W = c->slice;  // 1D: ld; 2D: ny*ld
   const int ntiles = (int)((W + 2 * NC - 1) / (2 * NC));

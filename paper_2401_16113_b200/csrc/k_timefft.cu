@@ -198,11 +198,13 @@ static cudaError_t run_fft(cnpint_ctx* c, const double* vin, const double2* spin
                            const double* vscale, int accumulate) {
   FftCfg f = fft_cfg(c->N);
   const int64_t W = c->slice;  // 1D: ld; 2D: ny*ld
-  static bool attr_done[3] = {false, false, false};
-  if (!attr_done[MODE]) {
-    cudaError_t e = cudaFuncSetAttribute(k_time_fft<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_done[MODE] = true;
+  {
+    int done = 0;
+    cudaError_t ce = cnp_dev_cached((const void*)k_time_fft<MODE>, &done, [&](int* v) {
+      *v = 1;
+      return cudaFuncSetAttribute(k_time_fft<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    if (ce != cudaSuccess) return ce;
   }
   unsigned grid = (unsigned)((W + f.X - 1) / f.X);
   const int kid = MODE == 0 ? KID_FFT_FWD : MODE == 1 ? KID_FFT_INV : KID_TIMEPASS2D;

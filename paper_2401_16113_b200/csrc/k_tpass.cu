@@ -199,15 +199,17 @@ template <int LOGN>
 static cudaError_t run_tpass(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   using TP = TpPlan<LOGN>;
   auto kern = k_tpass_r<LOGN>;
-  static int grid_max = 0;
-  if (!grid_max) {
+  int grid_max = 0;
+  cudaError_t ce = cnp_dev_cached((const void*)kern, &grid_max, [&](int* v) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TP::bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TP::NT, TP::bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-    grid_max = per_sm * c->num_sms;
-  }
+    *v = per_sm * c->num_sms;
+    return cudaSuccess;
+  });
+  if (ce != cudaSuccess) return ce;
   const int ntiles = (int)((c->slice / 2 + TP::NC - 1) / TP::NC);
   const int grid = ntiles < grid_max ? ntiles : grid_max;
   cnp_launch(c, kern, dim3(grid), dim3(TP::NT), TP::bytes, in, out, vscale, c->slice, (int)c->ld, c->nx,

@@ -461,13 +461,14 @@ TriCfg tri_cfg(int m, int toeplitz) {
   // (variable rows also carry α', γ'; measured: 8 / 512 threads at c2 and 4 at c3 are slower);
   // G = warps per system, NS = systems per CTA (<= 8 warps when G < 8).  Tuning overrides:
   // CNPINT_TRI_LCAP_T / CNPINT_TRI_LCAP_V (4, 8 or 16).
-  static int lcap_t = -1, lcap_v = -1;
-  if (lcap_t < 0) {
+  static const int lcap_t = [] {  // tuning knobs, read once (thread-safe static initialisation)
     const char* e = getenv("CNPINT_TRI_LCAP_T");
-    lcap_t = e && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 16) ? atoi(e) : 16;
-    e = getenv("CNPINT_TRI_LCAP_V");
-    lcap_v = e && (atoi(e) == 4 || atoi(e) == 8) ? atoi(e) : 8;
-  }
+    return e && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 16) ? atoi(e) : 16;
+  }();
+  static const int lcap_v = [] {
+    const char* e = getenv("CNPINT_TRI_LCAP_V");
+    return e && (atoi(e) == 4 || atoi(e) == 8) ? atoi(e) : 8;
+  }();
   const int Lcap = toeplitz ? lcap_t : lcap_v;
   int G = 1;
   while (G < 16 && 32 * G * Lcap < m) G <<= 1;
@@ -506,8 +507,7 @@ TriCfg tri_cfg(int m, int toeplitz) {
 // (read only in builds with -DCNPINT_EXPERIMENTS; the product build always runs every phase)
 static int tri_skip() {
 #ifdef CNPINT_EXPERIMENTS
-  static int v = -1;
-  if (v < 0) v = getenv("CNPINT_TRI_SKIP") ? atoi(getenv("CNPINT_TRI_SKIP")) : 0;
+  static const int v = getenv("CNPINT_TRI_SKIP") ? atoi(getenv("CNPINT_TRI_SKIP")) : 0;
   return v;
 #else
   return 0;
@@ -516,11 +516,13 @@ static int tri_skip() {
 
 template <int MODE, int L, int MAXT>
 static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_tridiag<MODE, L, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  {
+    int done = 0;
+    cudaError_t ce = cnp_dev_cached((const void*)k_tridiag<MODE, L, MAXT>, &done, [&](int* v) {
+      *v = 1;
+      return cudaFuncSetAttribute(k_tridiag<MODE, L, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    if (ce != cudaSuccess) return ce;
   }
   const int K = c->H + 1;
   const int grid = (K + t.NS - 1) / t.NS;

@@ -363,7 +363,10 @@ def test_2d_fast_diagonalisation_vs_dense_shifted_solve():
 
 
 def test_toeplitz_eig_closed_form():
-    for (s, d, u) in ((1.0, -2.0, 1.0), (35.77, -72.8, 37.05), (0.3, -1.0, 0.6)):
+    # the last two triples have negative off-diagonals (s·u > 0 still): the symmetrised off-diagonal
+    # is sgn(s)·√(su), so mode j's eigenvalue must not be that of mode n+1−j
+    for (s, d, u) in ((1.0, -2.0, 1.0), (35.77, -72.8, 37.05), (0.3, -1.0, 0.6), (-1.0, -4.0, -1.0),
+                      (-0.3, 1.0, -0.6)):
         n = 9
         D, e = precond.toeplitz_eig(n, s, d, u)
         S = precond.dst1_matrix(n)
@@ -371,6 +374,108 @@ def test_toeplitz_eig_closed_form():
         assert np.abs(S @ S - np.eye(n)).max() < 1e-13
         assert np.abs((D[:, None] * S) @ np.diag(e) @ (S / D[None, :]) - L).max() < 1e-12
         np.testing.assert_allclose(np.sort(np.linalg.eigvals(L).real), np.sort(e), atol=1e-12)
+
+
+def test_2d_shifted_solve_negative_offdiagonals_vs_dense():
+    """2D fast diagonalisation with L_x = tridiag(−1, −4, −1), L_y = tridiag(−0.5, −3, −0.7)
+    (negative-definite, negative off-diagonals): each shifted system against a dense solve, and P_α⁻¹
+    against numpy.linalg.solve on the dense P_α."""
+    w = small2d(5, 8, 0.1)
+    op = problem.Operator2D(xs=-1.0, xd=-4.0, xu=-1.0, ys=-0.5, yd=-3.0, yu=-0.7, shift=-0.2, n=5,
+                            x=np.arange(1, 6) / 6.0, h=1.0 / 6.0)
+    tau = w.T / w.N
+    l1, l2 = precond.lambdas(w.N, w.alpha)
+    rng = np.random.default_rng(7)
+    R = rng.standard_normal((3, 5, 5)) + 1j * rng.standard_normal((3, 5, 5))
+    Z = precond.shifted_solve(w, op, l1[:3], l2[:3], R)
+    A = tau * op.dense()
+    for k in range(3):
+        assert rel(Z[k].ravel(), np.linalg.solve(l1[k] * np.eye(25) - l2[k] * A, R[k].ravel())) < 1e-12
+    v = rng.standard_normal((w.N, 5, 5))
+    assert rel(precond.pinv_dft(w, op, v), precond.pinv_dense(w, op, v)) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["logprice", "price", "bs2d"])
+def test_operator_rows_exact_on_quadratics(kind):
+    """Central differences are exact on polynomials of degree ≤ 2, so at interior rows (both
+    neighbours inside the domain) L_h applied to 1, x, x² (and y, y², xy in 2D) must equal the
+    continuous 𝓛 (BASELINE.json configs: σ²/2·∂xx + drift·∂x − r) evaluated by hand:
+      𝓛1 = −r,  𝓛x = b(x) − r x,  𝓛x² = σ²(x)·… — three equations per row pin lo, di, up (a dropped
+    term, a wrong sign or swapped lo/up fails one of them), independently of build_operator's formulas."""
+    w = {"logprice": synth.scaled(synth.C1, 31, 8), "price": synth.scaled(synth.C3, 31, 8),
+         "bs2d": synth.scaled(synth.C4, 15, 8)}[kind]
+    op = problem.build_operator(w)
+    r = w.r
+    if kind in ("logprice", "price"):
+        x = op.x
+        inner = slice(1, op.m - 1)
+        if kind == "logprice":        # 𝓛 = (σ²/2)∂xx + (r − σ²/2)∂x − r
+            a2 = 0.5 * w.sigma ** 2 * np.ones_like(x)
+            a1 = (r - 0.5 * w.sigma ** 2) * np.ones_like(x)
+        else:                         # 𝓛 = (σ²S²/2)∂SS + rS∂S − r
+            a2 = 0.5 * w.sigma ** 2 * x * x
+            a1 = r * x
+        for u, Lu in ((np.ones_like(x), -r * np.ones_like(x)),
+                      (x.copy(), a1 - r * x),
+                      (x * x, 2 * a2 + 2 * a1 * x - r * x * x)):
+            got = problem.apply_L(op, u)
+            assert np.abs(got[inner] - Lu[inner]).max() <= 1e-9 * max(1.0, np.abs(Lu[inner]).max())
+        return
+    X, Y = np.meshgrid(op.x, op.x)     # [y][x]
+    s1, s2 = w.sigma2
+    b1, b2 = r - 0.5 * s1 * s1, r - 0.5 * s2 * s2
+    inner = (slice(1, op.n - 1), slice(1, op.n - 1))
+    one = np.ones_like(X)
+    cases = ((one, -r * one), (X, b1 - r * X), (Y, b2 - r * Y), (X * X, s1 * s1 + 2 * b1 * X - r * X * X),
+             (Y * Y, s2 * s2 + 2 * b2 * Y - r * Y * Y), (X * Y, b1 * Y + b2 * X - r * X * Y))
+    for u, Lu in cases:
+        got = problem.apply_L(op, u)
+        assert np.abs(got[inner] - Lu[inner]).max() <= 1e-9 * max(1.0, np.abs(Lu[inner]).max())
+
+
+def test_pinv_dft_matrix_route_at_N4096():
+    """The dense-DFT-matrix route of Eq. 3.2 (exact (k·t mod N) table, λ from D_ℓ = diag(√N𝔽Λ_αc_ℓ)
+    by a dense product) against the library-FFT route at N = 4096 (c2's time length) on one column
+    block (m = 15), and both against the FFT-free fixed-point sweep of the block form."""
+    w = synth.scaled(synth.C1, 15, 4096, alpha=0.01)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 3)[0]
+    zf = precond.pinv_dft(w, op, v)
+    zm = precond.pinv_dft(w, op, v, dft="matrix")
+    zs, _ = precond.pinv_sweep(w, op, v)
+    assert rel(zm, zf) < 1e-12 and rel(zs, zf) < 1e-12 and rel(zs, zm) < 1e-12
+    assert rel(aao.apply_P(w, op, zm), v) < 1e-12
+
+
+def test_gmres_iterates_equal_maxit_reruns():
+    """gmres_right(iterates=[…]) records x_j after every inner step; each equals the result of a
+    separate run stopped at maxit = j (the definition of the j-th iterate)."""
+    w = synth.scaled(synth.C1, 31, 32, alpha=0.3)
+    op = problem.build_operator(w)
+    b = problem.assemble_rhs(w, op)
+    A = lambda x: aao.apply_M(w, op, x)
+    P = lambda x: precond.pinv_dft(w, op, x)
+    its = []
+    u, rep = gmres.gmres_right(A, P, b, 1e-10, 3, iterates=its)   # restart 3: crosses cycles
+    assert len(its) == rep.iterations >= 4 and rep.restarts >= 1
+    for j in (1, 2, 3):
+        uj, _ = gmres.gmres_right(A, P, b, 1e-10, 3, maxit=j)
+        assert rel(its[j - 1], uj) < 1e-14
+    assert rel(its[-1], u) < 1e-14
+
+
+@pytest.mark.parametrize("n", [15, 31])
+def test_q1_solver_dst_equals_sparse_lu(n):
+    """The dense-DST Q1 solve (used for n ≥ 256) against scipy's sparse LU of Q1 = I − ½τL_h."""
+    w = small2d(n, 8)
+    op = problem.build_operator(w)
+    tau = w.T / w.N
+    r = np.random.default_rng(n).standard_normal((n, n))
+    x1 = aao.Q1Solver(op, tau, dst_min=1)(r)
+    x2 = aao.Q1Solver(op, tau, dst_min=10 ** 9)(r)
+    assert aao.Q1Solver(op, tau, dst_min=1).dst is not None and aao.Q1Solver(op, tau, dst_min=10 ** 9).dst is None
+    assert rel(x1, x2) < 1e-13
+    assert rel(aao.Q1(op, tau, x1), r) < 1e-13
 
 
 @pytest.mark.parametrize("mk", [lambda: synth.C1])
