@@ -380,6 +380,9 @@ static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const
   return cudaGetLastError();
 }
 
+cudaError_t launch_dst2(cnpint_ctx* c, bool ypass, const double* in, double* out, const double* pre,
+                        const double* post, int accumulate);
+
 template <bool YPASS>
 static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
                            int accumulate) {
@@ -392,7 +395,14 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   // the Stockham kernel everywhere (cross-check).
   const bool reg = !(c->debug & 32);
   cnp_prof_begin(c, kid);
-  cudaError_t e;
+  cudaError_t e = cudaErrorNotSupported;
+  // the pipelined half-length kernel (k_dst2.cu) for n + 1 ∈ {64, …, 512} on square grids; debug
+  // bit 256 keeps the first-generation kernels below (cross-check and A/B)
+  if (!(c->debug & (256 | 32))) e = launch_dst2(c, YPASS, in, out, pre, post, accumulate);
+  if (e != cudaErrorNotSupported) {
+    cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
+    return e;
+  }
   switch (logE) {
     case 2: e = run_dst_t<YPASS, 2>(c, in, out, pre, post, accumulate); break;
     case 3: e = run_dst_t<YPASS, 3>(c, in, out, pre, post, accumulate); break;
