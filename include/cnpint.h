@@ -238,7 +238,8 @@ cnpint_status cnpint_peak_kernel(int kind, double* d_out, int iters, void* cuda_
  * 32 = the shared-memory Stockham DST kernel for every 2D sine pass; 64 = the cluster kernel instead
  * of the register time pass for 2D N = 256, 512; 128 = classic CGS2 in cnpint_gmres (a second
  * reading pass c2 = Ṽᵀ(w − Ṽs²c1)) instead of the Gram form c2 = c1 − G̃s²c1, whose Gram row
- * Ṽᵀ Ṽ_j is reduced inside the matvec (K7). */
+ * Ṽᵀ Ṽ_j is reduced inside the matvec (K7); 256 = the pipelined half-length DST kernel
+ * (k_dst2.cu: TMA bulk-copy ring, n + 1 ∈ {64, …, 512}, square grids) for the 2D sine passes. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

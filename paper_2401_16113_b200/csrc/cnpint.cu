@@ -1018,7 +1018,9 @@ cnpint_status cnpint_krylov_basis(cnpint_ctx* c, int i, const double** d_vec, do
   if (i < 0 || i >= c->last_nv || !c->last_v0) { seterr(c, "krylov_basis: no such vector"); return CNPINT_EINVAL; }
   if (d_vec) *d_vec = i == 0 ? c->last_v0 : c->d_V + (size_t)i * c->vec;
   if (scale) {
-    CK(cudaMemcpyAsync(scale, c->d_scl + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    // s_0 was replaced by the cycle-end residual's cycle start, which saved it in scal[12]
+    const double* src = i == 0 ? c->d_scal + 12 : c->d_scl + i;
+    CK(cudaMemcpyAsync(scale, src, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
   return CNPINT_OK;

@@ -396,9 +396,10 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   const bool reg = !(c->debug & 32);
   cnp_prof_begin(c, kid);
   cudaError_t e = cudaErrorNotSupported;
-  // the pipelined half-length kernel (k_dst2.cu) for n + 1 ∈ {64, …, 512} on square grids; debug
-  // bit 256 keeps the first-generation kernels below (cross-check and A/B)
-  if (!(c->debug & (256 | 32))) e = launch_dst2(c, YPASS, in, out, pre, post, accumulate);
+  // debug bit 256: the pipelined half-length kernel (k_dst2.cu) for n + 1 ∈ {64, …, 512} on square
+  // grids — parity-green but not faster on B200 (x pass 0.97-1.04x of the kernels below, y pass
+  // 0.4x: 511 small TMA bulk copies per tile issue too slowly; profiles/r02_dst2_ab.txt), so opt-in
+  if ((c->debug & 256) && !(c->debug & 32)) e = launch_dst2(c, YPASS, in, out, pre, post, accumulate);
   if (e != cudaErrorNotSupported) {
     cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
     return e;

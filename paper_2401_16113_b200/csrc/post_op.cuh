@@ -8,6 +8,7 @@
 CNP_DEV void cycle_start_dev(double* scl, double* g, double* scal, int first, int rmax, double* G = nullptr) {
   const double beta = sqrt(scal[2]);
   if (G) G[0] = scal[2];  // Gram CGS2: G̃_00 = ‖Ṽ_0‖²
+  if (!first) scal[12] = scl[0];  // the ending cycle's s_0 (cnpint_krylov_basis test hook)
   if (first) scal[0] = beta;
   scal[4] = beta / scal[0];
   scl[0] = beta > 0.0 ? 1.0 / beta : 0.0;
