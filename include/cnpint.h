@@ -34,8 +34,10 @@
  * Errors
  *   Argument errors are detected synchronously (CNPINT_EINVAL / CNPINT_EUNSUPPORTED) and
  *   nothing is enqueued.  CUDA launch/runtime failures return CNPINT_ECUDA.  A zero or
- *   non-finite pivot in the shifted tridiagonal solve sets a device status word (SPEC.md:298
- *   SingularPreconditioner) reported as CNPINT_ESINGULAR by cnpint_gmres / cnpint_device_status.
+ *   non-finite pivot in the shifted tridiagonal solve — "zero" read relatively: a pivot or 2×2
+ *   elimination determinant that cancels below 1e-13 of its terms — sets a device status word
+ *   (SPEC.md:298 SingularPreconditioner) reported as CNPINT_ESINGULAR by cnpint_device_status and
+ *   by cnpint_gmres* (which stop at the step whose P_α⁻¹ met it; the status word is cleared).
  *   cnpint_last_error(ctx) returns a human-readable message for the last failure.
  */
 #ifndef CNPINT_H

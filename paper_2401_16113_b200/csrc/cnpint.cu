@@ -853,6 +853,10 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       jdone = j + 1;
       est = h[1];
       if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
+      if (h[8] != 0.0) {  // the step's P⁻¹ met a singular shifted system: stop now (status word read back)
+        cnpint_status ds = cnpint_device_status(c);
+        return ds != CNPINT_OK ? ds : CNPINT_ESINGULAR;
+      }
       if (h[3] != 0.0) {
         // a singular shifted solve (zero / non-finite pivot, e.g. P_1 with a singular variable-row Ã)
         // poisons P⁻¹ first: report it as such (and clear the status word) before calling it breakdown
@@ -962,6 +966,10 @@ cnpint_status cnpint_gmres_left(cnpint_ctx* c, const double* d_b, double* d_u, d
       jdone = j + 1;
       est = h[1];
       if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
+      if (h[8] != 0.0) {  // singular shifted system in this step's P⁻¹ (see cnpint_gmres)
+        cnpint_status ds = cnpint_device_status(c);
+        return ds != CNPINT_OK ? ds : CNPINT_ESINGULAR;
+      }
       if (h[3] != 0.0) {
         if (cnpint_status ds = cnpint_device_status(c)) return ds;  // singular pivot first (see cnpint_gmres)
         seterr(c, "gmres_left: non-finite scalar in the Arnoldi process");

@@ -411,9 +411,9 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
     case 5: e = run_dst_t<YPASS, 5>(c, in, out, pre, post, accumulate); break;
     case 6: e = run_dst_t<YPASS, 6>(c, in, out, pre, post, accumulate); break;
     case 7: e = run_dst_t<YPASS, 7>(c, in, out, pre, post, accumulate); break;
-    case 8: e = run_dst_t<YPASS, 8>(c, in, out, pre, post, accumulate); break;
-    case 9: e = (reg && YPASS) ? run_dst_r<YPASS, 9>(c, in, out, pre, post, accumulate) : run_dst_t<YPASS, 9>(c, in, out, pre, post, accumulate); break;
-    case 10: e = run_dst_t<YPASS, 10>(c, in, out, pre, post, accumulate); break;
+    case 8: e = (c->debug & 1024) ? run_dst_r<YPASS, 8>(c, in, out, pre, post, accumulate) : run_dst_t<YPASS, 8>(c, in, out, pre, post, accumulate); break;
+    case 9: e = (reg && (YPASS || (c->debug & 1024))) ? run_dst_r<YPASS, 9>(c, in, out, pre, post, accumulate) : run_dst_t<YPASS, 9>(c, in, out, pre, post, accumulate); break;
+    case 10: e = (c->debug & 1024) ? run_dst_r<YPASS, 10>(c, in, out, pre, post, accumulate) : run_dst_t<YPASS, 10>(c, in, out, pre, post, accumulate); break;
     case 11: e = run_dst_t<YPASS, 11>(c, in, out, pre, post, accumulate); break;
     default: e = cudaErrorInvalidValue; break;
   }

@@ -58,8 +58,20 @@ CNP_DEV Seg shfl_seg(const Seg& s, int d) {
 // Merge segment A (in place) with its right neighbour B; the affine maps
 //   x_m = P0 + P1 x_s + P2 x_e,  x_{m+1} = R0 + R1 x_s + R2 x_e
 // are written to cf[0..5].  Returns false on a zero / non-finite 2x2 determinant.
+// "Singular to working precision": a pivot or 2×2 determinant that cancels to below 1e-13 of the
+// magnitude of its terms (or is not finite).  An exactly singular system (e.g. P_1 at k = 0 with a
+// singular Ã, Remark 3.2) rarely produces an exact zero in the partitioned elimination, so the zero
+// test of the header is read relatively.  The shifted systems of P_α (α < 1) are diagonally dominant
+// (R22): their pivots never come near this.
+CNP_DEV bool cancels(double2 x, double ref2) {
+  const double x2 = fma(x.x, x.x, x.y * x.y);
+  return !(x2 > 1e-26 * ref2) || !isfinite(x2);
+}
+CNP_DEV double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
 CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf) {
   const double2 det = csub(cmul(A.gb, B.fb), cmul(A.gc, B.fa));
+  const bool sing = cancels(det, cabs2(cmul(A.gb, B.fb)) + cabs2(cmul(A.gc, B.fa)));
   const double2 id = crecip_nr(det);
   const double2 P0 = cmul(csub(cmul(B.fb, A.gd), cmul(A.gc, B.fd)), id);
   const double2 P1 = cneg(cmul(cmul(B.fb, A.ga), id));
@@ -75,7 +87,7 @@ CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf) {
   A.gb = cfma(B.ga, R2, B.gb);
   A.gd = cfms(B.gd, B.ga, R0);
   A.gc = B.gc;
-  return cfinite(id);
+  return cfinite(id) && !sing;
 }
 
 CNP_DEV void unmerge(const double2* cf, double2 xs, double2 xe, double2& xm, double2& xm1) {
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           const double2 bb = make_double2(skk.x - tau * di[i], skk.y);
           const double2 piv = (j == 1) ? bb : crfms(bb, a, gam);
           const double2 inv = crecip_nr(piv);
-          ok &= cfinite(inv);
+          ok &= cfinite(inv) && !cancels(piv, cabs2(bb) + (j == 1 ? 0.0 : a * a * cabs2(gam)));
           alp = (j == 1) ? cscale(inv, a) : cscale(cmul(alp, inv), -a);
           gam = cscale(inv, c);
           last = (j == 1) ? cmul(dl[1], inv) : cmul(crfms(dl[j], a, last), inv);
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(MAXT, 2)
     // fb x_0 + fc x_{m−1} = fd ; ga x_0 + gb x_{m−1} = gd  (x_{−1} = x_m = 0)
     const double2 det = csub(cmul(t.fb, t.gb), cmul(t.fc, t.ga));
     const double2 id = crecip(det);
-    ok &= cfinite(id);
+    ok &= cfinite(id) && !cancels(det, cabs2(cmul(t.fb, t.gb)) + cabs2(cmul(t.fc, t.ga)));
     xs = cmul(csub(cmul(t.fd, t.gb), cmul(t.fc, t.gd)), id);
     xe = cmul(csub(cmul(t.fb, t.gd), cmul(t.ga, t.fd)), id);
   };
@@ -439,7 +451,7 @@ __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __res
     const double2 d = cmul(src[i], il);
     const double2 piv = (i == 0) ? b : crfms(b, a, cp[i - 1]);
     const double2 inv = crecip(piv);
-    ok &= cfinite(inv);
+    ok &= cfinite(inv) && !cancels(piv, cabs2(b) + (i == 0 ? 0.0 : a * a * cabs2(cp[i - 1])));
     cp[i] = cscale(inv, c);
     dp[i] = (i == 0) ? cmul(d, inv) : cmul(crfms(d, a, dp[i - 1]), inv);
   }
