@@ -231,6 +231,60 @@ cnpint_status cnpint_krylov_basis(cnpint_ctx* ctx, int i, const double** d_vec, 
  * events on the same stream.  EINVAL for bad arguments, ECUDA on launch failure. */
 cnpint_status cnpint_peak_kernel(int kind, double* d_out, int iters, void* cuda_stream, double* flops);
 
+/* ---------------------------------------------------------------------------------------------
+ * 1D x-sharded handles.  R ranks (one GPU each) split the
+ * spatial index of a 1D operator into contiguous chunks [x0[r], x0[r+1]), x0[0] = 0, x0[R] = nx, every
+ * chunk >= 2 rows; rank r's vectors are [N][ld_r] over its chunk (ld_r = cnpint_ld).  P_α⁻¹ (PAPER.md
+ * Eq. 3.2): the time transforms are per column (local); each frequency's tridiagonal system
+ * (λ1_k I − λ2_k Ã) ẑ_k = ŵ_k is solved by a partition method — a local solve, an
+ * all-gather of 2 complex per frequency (the local solution's end values), a redundant block-
+ * tridiagonal 2R × 2R reduced solve, a local re-solve with corrected end rows.  𝓜u
+ * all-gathers every rank's two boundary columns (2N doubles).  GMRES all-reduces its dot products.
+ * Constant-coefficient operators, 0 < α < 1.
+ *
+ * Collectives are the caller's (e.g. NCCL through torch.distributed): op 0 = all-gather
+ * (d_recv[r·count + i] = rank r's d_send[i], r < R), op 1 = in-place all-reduce sum of d_send (==
+ * d_recv); device buffers of the handle's workspace; enqueue on cuda_stream or synchronise it; return 0
+ * on success.  With R = 1 no callback is needed. */
+typedef int (*cnpint_collective_fn)(void* user, int op, const double* d_send, double* d_recv, size_t count,
+                                    void* cuda_stream);
+
+size_t cnpint_shard_workspace_bytes(int N, const cnpint_operator* op, int R, const int* x0, int rank,
+                                    int restart_max);
+/* Arguments as cnpint_create, with op the GLOBAL 1D operator, R ranks, chunk bounds x0[R+1] and this
+ * rank.  Builds rank `rank`'s handle (local operator = rows x0[rank]..x0[rank+1]−1, the couplings to the
+ * neighbours kept aside) and the spike-end table of every rank (host, long double). */
+cnpint_status cnpint_shard_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op, int R,
+                                  const int* x0, int rank, int restart_max, void* d_workspace, size_t ws_bytes,
+                                  void* cuda_stream);
+cnpint_status cnpint_shard_set_collective(cnpint_ctx* ctx, cnpint_collective_fn fn, void* user);
+/* The exchange buffers inside the workspace (device): the end values (send ends_count doubles, receive
+ * R·ends_count) and the boundary columns (send halo_count = 2N, receive R·2N).  Any pointer may be NULL. */
+cnpint_status cnpint_shard_buffers(cnpint_ctx* ctx, double** ends_send, double** ends_recv, size_t* ends_count,
+                                   double** halo_send, double** halo_recv, size_t* halo_count);
+/* Whole operations through the collective callback (rank-local vectors in, rank-local out). */
+cnpint_status cnpint_shard_apply_Pinv(cnpint_ctx* ctx, const double* d_v, double* d_z);
+cnpint_status cnpint_shard_apply_A(cnpint_ctx* ctx, const double* d_u, double* d_y);
+/* Right-preconditioned restarted GMRES on the sharded system (the algorithm of cnpint_gmres with classic
+ * CGS2 and all-reduced dot products); every rank receives the same report.  Synchronises. */
+cnpint_status cnpint_shard_gmres(cnpint_ctx* ctx, const double* d_b, double* d_u, double tol, int restart,
+                                 int maxit, cnpint_gmres_report* rep);
+/* Phase-split operations (the caller moves the exchange buffers between the phases): P_α⁻¹ =
+ * pinv_begin → all-gather of the end values → pinv_end; 𝓜u = halo_begin → all-gather of the boundary
+ * columns → apply_A_end. */
+cnpint_status cnpint_shard_pinv_begin(cnpint_ctx* ctx, const double* d_v);
+cnpint_status cnpint_shard_pinv_end(cnpint_ctx* ctx, double* d_z);
+cnpint_status cnpint_shard_halo_begin(cnpint_ctx* ctx, const double* d_u);
+cnpint_status cnpint_shard_apply_A_end(cnpint_ctx* ctx, const double* d_u, double* d_y);
+/* Host-only partition arithmetic (no GPU; the same code the handles run): the spike-end table
+ * red[(k R + r) 4 + (v1, vm, w1, wm)] (complex, K = N/2+1 frequencies) and ab[2r + (α_r, β_r)]; and the
+ * reduced solve for rank `rank` given every rank's end values ends_all[(r K + k) 2 + (g_1, g_m)] (complex),
+ * writing neighbours[k] = (xe_{rank−1}, xs_{rank+1}) (complex pairs).  ESINGULAR if a 2×2 block cancels. */
+cnpint_status cnpint_shard_spike_ends_host(int N, double T, double alpha, const cnpint_operator* op, int R,
+                                           const int* x0, double* red_out, double* ab_out);
+cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* red, const double* ab,
+                                        const double* ends_all, double* neighbours);
+
 /* Test hook (negative controls): 0 = none, 1 = flip the sign of the FFT twiddles,
  * 2 = use the printed Eq. eigCx ordering λ1_k = 1 − a e^{+2πik/N} (R3).
  * The parity suite must fail with either set.  Kernel-variant bits (not negative controls; the

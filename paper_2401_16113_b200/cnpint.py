@@ -29,7 +29,11 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_apply_Pinv_host", "cnpint_apply_A_host", "cnpint_gmres_host", "cnpint_device_status",
            "cnpint_launch_count", "cnpint_stream_copy", "cnpint_set_debug", "cnpint_profile_enable",
            "cnpint_profile_read", "cnpint_kernel_name", "cnpint_set_time_dependence", "cnpint_gmres_left",
-           "cnpint_krylov_basis", "cnpint_peak_kernel"]
+           "cnpint_krylov_basis", "cnpint_peak_kernel",
+           "cnpint_shard_workspace_bytes", "cnpint_shard_create", "cnpint_shard_set_collective", "cnpint_shard_buffers",
+           "cnpint_shard_apply_Pinv", "cnpint_shard_apply_A", "cnpint_shard_gmres", "cnpint_shard_pinv_begin",
+           "cnpint_shard_pinv_end", "cnpint_shard_halo_begin", "cnpint_shard_apply_A_end",
+           "cnpint_shard_spike_ends_host", "cnpint_shard_reduced_host"]
 
 
 class CnpintError(RuntimeError):
@@ -52,6 +56,9 @@ class GmresReport(C.Structure):
 
 
 _lib = None
+
+# int (*)(void* user, int op, const double* d_send, double* d_recv, size_t count, void* cuda_stream)
+COLLECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 def load_library(path: str = LIB_PATH):
@@ -87,6 +94,19 @@ def load_library(path: str = LIB_PATH):
         "cnpint_set_time_dependence": (C.c_int, [vp, dp]),
         "cnpint_krylov_basis": (C.c_int, [vp, C.c_int, C.POINTER(C.c_void_p), dp, C.POINTER(C.c_int)]),
         "cnpint_peak_kernel": (C.c_int, [C.c_int, vp, C.c_int, vp, dp]),
+        "cnpint_shard_workspace_bytes": (C.c_size_t, [C.c_int, C.POINTER(Operator), C.c_int, C.POINTER(C.c_int), C.c_int,
+                                                      C.c_int]),
+        "cnpint_shard_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_double, C.c_double, C.POINTER(Operator),
+                                          C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, vp, C.c_size_t, vp]),
+        "cnpint_shard_set_collective": (C.c_int, [vp, COLLECTIVE_FN, vp]),
+        "cnpint_shard_buffers": (C.c_int, [vp] + [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)] * 2),
+        "cnpint_shard_apply_Pinv": (C.c_int, [vp, vp, vp]), "cnpint_shard_apply_A": (C.c_int, [vp, vp, vp]),
+        "cnpint_shard_gmres": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(GmresReport)]),
+        "cnpint_shard_pinv_begin": (C.c_int, [vp, vp]), "cnpint_shard_pinv_end": (C.c_int, [vp, vp]),
+        "cnpint_shard_halo_begin": (C.c_int, [vp, vp]), "cnpint_shard_apply_A_end": (C.c_int, [vp, vp, vp]),
+        "cnpint_shard_spike_ends_host": (C.c_int, [C.c_int, C.c_double, C.c_double, C.POINTER(Operator), C.c_int,
+                                                   C.POINTER(C.c_int), dp, dp]),
+        "cnpint_shard_reduced_host": (C.c_int, [C.c_int, C.c_int, C.c_int, dp, dp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -538,6 +538,7 @@ void cnpint_destroy(cnpint_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);  // the caller may release the workspace right after this call
   prof_free(c);
+  cnp_shard_free(c);
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
 }

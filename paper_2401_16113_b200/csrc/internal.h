@@ -126,6 +126,7 @@ struct cnpint_ctx {
   double* h_pinned;    // mapped pinned host scalars [16]: d_scal[0..7], status at [8]
   double* d_hmap;      // its device alias
   PostOp post;         // pending post-fold operation for the next reducing launch (op 0 = none)
+  struct ShardInfo* shard;  // 1D x-sharded handle (shard.cu, NEXT #3), null for a whole-domain handle
   const double* last_v0;  // Ṽ_0 of the last completed GMRES cycle (b itself in the first), test hook
   int last_nv;            // basis vectors Ṽ_0..Ṽ_{last_nv−1} of that cycle
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
@@ -211,6 +212,7 @@ static inline cudaError_t cnp_launch(const cnpint_ctx* c, void (*k)(KArgs...), d
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 void cnp_prof_begin(cnpint_ctx* c, int kid);
+void cnp_shard_free(cnpint_ctx* c);  // shard.cu
 // Per-(key, CUDA device) cache of a launcher's one-time setup (cudaFuncSetAttribute is per-device
 // state; occupancy-derived grid sizes depend on the device): compute(&v) runs until it succeeds once
 // for the current device, under no lock (it must be idempotent); lookups and stores are mutex-guarded,
