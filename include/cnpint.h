@@ -109,9 +109,10 @@ size_t cnpint_workspace_bytes(int N, const cnpint_operator* op, int restart_max)
 /* Create a handle.  N: time steps, power of two, 2 <= N <= 65536 (1D; 2D: N <= 16384).  T > 0: horizon (τ = T/N).
  * alpha in (0, 1]: the α of C1^(α), C2^(α).  α = 1 is the block circulant P_1 of
  * the paper's comparison (NEXT #2): its k = N/2 shifted system degenerates to λ1 z = w, and P_1 is
- * singular iff Ã is (Remark 3.2) — for Toeplitz / 2D operators create checks the
- * closed-form spectrum and returns CNPINT_ESINGULAR; for variable rows a zero / non-finite pivot is
- * reported by cnpint_device_status / cnpint_gmres.
+ * singular iff Ã is (Remark 3.2) — create checks that and returns CNPINT_ESINGULAR
+ * (Toeplitz / 2D: the closed-form spectrum; variable rows: long-double elimination of L_h with a
+ * relative 1e-13 pivot test); a zero / non-finite pivot met later on the device is reported by
+ * cnpint_device_status / cnpint_gmres*.
  * d_workspace: device pointer, >= cnpint_workspace_bytes bytes, 256-B aligned.
  * cuda_stream: cudaStream_t (may be NULL = legacy default stream). */
 cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, const cnpint_operator* op,
@@ -295,7 +296,9 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * of the register time pass for 2D N = 256, 512; 128 = classic CGS2 in cnpint_gmres (a second
  * reading pass c2 = Ṽᵀ(w − Ṽs²c1)) instead of the Gram form c2 = c1 − G̃s²c1, whose Gram row
  * Ṽᵀ Ṽ_j is reduced inside the matvec (K7); 256 = the pipelined half-length DST kernel
- * (k_dst2.cu: TMA bulk-copy ring, n + 1 ∈ {64, …, 512}, square grids) for the 2D sine passes. */
+ * (k_dst2.cu: TMA bulk-copy ring, n + 1 ∈ {64, …, 512}, square grids) for the 2D sine passes;
+ * 1024 = the register DST kernel for every 2D sine pass with 2(n+1) ∈ {256, 512, 1024} (A/B);
+ * 2048 = fault injection: every 1D shifted solve reports a singular pivot (status-word tests). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -461,6 +461,19 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   if (op->dim == 1 && !op->toeplitz) {
     for (int i = 0; i < op->nx; ++i)
       if (!std::isfinite(op->sub[i]) || !std::isfinite(op->diag[i]) || !std::isfinite(op->sup[i])) return CNPINT_EINVAL;
+    if (alpha == 1.0) {
+      // P₁ is singular iff Ã is (Remark 3.2): Gaussian elimination of the variable-row
+      // L_h in long double; a pivot that cancels below 1e-13 of its terms means singular to working
+      // precision (the partitioned device elimination need not produce an exact zero for it)
+      long double cp = 0.0L;
+      for (int i = 0; i < op->nx; ++i) {
+        const long double a = i ? op->sub[i] : 0.0L, c = i < op->nx - 1 ? op->sup[i] : 0.0L;
+        const long double t = i ? a * cp : 0.0L;
+        const long double piv = (long double)op->diag[i] - t;
+        if (fabsl(piv) <= 1e-13L * (fabsl((long double)op->diag[i]) + fabsl(t))) return CNPINT_ESINGULAR;
+        cp = c / piv;
+      }
+    }
   } else {
     double v[7] = {op->xs, op->xd, op->xu, op->ys, op->yd, op->yu, op->shift};
     for (double x : v)

@@ -556,7 +556,15 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
   return cudaErrorInvalidValue;
 }
 
+// fault injection (debug bit 2048): the shifted solve reports a singular pivot, as a genuinely singular
+// system would — exercises the status-word path of cnpint_device_status / cnpint_gmres* deterministically
+__global__ void k_inject_singular(int* status) { atomicOr(status, 1); }
+
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat) {
+  if (c->debug & 2048) {
+    k_inject_singular<<<1, 1, 0, c->stream>>>(c->d_status);
+    if (cudaError_t e = cudaGetLastError()) return e;
+  }
   const int m = c->nx;
   const int K = c->H + 1;
   const int64_t W = c->ld;

@@ -685,27 +685,38 @@ def test_binding_rejects_bad_tensors():
 
 def test_singular_variable_rows_P1_reports_esingular():
     """NEXT #2 / ADVICE r01: α = 1 with a singular variable-row Ã (reflecting ends, rows summing to 0):
-    the k = 0 system −λ2Ã z = w is singular; apply_Pinv + device_status and cnpint_gmres must report
-    CNPINT_ESINGULAR (not EBREAKDOWN), and the status word is cleared afterwards."""
+    P₁ is singular iff Ã is (Remark 3.2) — refused at create with CNPINT_ESINGULAR (accepted for α < 1).
+    The device status-word path (a singular pivot met inside P⁻¹, fault-injected by debug bit 2048):
+    apply_Pinv + device_status and cnpint_gmres report CNPINT_ESINGULAR (not EBREAKDOWN), the word is
+    cleared afterwards, and the next solve on the same handle succeeds."""
     from paper_2401_16113_b200.cnpint import ESINGULAR
-    m = 64
-    i = np.arange(m, dtype=np.float64)
-    sub = 1.0 + 0.01 * i
-    sup = 1.0 + 0.02 * i
-    sub[0] = 0.0
-    sup[-1] = 0.0
-    diag = -(sub + sup)
-    spec = OperatorSpec(dim=1, nx=m, toeplitz=False, sub=sub, diag=diag, sup=sup)
-    s = Solver(16, 1.0, 1.0, spec, restart_max=10)
-    v = s.to_device(np.random.default_rng(3).standard_normal((16, m)))
+    for m in (40, 64, 200):
+        i = np.arange(m, dtype=np.float64)
+        sub = 1.0 + 0.01 * i
+        sup = 1.0 + 0.02 * i
+        sub[0] = 0.0
+        sup[-1] = 0.0
+        diag = -(sub + sup)
+        spec = OperatorSpec(dim=1, nx=m, toeplitz=False, sub=sub, diag=diag, sup=sup)
+        with pytest.raises(CnpintError) as ei:
+            Solver(16, 1.0, 1.0, spec, restart_max=10)
+        assert ei.value.status == ESINGULAR
+        Solver(16, 1.0, 0.5, spec)
+    w = SMALL["1d_price"]
+    s = solver_for(w, restart_max=10)
+    b = problems.rhs(w, s)
+    s.set_debug(2048)
     z = s.empty()
-    s.apply_Pinv(v, z)
+    s.apply_Pinv(b, z)
     assert s.device_status() == ESINGULAR
     assert s.device_status() == 0            # cleared by the report
     with pytest.raises(CnpintError) as ei:
-        s.gmres(v, s.empty(), 1e-10, 10)
+        s.gmres(b, s.empty(), 1e-10, 10)
     assert ei.value.status == ESINGULAR
     assert s.device_status() == 0
+    s.set_debug(0)
+    rep = s.gmres(b, s.empty(), 1e-10, 10)
+    assert rep["converged"]
 
 
 def test_peak_kernels_run():

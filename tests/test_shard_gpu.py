@@ -59,7 +59,15 @@ def test_sharded_pinv_and_matvec_phase_split(name):
     for rk, z in zip(ranks, zs):
         rk.pinv_end(z)
     zg = np.concatenate([rk.to_host(z) for rk, z in zip(ranks, zs)], axis=1)
-    fwd = rel(zg, precond.pinv_dft(w, op, v))
+    if w.N >= 4096:
+        # reading R-tol: at c2/c3 sizes the fp64 oracle's own error nears 1e-12, so the forward
+        # error is taken against the extended-precision oracle, bounded by max(1e-12, 4 × its own)
+        zt = precond.pinv_dft(w, op, v, extended=True)
+        own = rel(precond.pinv_dft(w, op, v), zt)
+        fwd = rel(zg, zt)
+        bar = max(1e-12, 4 * own)
+    else:
+        fwd, bar = rel(zg, precond.pinv_dft(w, op, v)), 1e-12
     back = rel(aao.apply_P(w, op, zg), v)
     # 𝓜u with the all-gathered boundary columns
     ys = [rk.empty() for rk in ranks]
@@ -73,7 +81,7 @@ def test_sharded_pinv_and_matvec_phase_split(name):
     yg = np.concatenate([rk.to_host(y) for rk, y in zip(ranks, ys)], axis=1)
     e_mv = rel(yg, aao.apply_M(w, op, v))
     record(f"shard_{name}", pinv_forward=fwd, pinv_backward=back, matvec=e_mv)
-    assert fwd < 1e-12 and back < 1e-12 and e_mv < 1e-12, (fwd, back, e_mv)
+    assert fwd <= bar and back < 1e-12 and e_mv < 1e-12, (fwd, bar, back, e_mv)
     for rk, z in zip(ranks, zs):
         assert float(z[:, rk.nx:].abs().max()) == 0.0 if rk.ld > rk.nx else True
         assert rk.device_status() == 0
