@@ -187,6 +187,15 @@ cnpint_status cnpint_apply_A_host(cnpint_ctx* ctx, const double* h_u, double* h_
 cnpint_status cnpint_gmres_host(cnpint_ctx* ctx, const double* h_b, double* h_u, double tol, int restart,
                                 int maxit, cnpint_gmres_report* rep);
 
+/* End-to-end GMRES over `count` right-hand sides in host memory (packed layout; pinned memory for the
+ * copies to overlap): solve i runs on the handle's stream while the H2D copy of b_{i+1} and the D2H
+ * copy of u_{i−1} run on two internal copy streams, so PCIe traffic in both directions hides behind
+ * the computation.  d_stage: caller-owned device scratch of 4·cnpint_vec_elems doubles, 16-B aligned.
+ * reps: NULL or an array of `count` reports.  Synchronises; returns CNPINT_OK, CNPINT_ENOCONV (some
+ * solve reached maxit; its report says which) or the first error. */
+cnpint_status cnpint_gmres_host_batch(cnpint_ctx* ctx, int count, const double* const* h_b, double* const* h_u,
+                                      double tol, int restart, int maxit, double* d_stage, cnpint_gmres_report* reps);
+
 /* Time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8).
  * d_half: host array of the N values d(t_{t+½}), t = 0..N−1 (finite, > 0), copied; NULL restores the
  * constant-coefficient method.  Afterwards 𝓜 = B1⊗I − (D̃B2)⊗Ã with D̃ = diag(d_half) in apply_A,

@@ -33,7 +33,7 @@ EXPORTS = ["cnpint_workspace_bytes", "cnpint_create", "cnpint_destroy", "cnpint_
            "cnpint_shard_workspace_bytes", "cnpint_shard_create", "cnpint_shard_set_collective", "cnpint_shard_buffers",
            "cnpint_shard_apply_Pinv", "cnpint_shard_apply_A", "cnpint_shard_gmres", "cnpint_shard_pinv_begin",
            "cnpint_shard_pinv_end", "cnpint_shard_halo_begin", "cnpint_shard_apply_A_end",
-           "cnpint_shard_spike_ends_host", "cnpint_shard_reduced_host"]
+           "cnpint_shard_spike_ends_host", "cnpint_shard_reduced_host", "cnpint_gmres_host_batch"]
 
 
 class CnpintError(RuntimeError):
@@ -107,6 +107,8 @@ def load_library(path: str = LIB_PATH):
         "cnpint_shard_spike_ends_host": (C.c_int, [C.c_int, C.c_double, C.c_double, C.POINTER(Operator), C.c_int,
                                                    C.POINTER(C.c_int), dp, dp]),
         "cnpint_shard_reduced_host": (C.c_int, [C.c_int, C.c_int, C.c_int, dp, dp, dp, dp]),
+        "cnpint_gmres_host_batch": (C.c_int, [vp, C.c_int, C.POINTER(dp), C.POINTER(dp), C.c_double, C.c_int, C.c_int,
+                                              vp, C.POINTER(GmresReport)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -365,6 +367,29 @@ class Solver:
             self._check(st, "gmres_host")
         return u, {"status": STATUS[st], "iterations": rep.iterations, "converged": bool(rep.converged),
                    "relres_true": rep.relres_true, "seconds": rep.seconds}
+
+    def gmres_host_batch(self, bs, us, tol: float, restart: int, maxit: int = 1000, stage=None):
+        """cnpint_gmres_host_batch over the host arrays bs → us (lists of packed float64 arrays, pinned for
+        overlap); stage: optional device scratch of 4·vec_elems doubles (allocated if None)."""
+        import torch
+        bs = [self._host_in(b, "b") for b in bs]
+        us = [self._host_out(u, "u") for u in us]
+        if len(bs) != len(us) or not bs:
+            raise CnpintError(EINVAL, "need as many outputs as right-hand sides")
+        if stage is None:
+            stage = torch.empty(4 * self.vec_elems, dtype=torch.float64, device=self.device)
+        ps = self._dev(stage, "stage", 4 * self.vec_elems)
+        dp = C.POINTER(C.c_double)
+        hb = (dp * len(bs))(*[b.ctypes.data_as(dp) for b in bs])
+        hu = (dp * len(us))(*[u.ctypes.data_as(dp) for u in us])
+        reps = (GmresReport * len(bs))()
+        with self._on_device():
+            self._sync_stream()
+            st = self.lib.cnpint_gmres_host_batch(self.h, len(bs), hb, hu, tol, restart, maxit, ps, reps)
+        if st not in (OK, ENOCONV):
+            self._check(st, "gmres_host_batch")
+        return [{"iterations": r.iterations, "converged": bool(r.converged), "relres_true": r.relres_true}
+                for r in reps]
 
     def device_status(self) -> int:
         with self._on_device():

@@ -552,6 +552,11 @@ void cnpint_destroy(cnpint_ctx* c) {
   cudaStreamSynchronize(c->stream);  // the caller may release the workspace right after this call
   prof_free(c);
   cnp_shard_free(c);
+  if (c->s_in) {
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->s_in);
+    cudaStreamDestroy(c->s_out);
+  }
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   delete c;
 }
@@ -1083,6 +1088,61 @@ cnpint_status cnpint_apply_A_host(cnpint_ctx* c, const double* h_u, double* h_y)
   if ((st = d2h_vec(c, c->d_io2, h_y, c->d_io3))) return st;
   CK(cudaStreamSynchronize(c->stream));
   return CNPINT_OK;
+}
+
+// Pipelined end-to-end solves: solve i on the handle's stream while the H2D copy of b_{i+1} (stream
+// s_in) and the D2H copy of u_{i−1} (stream s_out) move over PCIe in both directions.  Staging: d_stage
+// holds stage_in[2] and stage_out[2] (packed layout); b and u live in io2 / io3 as in cnpint_gmres_host.
+cnpint_status cnpint_gmres_host_batch(cnpint_ctx* c, int count, const double* const* h_b, double* const* h_u,
+                                      double tol, int restart, int maxit, double* d_stage, cnpint_gmres_report* reps) {
+  if (!c || count < 1 || !h_b || !h_u || !d_stage || ((uintptr_t)d_stage & 15)) return CNPINT_EINVAL;
+  for (int i = 0; i < count; ++i)
+    if (!h_b[i] || !h_u[i]) return CNPINT_EINVAL;
+  if (!c->s_in) {
+    CK(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* ev_in = c->ev;
+  cudaEvent_t* ev_rep = c->ev + 2;
+  cudaEvent_t* ev_ready = c->ev + 4;
+  cudaEvent_t* ev_done = c->ev + 6;
+  const size_t bytes = (size_t)c->N * c->ny * c->nx * sizeof(double);
+  double* stage_in[2] = {d_stage, d_stage + c->vec};
+  double* stage_out[2] = {d_stage + 2 * c->vec, d_stage + 3 * c->vec};
+  double* db = c->d_io2;
+  double* du = c->d_io3;
+  auto h2d = [&](int i) -> cnpint_status {
+    const int s = i & 1;
+    if (i >= 2) CK(cudaStreamWaitEvent(c->s_in, ev_rep[s], 0));  // stage_in[s] consumed by solve i − 2
+    CK(cudaMemcpyAsync(stage_in[s], h_b[i], bytes, cudaMemcpyHostToDevice, c->s_in));
+    CK(cudaEventRecord(ev_in[s], c->s_in));
+    return CNPINT_OK;
+  };
+  cnpint_status first_err = CNPINT_OK;
+  if (cnpint_status st = h2d(0)) return st;
+  if (count > 1)
+    if (cnpint_status st = h2d(1)) return st;
+  for (int i = 0; i < count; ++i) {
+    const int s = i & 1;
+    CK(cudaStreamWaitEvent(c->stream, ev_in[s], 0));
+    CK(launch_repack(c, stage_in[s], db, 0));
+    CK(cudaEventRecord(ev_rep[s], c->stream));
+    if (i + 2 < count)
+      if (cnpint_status st = h2d(i + 2)) return st;
+    cnpint_status st = cnpint_gmres(c, db, du, tol, restart, maxit, reps ? reps + i : nullptr);
+    if (st != CNPINT_OK && st != CNPINT_ENOCONV) return st;
+    if (st != CNPINT_OK && first_err == CNPINT_OK) first_err = st;
+    if (i >= 2) CK(cudaStreamWaitEvent(c->stream, ev_done[s], 0));  // stage_out[s] copied out by solve i − 2
+    CK(launch_repack(c, du, stage_out[s], 1));
+    CK(cudaEventRecord(ev_ready[s], c->stream));
+    CK(cudaStreamWaitEvent(c->s_out, ev_ready[s], 0));
+    CK(cudaMemcpyAsync(h_u[i], stage_out[s], bytes, cudaMemcpyDeviceToHost, c->s_out));
+    CK(cudaEventRecord(ev_done[s], c->s_out));
+  }
+  CK(cudaStreamSynchronize(c->s_out));
+  CK(cudaStreamSynchronize(c->stream));
+  return first_err;
 }
 
 cnpint_status cnpint_gmres_host(cnpint_ctx* c, const double* h_b, double* h_u, double tol, int restart, int maxit,

@@ -127,6 +127,8 @@ struct cnpint_ctx {
   double* d_hmap;      // its device alias
   PostOp post;         // pending post-fold operation for the next reducing launch (op 0 = none)
   struct ShardInfo* shard;  // 1D x-sharded handle (shard.cu, NEXT #3), null for a whole-domain handle
+  cudaStream_t s_in, s_out;  // copy streams of cnpint_gmres_host_batch (created on first use)
+  cudaEvent_t ev[8];         // its events: in[2], repacked[2], out_ready[2], out_done[2]
   const double* last_v0;  // Ṽ_0 of the last completed GMRES cycle (b itself in the first), test hook
   int last_nv;            // basis vectors Ṽ_0..Ṽ_{last_nv−1} of that cycle
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory

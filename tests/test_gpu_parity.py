@@ -457,6 +457,17 @@ def test_host_entry_points_match_device(name):
     u = s.empty()
     s.gmres(s.to_device(b), u, w.tol, w.restart)
     assert rel(uh, s.to_host(u)) == 0.0 and rh["converged"]
+    # the pipelined batch (copies of the neighbouring solves overlapped on two copy streams): five
+    # different right-hand sides, two alternating pinned output buffers per pair, bitwise the device solves
+    bs = [torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy() for _ in range(5)]
+    for i, bb in enumerate(bs):
+        bb[...] = b * (1.0 + i) + 0.1 * i * synth.random_vectors(w, 1, 60 + i)[0]
+    us = [torch.empty(b.shape, dtype=torch.float64, pin_memory=True).numpy() for _ in range(5)]
+    reps = s.gmres_host_batch(bs, us, w.tol, w.restart)
+    for bb, ub, rb in zip(bs, us, reps):
+        ud = s.empty()
+        s.gmres(s.to_device(bb), ud, w.tol, w.restart)
+        assert rb["converged"] and rel(ub, s.to_host(ud)) == 0.0
 
 
 def test_invalid_arguments():
