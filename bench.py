@@ -149,9 +149,11 @@ def ncu_traffic(kernel: str, workload: str):
     same workload (profiles/ncu_traffic.json, written from profiles/r01_ncu_full_summary.txt)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
-        d = json.load(open(p)).get(kernel)
-        if d and d.get("workload") == workload:
-            return d["bytes_per_launch"], d.get("algo_bytes_this_launch"), d.get("launch")
+        tab = json.load(open(p))
+        for key in (f"{kernel}@{workload}", kernel):
+            d = tab.get(key)
+            if d and d.get("workload") == workload:
+                return d["bytes_per_launch"], d.get("algo_bytes_this_launch"), d.get("launch")
     return None, None, None
 
 
