@@ -376,7 +376,7 @@ def run_gpu(args, rank, world, local):
     }
     del s, b
     torch.cuda.empty_cache()
-    if not args.no_table:
+    if not args.no_table and world == 1:  # the per-workload table is a single-GPU measurement
         result["workloads"] = workload_table(args, peak, stream)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(w)
