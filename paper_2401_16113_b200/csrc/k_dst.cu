@@ -397,6 +397,8 @@ static cudaError_t run_dst_t(cnpint_ctx* c, const double* in, double* out, const
 
 cudaError_t launch_dst2(cnpint_ctx* c, bool ypass, const double* in, double* out, const double* pre,
                         const double* post, int accumulate);
+cudaError_t launch_dst4_x(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
+                          int accumulate);
 
 template <bool YPASS>
 static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
@@ -415,6 +417,8 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   // grids — parity-green but not faster on B200 (x pass 0.97-1.04x of the kernels below, y pass
   // 0.4x: 511 small TMA bulk copies per tile issue too slowly; profiles/r02_dst2_ab.txt), so opt-in
   if ((c->debug & 256) && !(c->debug & 32)) e = launch_dst2(c, YPASS, in, out, pre, post, accumulate);
+  // debug bit 4096: the lean register x pass (k_dst4.cu)
+  if (!YPASS && (c->debug & 4096) && !(c->debug & (32 | 256))) e = launch_dst4_x(c, in, out, pre, post, accumulate);
   if (e != cudaErrorNotSupported) {
     cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
     return e;

@@ -1,0 +1,235 @@
+// K5, lean x pass (round 2): one axis of W⁻¹ / W (the diagonal-similarity reading of
+// k_dst.cu) on rows, as a half-length sine transform with a low instruction count per sample.
+//
+// Why another kernel: ncu's SASS counts (profiles/r02_dst_lean.txt) show the Stockham x pass executing
+// ≈ 234 thread-instructions per sample (47 IMAD + 22 LEA of index arithmetic, 38 DADD of the odd-extension
+// FFT, 17 LDS + 8 STS) and keeping 86 % of its time with every HBM access removed: it is bound by issue
+// and shared-memory latency, not by HBM.  This kernel does the same transform with ≈ 30-40:
+//   * half-length DST-I (see k_dst2.cu): y_j = A_j f_j + B_j f_{M−j} with A_j = (sin(jπ/M) + ½) g_j,
+//     B_j = (sin(jπ/M) − ½) g_{M−j} (the pre-scale g = ρ^{−j} folded in: 2 FMAs per line and sample),
+//     z = y^a + i y^b, one M-point complex FFT for two rows, F_{2k} = −Im Y_k, F_{2k+1} a prefix sum;
+//   * a line pair is owned by TP = M/8 threads for its whole life (64 at M = 512): samples are loaded
+//     from HBM straight into registers (coalesced rows, the mirrored sample f_{M−j} from L1), the FFT is
+//     three radix-8 register passes whose exchanges stay in the pair's 8-KB shared region behind
+//     named barriers of the pair alone (no CTA-wide barrier), the prefix sum is a warp-shuffle scan,
+//     results leave as 16-B stores;
+//   * all index arithmetic is compile time except the pair's row; tables (ω_M, A/B, post-scale) are
+//     built once per persistent CTA; 4 CTAs × 256 threads per SM (64 registers, 32 warps) hide latency.
+#include "common.cuh"
+#include "internal.h"
+
+#include "fft_device.cuh"
+
+namespace {
+
+CNP_DEV int zpos4(int k) { return k ^ ((k >> 3) & 7); }
+
+CNP_DEV void pair_sync(int id, int nthreads) {
+  if (nthreads >= 64) asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+  else __syncwarp();
+}
+
+}  // namespace
+
+template <int LOGM>
+struct D4Plan {
+  static constexpr int M = 1 << LOGM, H = M / 2, n = M - 1;
+  static constexpr int R1 = 8;
+  static constexpr int R2 = LOGM == 7 ? 4 : 8;
+  static constexpr int R3 = M / (R1 * R2);   // 8, 4, 4, 1 for LOGM = 9, 8, 7, 6
+  static constexpr int TP = M / 8;           // threads per line pair
+  static constexpr int NT = 256;
+  static constexpr int P = NT / TP;          // line pairs per CTA
+  static constexpr int I1 = (M / R1) / TP, I2 = (M / R2) / TP, I3 = (M / R3) / TP;
+  static constexpr size_t off_tw = (size_t)P * M * 16;        // pair regions: P × M complex
+  static constexpr size_t off_ab = off_tw + (size_t)M * 16;   // ω_M^q
+  static constexpr size_t off_post = off_ab + (size_t)M * 16; // (A_j, B_j)
+  static constexpr size_t bytes = off_post + (size_t)M * 8;   // post[x]
+};
+
+#ifndef DST4_MINB
+#define DST4_MINB 4
+#endif
+
+template <int LOGM>
+__global__ void __launch_bounds__(256, DST4_MINB)
+    k_dst4(const double* __restrict__ in, double* __restrict__ out, int nlines, int64_t ld,
+           const double* __restrict__ pre, const double* __restrict__ post, const double2* __restrict__ tw2M,
+           int accumulate, int debug_sign) {
+  using PL = D4Plan<LOGM>;
+  constexpr int M = PL::M, H = PL::H, n = PL::n, TP = PL::TP, P = PL::P;
+  constexpr int R1 = PL::R1, R2 = PL::R2, R3 = PL::R3;
+  char* const smem = reinterpret_cast<char*>(fft_smem);
+  double2* const twM = reinterpret_cast<double2*>(smem + PL::off_tw);
+  double2* const ab = reinterpret_cast<double2*>(smem + PL::off_ab);
+  double* const post_s = reinterpret_cast<double*>(smem + PL::off_post);
+  const int tid = threadIdx.x, pr = tid / TP, r = tid % TP;
+  double2* const A = reinterpret_cast<double2*>(smem) + pr * M;  // this pair's exchange region
+  // ---- tables (create-time constants): ω_M^q = ω_{2M}^{2q}; A_j, B_j; post-scale
+  const double sg = debug_sign ? -1.0 : 1.0;
+  for (int q = tid; q < M; q += PL::NT) {
+    double2 w = tw2M[2 * q];
+    w.y *= sg;
+    twM[q] = w;
+    double a = 0.0, b = 0.0;
+    if (q > 0) {
+      const double s = -tw2M[q].y;  // sin(qπ/M)
+      const double gj = pre ? pre[q - 1] : 1.0, gm = pre ? pre[M - q - 1] : 1.0;
+      a = (s + 0.5) * gj;
+      b = (s - 0.5) * gm;
+    }
+    ab[q] = make_double2(a, b);
+    post_s[q] = (q < n) ? (post ? post[q] : 1.0) : 0.0;  // x = n is the padding column: written as 0
+  }
+  __syncthreads();
+  pdl_enter();  // PDL: the rows below come from the previous kernel
+  const int npairs = nlines / 2;  // N·ny is even
+  const int stride = gridDim.x * P;
+  const int first = blockIdx.x * P;
+  const int iters = first < npairs ? (npairs - first + stride - 1) / stride : 0;  // uniform per CTA
+  const int bar = 1 + pr;
+  for (int it = 0; it < iters; ++it) {
+    const int g = first + pr + it * stride;
+    const bool act = g < npairs;
+    const double* ra = in + (int64_t)(2 * g) * ld;  // rows 2g (line a) and 2g + 1 (line b)
+    const double* rb = ra + ld;
+    // ---- step 1: z_j = y^a_j + i y^b_j for j = m + (M/R1) n1, loaded straight from HBM
+#pragma unroll
+    for (int i1 = 0; i1 < PL::I1; ++i1) {
+      const int m = r + i1 * TP;
+      double2 v[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) {
+        const int j = m + (M / R1) * n1;
+        double2 z = make_double2(0.0, 0.0);
+        if (j > 0 && act) {
+          const double2 c = ab[j];
+          const double fa = __ldg(ra + j - 1), fam = __ldg(ra + M - j - 1);
+          const double fb = __ldg(rb + j - 1), fbm = __ldg(rb + M - j - 1);
+          z = make_double2(fma(c.x, fa, c.y * fam), fma(c.x, fb, c.y * fbm));
+        }
+        v[n1] = z;
+      }
+      dftR<R1, false>(v);
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) A[k1 * (M / R1) + m] = k1 ? cmul(v[k1], twM[m * k1]) : v[0];
+    }
+    pair_sync(bar, TP);
+    // ---- step 2: item (k1, m3): B[k1][m3 + R3 m2] → DFT_R2 → ω_M^{R1 m3 k2} → C (in place, swizzled)
+    double2 u[PL::I2][R2];
+#pragma unroll
+    for (int i2 = 0; i2 < PL::I2; ++i2) {
+      const int q = r + i2 * TP, m3 = q % R3, k1 = q / R3;
+#pragma unroll
+      for (int m2 = 0; m2 < R2; ++m2) u[i2][m2] = A[k1 * (M / R1) + m3 + R3 * m2];
+      dftR<R2, false>(u[i2]);
+    }
+    pair_sync(bar, TP);
+#pragma unroll
+    for (int i2 = 0; i2 < PL::I2; ++i2) {
+      const int q = r + i2 * TP, m3 = q % R3, k1 = q / R3;
+#pragma unroll
+      for (int k2 = 0; k2 < R2; ++k2)
+        A[(k2 * R1 + k1) * R3 + (m3 ^ (k1 & (R3 - 1)))] = (k2 && m3) ? cmul(u[i2][k2], twM[R1 * m3 * k2]) : u[i2][k2];
+    }
+    pair_sync(bar, TP);
+    // ---- step 3: item (k1, k2): C → DFT_R3 → Z_k, k = k1 + R1 k2 + R1 R2 k3 (in place, swizzled)
+    double2 w3[PL::I3][R3];
+#pragma unroll
+    for (int i3 = 0; i3 < PL::I3; ++i3) {
+      const int q = r + i3 * TP, k1 = q % R1, k2 = q / R1;
+#pragma unroll
+      for (int m3 = 0; m3 < R3; ++m3) w3[i3][m3] = A[(k2 * R1 + k1) * R3 + (m3 ^ (k1 & (R3 - 1)))];
+      if constexpr (R3 > 1) dftR<R3, false>(w3[i3]);
+    }
+    pair_sync(bar, TP);
+#pragma unroll
+    for (int i3 = 0; i3 < PL::I3; ++i3) {
+      const int q = r + i3 * TP, k1 = q % R1, k2 = q / R1;
+#pragma unroll
+      for (int k3 = 0; k3 < R3; ++k3) A[zpos4(k1 + R1 * k2 + R1 * R2 * k3)] = w3[i3][k3];
+    }
+    pair_sync(bar, TP);
+    // ---- post: line ℓ (lanes [0, TP/2) → a, [TP/2, TP) → b); lane q owns k ∈ [8q, 8q+8]
+    {
+      const int ln = r / (TP / 2), q = r % (TP / 2);
+      double Rk[8], Ik[8];
+      double loc = 0.0;
+#pragma unroll
+      for (int i = 0; i <= 8; ++i) {
+        const int k = 8 * q + i;
+        const double2 Zk = A[zpos4(k & (M - 1))];
+        const double2 Zm = A[zpos4((M - k) & (M - 1))];
+        // Y^a = (Z_k + conj Z_{M−k})/2, Y^b = (Z_k − conj Z_{M−k})/(2i)
+        const double re = ln == 0 ? 0.5 * (Zk.x + Zm.x) : 0.5 * (Zk.y + Zm.y);
+        const double im = ln == 0 ? 0.5 * (Zk.y - Zm.y) : 0.5 * (Zm.x - Zk.x);
+        if (i < 8) {
+          Rk[i] = (k == 0) ? 0.5 * re : re;
+          loc += Rk[i];
+        }
+        if (i > 0) Ik[i - 1] = (k < H) ? -im : 0.0;  // F_{2k} at x = 2k − 1 (F_M: the padding column)
+      }
+      constexpr int W = TP / 2 < 32 ? TP / 2 : 32;
+      double incl = loc;
+#pragma unroll
+      for (int o = 1; o < W; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, incl, o, W);
+        if (q % W >= o) incl += t;
+      }
+      double run = incl - loc;
+      if (act) {
+        double* orow = out + (int64_t)(2 * g + ln) * ld + 16 * q;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          run += Rk[i];
+          const int x = 16 * q + 2 * i;  // outputs x (F_{2k+1}) and x + 1 (F_{2k+2}), k = 8q + i
+          double2 o2 = make_double2(run * post_s[x], Ik[i] * post_s[x + 1]);
+          double2* dst = reinterpret_cast<double2*>(orow + 2 * i);
+          if (accumulate) {
+            const double2 pv = *dst;
+            o2.x += pv.x;
+            o2.y += pv.y;
+          }
+          stg_cs2(dst, o2);
+        }
+      }
+    }
+    pair_sync(bar, TP);  // the region is free for the next pair's step 1
+  }
+}
+
+template <int LOGM>
+static cudaError_t run_dst4(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
+                            int accumulate) {
+  using PL = D4Plan<LOGM>;
+  auto kern = k_dst4<LOGM>;
+  int grid_max = 0;
+  cudaError_t ce = cnp_dev_cached((const void*)kern, &grid_max, [&](int* v) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PL::NT, PL::bytes);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    *v = per_sm * c->num_sms;
+    return cudaSuccess;
+  });
+  if (ce != cudaSuccess) return ce;
+  const int nlines = c->N * c->ny;
+  const int ntiles = (nlines / 2 + PL::P - 1) / PL::P;
+  const int grid = ntiles < grid_max ? ntiles : grid_max;
+  return cnp_launch(c, kern, dim3(grid), dim3(PL::NT), PL::bytes, in, out, nlines, c->ld, pre, post,
+                    (const double2*)c->d_twx, accumulate, c->debug & 1);
+}
+
+// x pass (rows) through the lean kernel when nx + 1 ∈ {64, …, 512} and ld = nx + 1; else NotSupported
+cudaError_t launch_dst4_x(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
+                          int accumulate) {
+  if (c->ld != c->nx + 1) return cudaErrorNotSupported;
+  switch (c->nx + 1) {
+    case 64: return run_dst4<6>(c, in, out, pre, post, accumulate);
+    case 128: return run_dst4<7>(c, in, out, pre, post, accumulate);
+    case 256: return run_dst4<8>(c, in, out, pre, post, accumulate);
+    case 512: return run_dst4<9>(c, in, out, pre, post, accumulate);
+    default: return cudaErrorNotSupported;
+  }
+}
