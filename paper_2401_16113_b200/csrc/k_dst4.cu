@@ -41,10 +41,13 @@ struct D4Plan {
   static constexpr int NT = 256;
   static constexpr int P = NT / TP;          // line pairs per CTA
   static constexpr int I1 = (M / R1) / TP, I2 = (M / R2) / TP, I3 = (M / R3) / TP;
-  static constexpr size_t off_tw = (size_t)P * M * 16;        // pair regions: P × M complex
-  static constexpr size_t off_ab = off_tw + (size_t)M * 16;   // ω_M^q
-  static constexpr size_t off_post = off_ab + (size_t)M * 16; // (A_j, B_j)
-  static constexpr size_t bytes = off_post + (size_t)M * 8;   // post[x]
+  // tables laid out so that a warp's reads hit distinct banks (ncu: the plain ω_M table and a
+  // post-scale read at stride 16 doubles cost 2-8× the ideal shared wavefronts)
+  static constexpr size_t off_tw = (size_t)P * M * 16;          // pair regions: P × M complex
+  static constexpr size_t off_t2 = off_tw + (size_t)M * 16;     // T1[k1][m] = ω_M^{m k1}
+  static constexpr size_t off_ab = off_t2 + (size_t)(M / R1) * 16;  // T2[k2][m3] = ω_M^{R1 m3 k2}
+  static constexpr size_t off_post = off_ab + (size_t)M * 16;   // (A_j, B_j)
+  static constexpr size_t bytes = off_post + (size_t)M * 8;     // post pairs [i][q]
 };
 
 #ifndef DST4_MINB
@@ -60,17 +63,29 @@ __global__ void __launch_bounds__(256, DST4_MINB)
   constexpr int M = PL::M, H = PL::H, n = PL::n, TP = PL::TP, P = PL::P;
   constexpr int R1 = PL::R1, R2 = PL::R2, R3 = PL::R3;
   char* const smem = reinterpret_cast<char*>(fft_smem);
-  double2* const twM = reinterpret_cast<double2*>(smem + PL::off_tw);
+  double2* const T1 = reinterpret_cast<double2*>(smem + PL::off_tw);
+  double2* const T2 = reinterpret_cast<double2*>(smem + PL::off_t2);
   double2* const ab = reinterpret_cast<double2*>(smem + PL::off_ab);
-  double* const post_s = reinterpret_cast<double*>(smem + PL::off_post);
+  double2* const post2 = reinterpret_cast<double2*>(smem + PL::off_post);
   const int tid = threadIdx.x, pr = tid / TP, r = tid % TP;
   double2* const A = reinterpret_cast<double2*>(smem) + pr * M;  // this pair's exchange region
   // ---- tables (create-time constants): ω_M^q = ω_{2M}^{2q}; A_j, B_j; post-scale
   const double sg = debug_sign ? -1.0 : 1.0;
-  for (int q = tid; q < M; q += PL::NT) {
-    double2 w = tw2M[2 * q];
+  // ω_M^q = ω_{2M}^{2q} (q < M, exact table); T1[k1·(M/R1) + m] = ω_M^{(m k1) mod M},
+  // T2[k2·R3 + m3] = ω_M^{R1 m3 k2}; post2[i·(TP/2) + q] = (post[16q + 2i], post[16q + 2i + 1])
+  auto omega = [&](int e) {
+    double2 w = tw2M[2 * (e & (M - 1))];
     w.y *= sg;
-    twM[q] = w;
+    return w;
+  };
+  for (int q = tid; q < M; q += PL::NT) {
+    const int k1 = q / (M / R1), m = q % (M / R1);
+    T1[q] = omega(m * k1);
+    if (q < M / R1) T2[q] = omega(R1 * (q % R3) * (q / R3));
+    if (q < M / 2) {
+      const int i = q / (TP / 2), l = q % (TP / 2), x = 16 * l + 2 * i;
+      post2[q] = make_double2(x < n ? (post ? post[x] : 1.0) : 0.0, x + 1 < n ? (post ? post[x + 1] : 1.0) : 0.0);
+    }
     double a = 0.0, b = 0.0;
     if (q > 0) {
       const double s = -tw2M[q].y;  // sin(qπ/M)
@@ -79,7 +94,6 @@ __global__ void __launch_bounds__(256, DST4_MINB)
       b = (s - 0.5) * gm;
     }
     ab[q] = make_double2(a, b);
-    post_s[q] = (q < n) ? (post ? post[q] : 1.0) : 0.0;  // x = n is the padding column: written as 0
   }
   __syncthreads();
   pdl_enter();  // PDL: the rows below come from the previous kernel
@@ -112,7 +126,7 @@ __global__ void __launch_bounds__(256, DST4_MINB)
       }
       dftR<R1, false>(v);
 #pragma unroll
-      for (int k1 = 0; k1 < R1; ++k1) A[k1 * (M / R1) + m] = k1 ? cmul(v[k1], twM[m * k1]) : v[0];
+      for (int k1 = 0; k1 < R1; ++k1) A[k1 * (M / R1) + m] = k1 ? cmul(v[k1], T1[k1 * (M / R1) + m]) : v[0];
     }
     pair_sync(bar, TP);
     // ---- step 2: item (k1, m3): B[k1][m3 + R3 m2] → DFT_R2 → ω_M^{R1 m3 k2} → C (in place, swizzled)
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(256, DST4_MINB)
       const int q = r + i2 * TP, m3 = q % R3, k1 = q / R3;
 #pragma unroll
       for (int k2 = 0; k2 < R2; ++k2)
-        A[(k2 * R1 + k1) * R3 + (m3 ^ (k1 & (R3 - 1)))] = (k2 && m3) ? cmul(u[i2][k2], twM[R1 * m3 * k2]) : u[i2][k2];
+        A[(k2 * R1 + k1) * R3 + (m3 ^ (k1 & (R3 - 1)))] = (k2 && m3) ? cmul(u[i2][k2], T2[k2 * R3 + m3]) : u[i2][k2];
     }
     pair_sync(bar, TP);
     // ---- step 3: item (k1, k2): C → DFT_R3 → Z_k, k = k1 + R1 k2 + R1 R2 k3 (in place, swizzled)
@@ -182,8 +196,9 @@ __global__ void __launch_bounds__(256, DST4_MINB)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           run += Rk[i];
-          const int x = 16 * q + 2 * i;  // outputs x (F_{2k+1}) and x + 1 (F_{2k+2}), k = 8q + i
-          double2 o2 = make_double2(run * post_s[x], Ik[i] * post_s[x + 1]);
+          // outputs x = 16q + 2i (F_{2k+1}) and x + 1 (F_{2k+2}), k = 8q + i; x = n is the padding column
+          const double2 ps = post2[i * (TP / 2) + q];
+          double2 o2 = make_double2(run * ps.x, Ik[i] * ps.y);
           double2* dst = reinterpret_cast<double2*>(orow + 2 * i);
           if (accumulate) {
             const double2 pv = *dst;
