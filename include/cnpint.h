@@ -307,7 +307,8 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * Ṽᵀ Ṽ_j is reduced inside the matvec (K7); 256 = the pipelined half-length DST kernel
  * (k_dst2.cu: TMA bulk-copy ring, n + 1 ∈ {64, …, 512}, square grids) for the 2D sine passes;
  * 1024 = the register DST kernel for every 2D sine pass with 2(n+1) ∈ {256, 512, 1024} (A/B);
- * 2048 = fault injection: every 1D shifted solve reports a singular pivot (status-word tests). */
+ * 2048 = fault injection: every 1D shifted solve reports a singular pivot (status-word tests);
+ * 4096 = the first-generation Stockham x pass instead of the lean register x pass (k_dst4.cu). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

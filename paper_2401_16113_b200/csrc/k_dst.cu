@@ -417,8 +417,11 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   // grids — parity-green but not faster on B200 (x pass 0.97-1.04x of the kernels below, y pass
   // 0.4x: 511 small TMA bulk copies per tile issue too slowly; profiles/r02_dst2_ab.txt), so opt-in
   if ((c->debug & 256) && !(c->debug & 32)) e = launch_dst2(c, YPASS, in, out, pre, post, accumulate);
-  // debug bit 4096: the lean register x pass (k_dst4.cu)
-  if (!YPASS && (c->debug & 4096) && !(c->debug & (32 | 256))) e = launch_dst4_x(c, in, out, pre, post, accumulate);
+  // x pass: the lean register kernel (k_dst4.cu) for n + 1 ∈ {64, …, 512} — measured faster than the
+  // Stockham pass at every BASELINE size (c4 237 → 217 µs, c5 n511 2027 → 1660 µs, profiles/r02_dst4_ab.txt);
+  // debug bit 4096 keeps the Stockham / register kernels below (A/B, cross-check)
+  if (!YPASS && e == cudaErrorNotSupported && !(c->debug & (32 | 256 | 4096)))
+    e = launch_dst4_x(c, in, out, pre, post, accumulate);
   if (e != cudaErrorNotSupported) {
     cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
     return e;
