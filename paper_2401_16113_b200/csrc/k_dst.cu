@@ -399,6 +399,8 @@ cudaError_t launch_dst2(cnpint_ctx* c, bool ypass, const double* in, double* out
                         const double* post, int accumulate);
 cudaError_t launch_dst4_x(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
                           int accumulate);
+cudaError_t launch_dst5_y(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
+                          int accumulate);
 
 template <bool YPASS>
 static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const double* pre, const double* post,
@@ -422,6 +424,9 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   // debug bit 4096 keeps the Stockham / register kernels below (A/B, cross-check)
   if (!YPASS && e == cudaErrorNotSupported && !(c->debug & (32 | 256 | 4096)))
     e = launch_dst4_x(c, in, out, pre, post, accumulate);
+  // debug bit 8192: the lean y pass (k_dst5.cu)
+  if (YPASS && e == cudaErrorNotSupported && (c->debug & 8192) && !(c->debug & (32 | 256)))
+    e = launch_dst5_y(c, in, out, pre, post, accumulate);
   if (e != cudaErrorNotSupported) {
     cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));
     return e;

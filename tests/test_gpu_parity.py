@@ -222,7 +222,7 @@ def test_time_fft_paths(name, debug):
 
 
 @pytest.mark.parametrize("name", ["2d_small", "2d_mid", "2d_n255_N8", "2d_n63_N16", "2d_n127_N16", "2d_n511_N4"])
-@pytest.mark.parametrize("debug", [0, 32, 256, 4096])
+@pytest.mark.parametrize("debug", [0, 32, 256, 4096, 8192])
 def test_dst_paths(name, debug):
     """2D P⁻¹ with the default DST kernels (debug 0: the lean register x pass k_dst4 for n + 1 ∈ {64, …,
     512}, register / Stockham y pass), the first-generation x pass (debug 4096), the pipelined
