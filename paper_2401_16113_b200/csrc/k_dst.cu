@@ -424,8 +424,9 @@ static cudaError_t run_dst(cnpint_ctx* c, const double* in, double* out, const d
   // debug bit 4096 keeps the Stockham / register kernels below (A/B, cross-check)
   if (!YPASS && e == cudaErrorNotSupported && !(c->debug & (32 | 256 | 4096)))
     e = launch_dst4_x(c, in, out, pre, post, accumulate);
-  // debug bit 8192: the lean y pass (k_dst5.cu)
-  if (YPASS && e == cudaErrorNotSupported && (c->debug & 8192) && !(c->debug & (32 | 256)))
+  // y pass: the lean kernel (k_dst5.cu) on square grids with n + 1 ∈ {64, …, 512} (c5 n511 y pass
+  // 2163 → 1271 µs, c4 182 → 156 µs, profiles/r02_dst5_ab.txt); debug bit 8192 keeps the first generation
+  if (YPASS && e == cudaErrorNotSupported && !(c->debug & (32 | 256 | 8192)))
     e = launch_dst5_y(c, in, out, pre, post, accumulate);
   if (e != cudaErrorNotSupported) {
     cnp_prof_end(c, kid, (accumulate ? 24.0 : 16.0) * cnp_units(c));

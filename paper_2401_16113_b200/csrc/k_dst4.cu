@@ -191,22 +191,34 @@ __global__ void __launch_bounds__(256, DST4_MINB)
         if (q % W >= o) incl += t;
       }
       double run = incl - loc;
-      if (act) {
-        double* orow = out + (int64_t)(2 * g + ln) * ld + 16 * q;
+      pair_sync(bar, TP);  // every Z read: the region takes the two staged output lines
+      double* sl = reinterpret_cast<double*>(A) + ln * M;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          run += Rk[i];
-          // outputs x = 16q + 2i (F_{2k+1}) and x + 1 (F_{2k+2}), k = 8q + i; x = n is the padding column
-          const double2 ps = post2[i * (TP / 2) + q];
-          double2 o2 = make_double2(run * ps.x, Ik[i] * ps.y);
-          double2* dst = reinterpret_cast<double2*>(orow + 2 * i);
-          if (accumulate) {
-            const double2 pv = *dst;
-            o2.x += pv.x;
-            o2.y += pv.y;
-          }
-          stg_cs2(dst, o2);
+      for (int i = 0; i < 8; ++i) {
+        run += Rk[i];
+        // outputs x = 16q + 2i (F_{2k+1}) and x + 1 (F_{2k+2}), k = 8q + i; x = n is the padding column
+        const double2 ps = post2[i * (TP / 2) + q];
+        const int x = 16 * q + 2 * i;
+        sl[x ^ ((x >> 4) & 15)] = run * ps.x;           // XOR swizzle: 16 lanes → distinct banks
+        sl[(x + 1) ^ ((x >> 4) & 15)] = Ik[i] * ps.y;
+      }
+    }
+    pair_sync(bar, TP);
+    if (act) {  // the two rows leave as consecutive 16-B stores (512 B per warp instruction)
+      const double* sr = reinterpret_cast<const double*>(A);
+#pragma unroll
+      for (int e = r; e < M; e += TP) {  // e: double2 index over the 2 rows × M/2
+        const int ln = e / (M / 2), x = 2 * (e - ln * (M / 2));
+        const int p0 = x ^ ((x >> 4) & 15);       // x even: the pair (x, x+1) stays adjacent, maybe swapped
+        const double2 s2 = *reinterpret_cast<const double2*>(sr + ln * M + (p0 & ~1));
+        double2 o2 = (p0 & 1) ? make_double2(s2.y, s2.x) : s2;
+        double2* dst = reinterpret_cast<double2*>(out + (int64_t)(2 * g + ln) * ld + x);
+        if (accumulate) {
+          const double2 pv = *dst;
+          o2.x += pv.x;
+          o2.y += pv.y;
         }
+        stg_cs2(dst, o2);
       }
     }
     pair_sync(bar, TP);  // the region is free for the next pair's step 1
