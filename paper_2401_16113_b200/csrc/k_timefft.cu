@@ -232,8 +232,16 @@ cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int 
   if (tfft_cfg(c->N).ok && !(c->debug & 8)) return launch_tfft_inv(c, zhat, z, accumulate);
   return run_fft<1>(c, nullptr, zhat, z, nullptr, nullptr, accumulate);
 }
+cudaError_t launch_tpass2(cnpint_ctx* c, const double* in, double* out, const double* vscale);
+
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_pass_2d(c, in, out, vscale);
+  if ((c->debug & 16384) && !(c->debug & (8 | 64))) {  // the lean time pass (k_tpass2.cu), N = 256 / 512 / 1024
+    cnp_prof_begin(c, KID_TIMEPASS2D);
+    const cudaError_t e = launch_tpass2(c, in, out, vscale);
+    cnp_prof_end(c, KID_TIMEPASS2D, 16.0 * cnp_units(c));
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (!(c->debug & 8) && tpass_ok(c)) return launch_tpass_2d(c, in, out, vscale);  // N = 256, 512 (bit 64 off)
   if (tfft_cfg(c->N, 2).ok && !(c->debug & 8)) return launch_tfft_pass_2d(c, in, out, vscale);
   return run_fft<2>(c, in, nullptr, out, nullptr, vscale, 0);
