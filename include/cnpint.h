@@ -309,7 +309,9 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 1024 = the register DST kernel for every 2D sine pass with 2(n+1) ∈ {256, 512, 1024} (A/B);
  * 2048 = fault injection: every 1D shifted solve reports a singular pivot (status-word tests);
  * 4096 = the first-generation Stockham x pass instead of the lean register x pass (k_dst4.cu);
- * 8192 = the first-generation y pass (register / Stockham) instead of the lean y pass (k_dst5.cu). */
+ * 8192 = the first-generation y pass (register / Stockham) instead of the lean y pass (k_dst5.cu);
+ * 16384 = the lean 2D time pass (k_tpass2.cu) also at N = 512 (default at N = 256, 1024; debug 64 turns
+ * both register time passes off in favour of the cluster kernel). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -236,7 +236,10 @@ cudaError_t launch_tpass2(cnpint_ctx* c, const double* in, double* out, const do
 
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_pass_2d(c, in, out, vscale);
-  if ((c->debug & 16384) && !(c->debug & (8 | 64))) {  // the lean time pass (k_tpass2.cu), N = 256 / 512 / 1024
+  // the lean time pass (k_tpass2.cu) at N = 256 and 1024 (c5 n511 N1024 2758 → 1990 µs, N256 577 → 417 µs;
+  // at N = 512 it ties k_tpass_r: 225 vs 222 µs, profiles/r02_tpass2_ab.txt); debug 16384 forces it at
+  // N = 512 too, debug 64 keeps the cluster kernel (and k_tpass_r off)
+  if (!(c->debug & (8 | 64)) && (c->N == 256 || c->N == 1024 || (c->debug & 16384))) {
     cnp_prof_begin(c, KID_TIMEPASS2D);
     const cudaError_t e = launch_tpass2(c, in, out, vscale);
     cnp_prof_end(c, KID_TIMEPASS2D, 16.0 * cnp_units(c));

@@ -248,8 +248,9 @@ def test_dst_paths(name, debug):
 @pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2", "2d_n15_N512", "2d_n31_N256"])
 @pytest.mark.parametrize("debug", [0, 16, 64, 16384])
 def test_timepass_2d_paths(name, debug):
-    """2D time pass: the three-phase four-step kernel (N >= 2048), the register kernel (N = 256, 512)
-    — both default (debug 0) — and the cluster kernel (debug 16 / 64) all give the oracle's P⁻¹."""
+    """2D time pass: the three-phase four-step kernel (N >= 2048), the lean register kernel k_tpass2
+    (N = 256, 1024; forced at 512 by debug 16384), the register kernel k_tpass_r (N = 512) — defaults
+    (debug 0) — and the cluster kernel (debug 64; debug 16 at N >= 2048) all give the oracle's P⁻¹."""
     w = SMALL[name]
     s = solver_for(w)
     s.set_debug(debug)
