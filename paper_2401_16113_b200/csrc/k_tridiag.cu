@@ -155,17 +155,6 @@ __global__ void __launch_bounds__(MAXT, 2)
   const int i0 = p < nlong ? p * (Lmin + 1) : nlong * (Lmin + 1) + (p - nlong) * Lmin;
   const int i1 = i0 + len;
   bool ok = true;
-  if (!TOEP && act) {
-    // variable rows: the chunk's coefficient rows (create-time constants) into L1 while the system's
-    // copy is in flight — the sweep's loads of lo/di/up sat on its dependency chain (ncu, c3:
-    // long-scoreboard stalls on them)
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(lo + i0));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(di + i0));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(up + i0));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(lo + i1 - 1));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(di + i1 - 1));
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(up + i1 - 1));
-  }
   cp_async_wait<0>();
   __syncthreads();
   Seg sg;
