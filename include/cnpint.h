@@ -216,7 +216,8 @@ int64_t cnpint_launch_count(const cnpint_ctx* ctx);
  * (0 <= kid < cnpint_kernel_name() == NULL), the summed event durations in ms, the launch count and
  * the ALGORITHMIC bytes those launches must move.  Classes:
  * 0 K1 matvec, 1 K2 time FFT, 2 K3 tridiagonal, 3 K4 inverse time FFT, 4 K6 2D time pass,
- * 5 K5 DST x, 6 K5 DST y, 7 K7 dots, 8 K7 update, 9 reductions, 10 GMRES scalar kernels. */
+ * 5 K5 DST x, 6 K5 DST y, 7 K7 dots, 8 K7 update, 9 reductions, 10 GMRES scalar kernels,
+ * 11 K5 fused x+y sine pass. */
 cnpint_status cnpint_profile_enable(cnpint_ctx* ctx, int on);
 cnpint_status cnpint_profile_read(cnpint_ctx* ctx, int kernel_class, double* ms_total, int64_t* launches,
                                   double* algo_bytes);
@@ -311,7 +312,8 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 4096 = the first-generation Stockham x pass instead of the lean register x pass (k_dst4.cu);
  * 8192 = the first-generation y pass (register / Stockham) instead of the lean y pass (k_dst5.cu);
  * 16384 = the lean 2D time pass (k_tpass2.cu) also at N = 512 (default at N = 256, 1024; debug 64 turns
- * both register time passes off in favour of the cluster kernel). */
+ * both register time passes off in favour of the cluster kernel); 32768 = the five-pass 2D P_α⁻¹
+ * (separate x and y sine passes) instead of the three-pass one with the fused sine pass (k_dstxy.cu). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -31,7 +31,7 @@ struct CnpProf {
 
 static const char* const KNAMES[KID_COUNT] = {"K1_matvec", "K2_time_fft", "K3_tridiag", "K4_time_ifft",
                                               "K6_time_pass_2d", "K5_dst_x", "K5_dst_y", "K7_dots",
-                                              "K7_update", "reduce", "K8_small"};
+                                              "K7_update", "reduce", "K8_small", "K5_dst_xy"};
 
 void cnp_prof_begin(cnpint_ctx* c, int kid) {
   CnpProf* p = (CnpProf*)c->prof;
@@ -87,6 +87,7 @@ void cnp_dev_cache_put(const void* key, int val) {
 }
 
 cudaError_t launch_reduce_n(cnpint_ctx* c, const double* part, int nparts, int stride, int ncols, double* out);
+cudaError_t launch_dstxy(cnpint_ctx* c, const double* in, double* out, int inverse, int accumulate);
 cudaError_t launch_dst_x_acc(cnpint_ctx* c, const double* in, double* out);
 
 namespace {
@@ -99,7 +100,7 @@ bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 struct Layout {
   size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
-  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status;
+  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status, xycnt;
   size_t total;
 };
 
@@ -185,6 +186,7 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   L.scal = take(16 * 8);
   L.status = take(64);
   L.dt = take((size_t)N * 8);  // d(t_{t+½}) of a time-dependent operator (cnpint_set_time_dependence)
+  L.xycnt = op->dim == 2 ? take((size_t)(N + 1) * 4) : 0;  // fused sine pass: per-slice counters + ticket
   L.total = off;
   return L;
 }
@@ -395,6 +397,23 @@ cnpint_status pinv_dev(cnpint_ctx* c, const double* in, const double* vscale, do
     double* a = (in == c->d_tmp1 || out == c->d_tmp1) ? c->d_io2 : c->d_tmp1;
     double* b = (in == c->d_tmp2 || out == c->d_tmp2) ? c->d_io2 : c->d_tmp2;
     if (a == b) b = c->d_io1;
+    if (!(c->debug & 32768)) {
+      // three HBM passes: W⁻¹ fused over both axes, the time pass, W fused (k_dstxy.cu; the scratch
+      // intermediate tmp3 stays in L2); debug bit 32768 keeps the five separate passes below
+      cnp_prof_begin(c, KID_DST_XY);
+      cudaError_t e = launch_dstxy(c, in, b, 0, 0);
+      cnp_prof_end(c, KID_DST_XY, 16.0 * cnp_units(c));
+      if (e == cudaSuccess) {
+        CK(launch_time_pass_2d(c, b, a, vscale));  // GMRES scale folded into the Γ-scaling
+        cnp_prof_begin(c, KID_DST_XY);
+        e = launch_dstxy(c, a, out, 1, accumulate);
+        cnp_prof_end(c, KID_DST_XY, (accumulate ? 24.0 : 16.0) * cnp_units(c));
+        CK(e);
+        return CNPINT_OK;
+      }
+      if (e != cudaErrorNotSupported) return cuda_fail(c, e, "launch_dstxy");
+      (void)cudaGetLastError();
+    }
     CK(launch_dst_x(c, in, a, nullptr, 0));
     CK(launch_dst_y(c, a, b, 0));
     CK(launch_time_pass_2d(c, b, a, vscale));  // GMRES scale folded into the Γ-scaling
@@ -524,6 +543,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_part = (double*)(w + L.part);
   if (restart_max >= 1) { c->d_G = (double*)(w + L.G); c->d_cg = (double*)(w + L.cg); }
   c->d_scal = (double*)(w + L.scal);
+  c->d_xycnt = op->dim == 2 ? (unsigned*)(w + L.xycnt) : nullptr;
   c->d_status = (int*)(w + L.status);
   c->d_counter = (unsigned*)(w + L.status + 32);
   // tables: build a host image of the table region [0, tables_end), upload, zero the rest

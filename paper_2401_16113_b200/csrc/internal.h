@@ -16,7 +16,7 @@
 // kernel classes for the per-class event profiler (cnpint_profile_*)
 enum {
   KID_MATVEC = 0, KID_FFT_FWD, KID_TRIDIAG, KID_FFT_INV, KID_TIMEPASS2D, KID_DST_X, KID_DST_Y,
-  KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_COUNT
+  KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_DST_XY, KID_COUNT
 };
 
 // K3 launch configuration (k_tridiag.cu): G warps per system, L = max rows per thread chunk,
@@ -89,6 +89,7 @@ struct cnpint_ctx {
   unsigned* d_fscnt;   // [nxb] per-block pass-A counters, then the work ticket (monotonic)
   unsigned fs_cnt;     // host mirror: Σ pass-A items per block over all launches so far
   unsigned fs_tick;    // host mirror: tickets consumed so far
+  unsigned* d_xycnt;   // 2D: [N] per-slice counters + the ticket of the fused sine pass (k_dstxy.cu)
   double* d_tmp1;      // [vec] scratch vectors
   double* d_tmp2;
   double* d_tmp3;
