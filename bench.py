@@ -177,12 +177,19 @@ def describe(w):
             f"({w.unknowns:,} fp64), T={w.T}, alpha={w.alpha}, GMRES({w.restart}) tol {w.tol}, x0=0")
 
 
+def fused_2d_sine(w, debug=0):
+    """True when the 2D P_α⁻¹ runs as three passes: the fused x+y sine pass k_dstxy (opt-in, debug
+    bit 32768; n + 1 ∈ {64, …, 512}, launch_dstxy in k_dstxy.cu).  The bench runs debug 0: five."""
+    return w.dim == 2 and w.n + 1 in (64, 128, 256, 512) and bool(debug & 32768)
+
+
 def pinv_structured_bytes(w):
     """Algorithmic bytes of one P_α⁻¹ as structured: 1D K2 + K3 + K4 (8 B in, 16 B per
-    half-spectrum complex out / in + out / in, 8 B out); 2D W⁻¹ (x, y), time pass, W (y, x): 5 × 16 B."""
+    half-spectrum complex out / in + out / in, 8 B out); 2D W⁻¹, time pass, W: 3 × 16 B with the fused
+    x+y sine pass, else W⁻¹ (x, y), time pass, W (y, x): 5 × 16 B."""
     if w.dim == 1:
         return 16.0 * w.unknowns + 32.0 * (w.N // 2 + 1) * w.m + 16.0 * w.unknowns
-    return 80.0 * w.unknowns
+    return (48.0 if fused_2d_sine(w) else 80.0) * w.unknowns
 
 
 def time_ops(s, w, stream, nvec, reps):

@@ -312,8 +312,9 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 4096 = the first-generation Stockham x pass instead of the lean register x pass (k_dst4.cu);
  * 8192 = the first-generation y pass (register / Stockham) instead of the lean y pass (k_dst5.cu);
  * 16384 = the lean 2D time pass (k_tpass2.cu) also at N = 512 (default at N = 256, 1024; debug 64 turns
- * both register time passes off in favour of the cluster kernel); 32768 = the five-pass 2D P_α⁻¹
- * (separate x and y sine passes) instead of the three-pass one with the fused sine pass (k_dstxy.cu). */
+ * both register time passes off in favour of the cluster kernel); 32768 = the three-pass 2D P_α⁻¹: W⁻¹
+ * and W each as one fused x+y sine pass (k_dstxy.cu, n + 1 ∈ {64, …, 512}; 48 instead of 80 B of HBM
+ * traffic per unknown, but no faster on B200: the passes are bound on chip, K5). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

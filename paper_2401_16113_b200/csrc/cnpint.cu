@@ -397,9 +397,10 @@ cnpint_status pinv_dev(cnpint_ctx* c, const double* in, const double* vscale, do
     double* a = (in == c->d_tmp1 || out == c->d_tmp1) ? c->d_io2 : c->d_tmp1;
     double* b = (in == c->d_tmp2 || out == c->d_tmp2) ? c->d_io2 : c->d_tmp2;
     if (a == b) b = c->d_io1;
-    if (!(c->debug & 32768)) {
+    if (c->debug & 32768) {
       // three HBM passes: W⁻¹ fused over both axes, the time pass, W fused (k_dstxy.cu; the scratch
-      // intermediate tmp3 stays in L2); debug bit 32768 keeps the five separate passes below
+      // intermediate tmp3 stays in L2).  Opt-in: it moves 48 instead of 80 B per unknown but measured
+      // 3-6 % slower than the five passes below (profiles/r02_dstxy_ab.txt): both are bound on chip.
       cnp_prof_begin(c, KID_DST_XY);
       cudaError_t e = launch_dstxy(c, in, b, 0, 0);
       cnp_prof_end(c, KID_DST_XY, 16.0 * cnp_units(c));
