@@ -100,7 +100,7 @@ bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 struct Layout {
   size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
-  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status, xycnt, vtab;
+  size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status, xycnt;
   size_t total;
 };
 
@@ -187,10 +187,6 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
   L.status = take(64);
   L.dt = take((size_t)N * 8);  // d(t_{t+½}) of a time-dependent operator (cnpint_set_time_dependence)
   L.xycnt = op->dim == 2 ? take((size_t)(N + 1) * 4) : 0;  // fused sine pass: per-slice counters + ticket
-  if (op->dim == 1 && !op->toeplitz) {  // K3 variable rows: tabulated merge tree (built on the device)
-    const TriCfg t = tri_cfg(nx, 0);
-    L.vtab = (!t.small && t.L > 0) ? take((size_t)(H + 1) * t.tabstride * 16) : 0;
-  }
   L.total = off;
   return L;
 }
@@ -549,7 +545,6 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   if (restart_max >= 1) { c->d_G = (double*)(w + L.G); c->d_cg = (double*)(w + L.cg); }
   c->d_scal = (double*)(w + L.scal);
   c->d_xycnt = op->dim == 2 ? (unsigned*)(w + L.xycnt) : nullptr;
-  c->d_vtab = L.vtab ? (double2*)(w + L.vtab) : nullptr;
   c->d_status = (int*)(w + L.status);
   c->d_counter = (unsigned*)(w + L.status + 32);
   // tables: build a host image of the table region [0, tables_end), upload, zero the rest
@@ -756,12 +751,6 @@ cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
   const size_t hi = L.tables_end;
   CK(cudaMemcpyAsync(c->ws + L.tw, img.data() + L.tw, hi - L.tw, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  // variable rows: the K3 merge-tree table depends on τ and the shifts (sk, 1/λ2): rebuild it on the device
-  if (c->d_vtab) {
-    int sing = 0;
-    CK(build_vtab(c, &sing));
-    c->vtab_sing = sing;
-  }
   return CNPINT_OK;
 }
 

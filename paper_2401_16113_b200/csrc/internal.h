@@ -26,7 +26,6 @@ struct TriCfg {
   size_t smem;
 };
 TriCfg tri_cfg(int m, int toeplitz);
-
 // rows allocated per system in shared memory: m rounded up to the swizzle block (and to even)
 static inline __host__ __device__ int tri_rows_alloc(int m, int padsh) {
   const int B = (1 << padsh) > 2 ? (1 << padsh) : 2;
@@ -85,8 +84,6 @@ struct cnpint_ctx {
   double2* d_sk;       // [H+1] s_k = λ1_k/λ2_k
   double2* d_il2;      // [H+1] 1/λ2_k
   double2* d_tritab;   // [H+1][tabstride] Toeplitz chunk tables of K3 (1D Toeplitz only)
-  double2* d_vtab;     // [H+1][tabstride] K3 variable rows: tabulated merge tree (MODE_VTAB), or null
-  int vtab_sing;       // the vtab build met a singular shifted system: every shifted solve reports it
   double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
   double* d_fsY;       // four-step FFT intermediate (1D N >= 2048, 2D N >= 256; k_fstep.cu), else null
   unsigned* d_fscnt;   // [nxb] per-block pass-A counters, then the work ticket (monotonic)
@@ -168,9 +165,6 @@ cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, c
 
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat);
-// K3 variable rows: (re)build the tabulated merge tree c->d_vtab (synchronous; *singular = 1 when a
-// shifted system is singular to working precision)
-cudaError_t build_vtab(cnpint_ctx* c, int* singular);
 cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 
 // N <= 16384: x-pair packed thread-block-cluster variant (k_tfft.cu)

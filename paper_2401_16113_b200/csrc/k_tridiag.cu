@@ -31,14 +31,6 @@
 //              merge's coefficient part is data independent and identical along a tree level
 //              (two variants: with / without the last segment), so it is tabulated too and the tree
 //              only carries the right-hand sides fd, gd (2 complex per merge instead of 8).
-//   MODE_VTAB  variable rows (c3) with a tabulated tree (round 2): the chunk sweeps run as in MODE_VAR,
-//              but the coefficient part of every merge (10 complex) and of the root (4) — data
-//              independent, different for every merge — is built once per handle by a MODE_VAR pass
-//              that writes it out (vtab, cnpint_set_debug), so the tree carries only fd, gd like
-//              MODE_FAST.  ncu of MODE_VAR at c3: the five warp-shuffle levels run the full merge on
-//              every lane (1/2 … 1/32 of them useful) and were half of its 145 fp64 operations per
-//              row.  The pivot and determinant checks are coefficient-only, so they run in the build
-//              pass too (a singular system found there makes every later solve report it).
 // Rows live in shared memory at sidx(i) = i ^ ((i >> padsh) & smask): an XOR swizzle inside each
 // chunk-length block that keeps both the coalesced copies and the per-thread chunk reads
 // bank-conflict free without padding.
@@ -77,9 +69,7 @@ CNP_DEV bool cancels(double2 x, double ref2) {
 }
 CNP_DEV double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 
-// tb (table build, MODE_VAR with a vtab output): also stores the merge's coefficient part in the
-// MODE_FAST / MODE_VTAB layout pa pb ra rb P1 P2 R1 R2 fcA gaB (P0 = pa gd_A + pb fd_B, R0 = ra fd_B + rb gd_A).
-CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf, double2* tb = nullptr) {
+CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf) {
   const double2 det = csub(cmul(A.gb, B.fb), cmul(A.gc, B.fa));
   const bool sing = cancels(det, cabs2(cmul(A.gb, B.fb)) + cabs2(cmul(A.gc, B.fa)));
   const double2 id = crecip_nr(det);
@@ -90,10 +80,6 @@ CNP_DEV bool merge(Seg& A, const Seg& B, double2* cf, double2* tb = nullptr) {
   const double2 R1 = cmul(cmul(B.fa, A.ga), id);
   const double2 R2 = cneg(cmul(cmul(A.gb, B.fc), id));
   cf[0] = P0; cf[1] = P1; cf[2] = P2; cf[3] = R0; cf[4] = R1; cf[5] = R2;
-  if (tb) {
-    tb[0] = cmul(B.fb, id); tb[1] = cneg(cmul(A.gc, id)); tb[2] = cmul(A.gb, id); tb[3] = cneg(cmul(B.fa, id));
-    tb[4] = P1; tb[5] = P2; tb[6] = R1; tb[7] = R2; tb[8] = A.fc; tb[9] = B.ga;
-  }
   A.fb = cfma(A.fc, P1, A.fb);
   A.fd = cfms(A.fd, A.fc, P0);
   A.fc = cmul(A.fc, P2);
@@ -111,7 +97,7 @@ CNP_DEV void unmerge(const double2* cf, double2 xs, double2 xe, double2& xm, dou
 
 }  // namespace
 
-enum { MODE_VAR = 0, MODE_TOEP = 1, MODE_FAST = 2, MODE_VTAB = 3 };
+enum { MODE_VAR = 0, MODE_TOEP = 1, MODE_FAST = 2 };
 
 // Toeplitz table per frequency k (tri_cfg().tabstride complex entries):
 //   [0, L)                   inv_j = 1/pivot_j of the chunk forward sweep (j = 1..L−1)
@@ -129,22 +115,20 @@ __global__ void __launch_bounds__(MAXT, 2)
               const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
               const double2* __restrict__ il2, const double2* __restrict__ tab, int m, int64_t W, int K, int G,
               int logG, int NS, int padsh, int smask, int TS, double tau, int* __restrict__ status,
-              const double2* __restrict__ lam1, int skip, double2* __restrict__ wtab) {
+              const double2* __restrict__ lam1, int skip) {
   pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
-  constexpr bool TOEP = MODE == MODE_TOEP || MODE == MODE_FAST;
+  constexpr bool TOEP = MODE != MODE_VAR;
   constexpr bool FAST = MODE == MODE_FAST;
-  constexpr bool VT = MODE == MODE_VTAB;
-  constexpr bool RT = FAST || VT;    // the tree carries only the right-hand sides (coefficients tabulated)
-  constexpr int NCF = RT ? 2 : 6;    // stored coefficients per merge
+  constexpr int NCF = FAST ? 2 : 6;  // stored coefficients per merge
   constexpr int L1S = 5 * L + 6;
   extern __shared__ double2 smem[];
   const int nwarp = NS * G, P = 32 * G;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp / G, wg = warp - g * G, p = wg * 32 + lane;
   const int MP = tri_rows_alloc(m, padsh);
-  const int per_sys = TOEP ? MP + TS : VT ? 3 * MP + TS : 3 * MP;
+  const int per_sys = TOEP ? MP + TS : 3 * MP;
   double2* const D = smem + g * per_sys;
-  double2* const T = TOEP ? D + MP : D + 3 * MP;  // Toeplitz table / variable-row tree table (VT)
+  double2* const T = D + MP;                 // Toeplitz table
   double2* const Ap = D + MP;                // variable rows: α'
   double2* const Gp = D + 2 * MP;            //                γ'
   double2* const coefw = smem + NS * per_sys;            // [nwarp][31][NCF]
@@ -162,7 +146,7 @@ __global__ void __launch_bounds__(MAXT, 2)
     const double2* src = what + (int64_t)k * W;
     if (!(skip & 1))
       for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
-    if (TOEP || VT)
+    if (TOEP)
       for (int i = p; i < TS; i += P) cp_async16(T + i, tab + (size_t)k * TS + i);
   }
   cp_async_commit();
@@ -228,7 +212,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           const double2 bb = make_double2(skk.x - tau * di[i], skk.y);
           const double2 piv = (j == 1) ? bb : crfms(bb, a, gam);
           const double2 inv = crecip_nr(piv);
-          if constexpr (!VT) ok &= cfinite(inv) && !cancels(piv, cabs2(bb) + (j == 1 ? 0.0 : a * a * cabs2(gam)));
+          ok &= cfinite(inv) && !cancels(piv, cabs2(bb) + (j == 1 ? 0.0 : a * a * cabs2(gam)));
           alp = (j == 1) ? cscale(inv, a) : cscale(cmul(alp, inv), -a);
           gam = cscale(inv, c);
           last = (j == 1) ? cmul(dl[1], inv) : cmul(crfms(dl[j], a, last), inv);
@@ -276,26 +260,17 @@ __global__ void __launch_bounds__(MAXT, 2)
   // ---------------- tree up: 5 warp levels
   double2* cw = coefw + warp * 31 * NCF;
   const double2* TT = T + L1S;  // fast-tree table
-  // table entry of a merge: FAST per (level, variant); VT per merge (warp levels: 31 per warp, then the
-  // G − 1 cross-warp merges, then the root); the MODE_VAR build writes the VT layout to wtab
-  auto wcf = [&](int lv, int v) -> const double2* {
-    return FAST ? TT + ((lv - 1) * 2 + v) * 10 : T + (wg * 31 + 32 - (64 >> lv) + (lane >> lv)) * 10;
-  };
-  auto xcf = [&](int lv, int v) -> const double2* {
-    return FAST ? TT + ((5 + lv - 1) * 2 + v) * 10 : T + (G * 31 + G - (2 * G >> lv) + (lane >> lv)) * 10;
-  };
-  double2* const wt = (!TOEP && !VT && wtab && act) ? wtab + (size_t)k * TS : nullptr;
   if (act && !diag_only) {
 #pragma unroll
     for (int lv = 1; lv <= 5; ++lv) {
       const int sft = 1 << (lv - 1);
       const bool left = (lane & ((1 << lv) - 1)) == 0;
       double2* slot = cw + (32 - (64 >> lv) + (lane >> lv)) * NCF;
-      if (RT) {
+      if (FAST) {
         const double2 fdB = shfl_down<double2>(sg.fd, sft), gdB = shfl_down<double2>(sg.gd, sft);
         if (left) {
           const int v = (wg == G - 1 && lane + 2 * sft == 32) ? 1 : 0;
-          const double2* cf = wcf(lv, v);
+          const double2* cf = TT + ((lv - 1) * 2 + v) * 10;
           const double2 P0 = cfma(cf[0], sg.gd, cmul(cf[1], fdB));
           const double2 R0 = cfma(cf[2], fdB, cmul(cf[3], sg.gd));
           slot[0] = P0;
@@ -305,14 +280,14 @@ __global__ void __launch_bounds__(MAXT, 2)
         }
       } else {
         const Seg B = shfl_seg(sg, sft);
-        if (left) ok &= merge(sg, B, slot, wt ? wt + (wg * 31 + 32 - (64 >> lv) + (lane >> lv)) * 10 : nullptr);
+        if (left) ok &= merge(sg, B, slot);
       }
     }
   }
   double2 xs = make_double2(0.0, 0.0), xe = make_double2(0.0, 0.0);
   auto root = [&](const Seg& t) {
-    if (RT) {
-      const double2* r = FAST ? TT + (5 + logG) * 20 : T + (G * 31 + G - 1) * 10;
+    if (FAST) {
+      const double2* r = TT + (5 + logG) * 20;
       xs = cfma(r[0], t.fd, cmul(r[1], t.gd));
       xe = cfma(r[2], t.fd, cmul(r[3], t.gd));
       return;
@@ -323,10 +298,6 @@ __global__ void __launch_bounds__(MAXT, 2)
     ok &= cfinite(id) && !cancels(det, cabs2(cmul(t.fb, t.gb)) + cabs2(cmul(t.fc, t.ga)));
     xs = cmul(csub(cmul(t.fd, t.gb), cmul(t.fc, t.gd)), id);
     xe = cmul(csub(cmul(t.fb, t.gd), cmul(t.ga, t.fd)), id);
-    if (wt) {  // x_0 = r0 fd + r1 gd, x_{m−1} = r2 fd + r3 gd
-      double2* r = wt + (G * 31 + G - 1) * 10;
-      r[0] = cmul(t.gb, id); r[1] = cneg(cmul(t.fc, id)); r[2] = cneg(cmul(t.ga, id)); r[3] = cmul(t.fb, id);
-    }
   };
   if (G == 1) {
     if (act && !diag_only && lane == 0) root(sg);
@@ -335,7 +306,7 @@ __global__ void __launch_bounds__(MAXT, 2)
     if (lane == 0) {
       double2* r = segr + warp * 8;
       r[3] = sg.fd; r[7] = sg.gd;
-      if (!RT) { r[0] = sg.fa; r[1] = sg.fb; r[2] = sg.fc; r[4] = sg.ga; r[5] = sg.gb; r[6] = sg.gc; }
+      if (!FAST) { r[0] = sg.fa; r[1] = sg.fb; r[2] = sg.fc; r[4] = sg.ga; r[5] = sg.gb; r[6] = sg.gc; }
     }
     named_sync(1 + g, 32 * G);
     if (wg == 0 && act && !diag_only) {
@@ -343,18 +314,18 @@ __global__ void __launch_bounds__(MAXT, 2)
       if (lane < G) {
         const double2* r = segr + (g * G + lane) * 8;
         t.fd = r[3]; t.gd = r[7];
-        if (!RT) { t.fa = r[0]; t.fb = r[1]; t.fc = r[2]; t.ga = r[4]; t.gb = r[5]; t.gc = r[6]; }
+        if (!FAST) { t.fa = r[0]; t.fb = r[1]; t.fc = r[2]; t.ga = r[4]; t.gb = r[5]; t.gc = r[6]; }
       }
       double2* cx = coefx + g * 15 * NCF;
       for (int lv = 1; lv <= logG; ++lv) {
         const int sft = 1 << (lv - 1);
         const bool left = (lane & ((1 << lv) - 1)) == 0 && lane < G;
         double2* slot = cx + (G - (2 * G >> lv) + (lane >> lv)) * NCF;
-        if (RT) {
+        if (FAST) {
           const double2 fdB = shfl_down<double2>(t.fd, sft), gdB = shfl_down<double2>(t.gd, sft);
           if (left) {
             const int v = (lane + 2 * sft == G) ? 1 : 0;
-            const double2* cf = xcf(lv, v);
+            const double2* cf = TT + ((5 + lv - 1) * 2 + v) * 10;
             const double2 P0 = cfma(cf[0], t.gd, cmul(cf[1], fdB));
             const double2 R0 = cfma(cf[2], fdB, cmul(cf[3], t.gd));
             slot[0] = P0;
@@ -364,7 +335,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           }
         } else {
           const Seg B = shfl_seg(t, sft);
-          if (left) ok &= merge(t, B, slot, wt ? wt + (G * 31 + G - (2 * G >> lv) + (lane >> lv)) * 10 : nullptr);
+          if (left) ok &= merge(t, B, slot);
         }
       }
       if (lane == 0) root(t);
@@ -375,9 +346,9 @@ __global__ void __launch_bounds__(MAXT, 2)
         double2 xm = make_double2(0.0, 0.0), xm1 = xm;
         if (left) {
           const double2* slot = cx + (G - (2 * G >> lv) + (lane >> lv)) * NCF;
-          if (RT) {
+          if (FAST) {
             const int v = (lane + 2 * sft == G) ? 1 : 0;
-            const double2* cf = xcf(lv, v);
+            const double2* cf = TT + ((5 + lv - 1) * 2 + v) * 10;
             xm = cfma(cf[5], xe, cfma(cf[4], xs, slot[0]));
             xm1 = cfma(cf[7], xe, cfma(cf[6], xs, slot[1]));
           } else {
@@ -409,9 +380,9 @@ __global__ void __launch_bounds__(MAXT, 2)
       double2 xm = make_double2(0.0, 0.0), xm1 = xm;
       if (left) {
         const double2* slot = cw + (32 - (64 >> lv) + (lane >> lv)) * NCF;
-        if (RT) {
+        if (FAST) {
           const int v = (wg == G - 1 && lane + 2 * sft == 32) ? 1 : 0;
-          const double2* cf = wcf(lv, v);
+          const double2* cf = TT + ((lv - 1) * 2 + v) * 10;
           xm = cfma(cf[5], xe, cfma(cf[4], xs, slot[0]));
           xm1 = cfma(cf[7], xe, cfma(cf[6], xs, slot[1]));
         } else {
@@ -529,13 +500,11 @@ TriCfg tri_cfg(int m, int toeplitz) {
   t.smask = (1 << t.padsh) - 1;
   if (t.smask > 7) t.smask = 7;
   t.nlv = 5 + t.logG;
-  // Toeplitz: chunk + fast-tree table; variable rows: the MODE_VTAB tree table (10 complex per merge:
-  // 31 per warp, G − 1 across warps; 4 for the root)
-  t.tabstride = t.L <= 0 ? 0 : toeplitz ? 5 * t.L + 6 + t.nlv * 20 + 4 : (32 * G - 1) * 10 + 4;
+  t.tabstride = toeplitz && t.L > 0 ? 5 * t.L + 6 + t.nlv * 20 + 4 : 0;
   t.NS = G >= 8 ? 1 : 8 / G;
   const int MP = tri_rows_alloc(m, t.padsh);
-  const int per_sys = toeplitz ? MP + t.tabstride : 3 * MP + t.tabstride;
-  const int ncf = (t.fast || !toeplitz) ? 2 : 6;
+  const int per_sys = toeplitz ? MP + t.tabstride : 3 * MP;
+  const int ncf = t.fast ? 2 : 6;
   auto smem_of = [&](int ns) {
     const int nw = ns * G;
     return (size_t)(ns * per_sys + nw * 31 * ncf + ns * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
@@ -558,8 +527,7 @@ static int tri_skip() {
 }
 
 template <int MODE, int L, int MAXT>
-static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat,
-                             double2* wtab = nullptr) {
+static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
   {
     int done = 0;
     cudaError_t ce = cnp_dev_cached((const void*)k_tridiag<MODE, L, MAXT>, &done, [&](int* v) {
@@ -571,43 +539,21 @@ static cudaError_t run_tri_t(cnpint_ctx* c, const TriCfg& t, const double2* what
   const int K = c->H + 1;
   const int grid = (K + t.NS - 1) / t.NS;
   // shared memory of this variant (the generic trees store 6 coefficients per merge, the fast one 2)
-  const int ncf = (MODE == MODE_FAST || MODE == MODE_VTAB) ? 2 : 6, nw = t.NS * t.G;
+  const int ncf = MODE == MODE_FAST ? 2 : 6, nw = t.NS * t.G;
   const int MP = tri_rows_alloc(c->nx, t.padsh);
-  const int per_sys = MODE == MODE_VAR ? 3 * MP : MODE == MODE_VTAB ? 3 * MP + t.tabstride : MP + t.tabstride;
-  const size_t smem = (size_t)(t.NS * per_sys + nw * 31 * ncf + t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
-  const double2* tab = MODE == MODE_VTAB ? c->d_vtab : c->d_tritab;
+  const size_t smem = (size_t)(t.NS * (MODE == MODE_VAR ? 3 * MP : MP + t.tabstride) + nw * 31 * ncf +
+                               t.NS * 15 * ncf + nw * 8 + nw * 2) * sizeof(double2);
   return cnp_launch(c, k_tridiag<MODE, L, MAXT>, dim3(grid), dim3(32 * t.G * t.NS), smem, what, zhat, c->d_lo,
-                    c->d_di, c->d_up, c->d_sk, c->d_il2, tab, c->nx, c->ld, K, t.G, t.logG, t.NS, t.padsh,
-                    t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1, tri_skip(), wtab);
+                    c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_tritab, c->nx, c->ld, K, t.G, t.logG, t.NS, t.padsh,
+                    t.smask, t.tabstride, c->tau_p, c->d_status, c->d_lam1, tri_skip());
 }
 
 template <int MODE, int L>
-static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat,
-                           double2* wtab = nullptr) {
+static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
   const int nt = 32 * t.G * t.NS;
-  if (nt <= 256) return run_tri_t<MODE, L, 256>(c, t, what, zhat, wtab);
-  if (nt <= 512) return run_tri_t<MODE, L, 512>(c, t, what, zhat, wtab);
+  if (nt <= 256) return run_tri_t<MODE, L, 256>(c, t, what, zhat);
+  if (nt <= 512) return run_tri_t<MODE, L, 512>(c, t, what, zhat);
   return cudaErrorInvalidValue;
-}
-
-// K3 variable rows: one MODE_VAR pass over the handle's spectrum scratch (its right-hand sides do not
-// matter) that writes the coefficient part of every merge and root to d_vtab; its pivot / determinant
-// checks are coefficient-only, so a singular system is found here once for all later solves.
-cudaError_t build_vtab(cnpint_ctx* c, int* singular) {
-  *singular = 0;
-  if (!c->d_vtab) return cudaSuccess;
-  const TriCfg t = tri_cfg(c->nx, 0);
-  if (cudaError_t e = cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream)) return e;
-  cudaError_t e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, c->d_spec, c->d_spec, c->d_vtab)
-                : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, c->d_spec, c->d_spec, c->d_vtab)
-                           : cudaErrorInvalidValue;
-  if (e != cudaSuccess) return e;
-  int st = 0;
-  if ((e = cudaMemcpyAsync(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream))) return e;
-  if ((e = cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream))) return e;
-  if ((e = cudaStreamSynchronize(c->stream))) return e;
-  *singular = st != 0;
-  return cudaSuccess;
 }
 
 // fault injection (debug bit 2048): the shifted solve reports a singular pivot, as a genuinely singular
@@ -615,8 +561,7 @@ cudaError_t build_vtab(cnpint_ctx* c, int* singular) {
 __global__ void k_inject_singular(int* status) { atomicOr(status, 1); }
 
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat) {
-  if ((c->debug & 2048) || (c->vtab_sing && !(c->debug & 512))) {
-    // fault injection, or the vtab build found a singular system (the table-driven solve has no checks)
+  if (c->debug & 2048) {
     k_inject_singular<<<1, 1, 0, c->stream>>>(c->d_status);
     if (cudaError_t e = cudaGetLastError()) return e;
   }
@@ -631,10 +576,7 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
                                                             m, W, c->tau_p, K, c->d_status, c->d_lam1);
     e = cudaGetLastError();
-  } else if (!c->toeplitz && c->d_vtab && !(c->debug & 512)) {
-    e = t.L == 4 ? run_tri<MODE_VTAB, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VTAB, 8>(c, t, what, zhat)
-                                                                      : cudaErrorInvalidValue;
-  } else if (!c->toeplitz) {  // debug 512: the r01 generic tree (every merge computed per solve)
+  } else if (!c->toeplitz) {
     e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, what, zhat)
                                                                      : cudaErrorInvalidValue;
   } else if (t.fast && !(c->debug & 4)) {
