@@ -18,6 +18,7 @@
 
 #include "internal.h"
 
+
 int matvec_partial_blocks(const cnpint_ctx* c);
 
 // ------------------------------------------------------------------------------ profiler
@@ -98,7 +99,7 @@ size_t up_align(size_t v) { return (v + ALIGN - 1) & ~(ALIGN - 1); }
 bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
 
 struct Layout {
-  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
+  size_t lo, di, up, tw, gam, igam, lam1, lam2, sk, il2, tri, vtab, tables_end, spec, fsy, fscnt, tmp1, tmp2, tmp3, io1, io2, io3;
   size_t dxi, dx, dyi, dy, ex, ey, twx, twy;
   size_t dt, V, Z, part, c1, c2, scl, H, cs, sn, g, y, coef, G, cg, scal, status, xycnt;
   size_t total;
@@ -160,6 +161,10 @@ Layout layout(int N, const cnpint_operator* op, int restart_max) {
     L.twx = take((size_t)2 * (nx + 1) * 16); L.twy = take((size_t)2 * (ny + 1) * 16);
   }
   L.tables_end = off;
+  if (op->dim == 1 && !op->toeplitz) {  // built on the device after the upload (outside the host image)
+    const int ts = trivar_table_stride(nx);
+    L.vtab = ts ? take((size_t)(H + 1) * ts * 16) : 0;
+  }
   L.spec = op->dim == 1 ? take((size_t)(H + 1) * ld * 16) : take(16);
   L.fsy = take(fstep_y_bytes(op->dim, N, (int64_t)ny * ld));
   L.fscnt = take(fstep_y_bytes(op->dim, N, (int64_t)ny * ld) ? (size_t)(fstep_nxb(N, (int64_t)ny * ld) + 1) * 4 : 4);
@@ -523,6 +528,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   c->d_lam1 = (double2*)(w + L.lam1); c->d_lam2 = (double2*)(w + L.lam2);
   c->d_sk = (double2*)(w + L.sk); c->d_il2 = (double2*)(w + L.il2);
   c->d_tritab = (double2*)(w + L.tri);
+  c->d_vtab = L.vtab ? (double2*)(w + L.vtab) : nullptr;
   c->d_spec = (double2*)(w + L.spec);
   c->d_fsY = fstep_y_bytes(op->dim, N, c->slice) ? (double*)(w + L.fsy) : nullptr;
   c->d_fscnt = (unsigned*)(w + L.fscnt);
@@ -558,6 +564,10 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->h_pinned, 16 * sizeof(double), cudaHostAllocMapped);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&c->d_hmap, c->h_pinned, 0);
     if (e != cudaSuccess) st = cuda_fail(c, e, "cnpint_create");
+  }
+  if (st == CNPINT_OK) {  // K3 variable-row tables (coefficient-only part of the upper merge tree)
+    cudaError_t e = build_trivar_table(c);
+    if (e != cudaSuccess) st = cuda_fail(c, e, "build_trivar_table");
   }
   if (st != CNPINT_OK) {
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -751,6 +761,7 @@ cnpint_status cnpint_set_debug(cnpint_ctx* c, int flags) {
   const size_t hi = L.tables_end;
   CK(cudaMemcpyAsync(c->ws + L.tw, img.data() + L.tw, hi - L.tw, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  CK(build_trivar_table(c));  // depends on s_k (debug 2) and τ
   return CNPINT_OK;
 }
 

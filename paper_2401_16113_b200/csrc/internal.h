@@ -84,6 +84,7 @@ struct cnpint_ctx {
   double2* d_sk;       // [H+1] s_k = λ1_k/λ2_k
   double2* d_il2;      // [H+1] 1/λ2_k
   double2* d_tritab;   // [H+1][tabstride] Toeplitz chunk tables of K3 (1D Toeplitz only)
+  double2* d_vtab;     // [H+1][trivar_table_stride] K3 variable-row upper-tree tables (built on the device)
   double2* d_spec;     // [(H+1)][ny][ld] half spectrum (1D) ; 2D: unused
   double* d_fsY;       // four-step FFT intermediate (1D N >= 2048, 2D N >= 256; k_fstep.cu), else null
   unsigned* d_fscnt;   // [nxb] per-block pass-A counters, then the work ticket (monotonic)
@@ -165,6 +166,8 @@ cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, c
 
 cudaError_t launch_time_fft(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zhat);
+int trivar_table_stride(int m);
+cudaError_t build_trivar_table(cnpint_ctx* c);
 cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 
 // N <= 16384: x-pair packed thread-block-cluster variant (k_tfft.cu)

@@ -425,6 +425,329 @@ __global__ void __launch_bounds__(MAXT, 2)
   }
 }
 
+// Variable rows, second generation (round 2; c3).  MODE_VAR above measured (r01 ncu: 210 µs at c3, DRAM
+// 12 %, 18 % warps active, fp64 pipe 31 %): its merge tree runs levels 1–5 in every warp on all 32 lanes
+// while 16, 8, …, 1 of them merge, so a merge (≈ 115 fp64 instructions) is paid per warp per level, and
+// α', γ', δ' go through shared memory (3·MP complex per system).  Phase traces (scripts/trivar_trace.py,
+// clock64 per CTA, c3, cycles per system) of the intermediate designs: a dense shared-memory tree — load
+// 1.9 k, sweeps 5.3 k, tree 8.3 k (≈ 860 cycles per level), back-substitution and store 1.5 k; warp-shuffle
+// levels in each warp plus the upper levels in warp 0 — sweeps 2.4 k, tree 10.3 k.  A tree level is bound
+// by one warp issuing the merge's ≈ 115 fp64 instructions (the fp64 pipe takes a warp instruction every
+// other cycle per SM sub-partition) behind its ≈ 130-cycle dependency chain (DFMA 8 cycles, rcp + two
+// Newton steps 47 cycles: scripts/lat_bench.cu), and the upper levels are a serial chain of them.
+// But everything in a merge except the right-hand-side parts (fd, gd) depends only on the frequency k
+// and the rows, which are fixed for the handle.  So:
+//   * build (once per handle, k_trivar<…, BUILD>: at cnpint_create and whenever the tables change): the
+//     coefficient part of every merge of the upper levels S+1 … log2 P (S = max(2, log2 G) levels stay in
+//     the warps) and of the root is written to a per-frequency table vtab (MODE_FAST's layout: pa pb ra rb
+//     P1 P2 R1 R2 fcA gaB per merge, 4 root entries; ≈ 5 KB per frequency at c3), and every
+//     coefficient-only test of reading R29 (chunk pivots, merge and root determinants) runs there; a
+//     frequency that fails it is flagged in its table row, and every solve reports it in the status word;
+//   * solve: the chunk sweeps (α', γ', δ' stay in registers until the back-substitution; the rows lo, di,
+//     up are fetched while the system copy is in flight), tree levels 1 … S by warp shuffles inside each
+//     warp with the generic merge, one shared-memory hand-over of the P/2^S ≤ 32 segments' (fd, gd) to
+//     warp 0, whose lanes run the upper levels from the table (2 complex per merge through the shuffles,
+//     four complex FMAs), the root and the upper down levels, then the down levels 1 … S in each warp and
+//     the back-substitution.  The table row is staged into shared memory with the system (cp.async).
+// UNI: every chunk holds L − 1 or L rows (m ∈ (P(L−1), PL], c3), so only a chunk's last row is conditional.
+#ifndef CNPINT_TRIVAR_MINB
+#define CNPINT_TRIVAR_MINB 3  // resident CTAs per SM for P = 128 (c3): 168 registers, no spills
+#endif
+#ifdef CNPINT_TRIVAR_TRACE
+// experiment builds only: per-CTA clock64 stamps at the phase boundaries of k_trivar (scripts/trivar_trace.py)
+__device__ long long g_trv_trace[16384 * 10];
+#define TRV_STAMP(q) \
+  if (!BUILD && threadIdx.x == 0 && blockIdx.x < 16384) { \
+    long long t_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_)); g_trv_trace[blockIdx.x * 10 + (q)] = t_; \
+    if ((q) == 0) { unsigned s_; asm volatile("mov.u32 %0, %%smid;" : "=r"(s_)); g_trv_trace[blockIdx.x * 10 + 9] = s_; } }
+extern "C" int cnpint_trivar_trace(long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_trv_trace, sizeof(long long) * (size_t)n);
+}
+#else
+#define TRV_STAMP(q)
+#endif
+
+namespace {
+// build-time merge: as merge(), plus the coefficient part of the merge in MODE_FAST's layout
+// (P0 = pa gd_A + pb fd_B, R0 = ra fd_B + rb gd_A, fd ← fd_A − fcA P0, gd ← gd_B − gaB R0), field f at tb[f·st]
+CNP_DEV bool merge_tab(Seg& A, const Seg& B, double2* tb, int st) {
+  const double2 det = csub(cmul(A.gb, B.fb), cmul(A.gc, B.fa));
+  const bool sing = cancels(det, cabs2(cmul(A.gb, B.fb)) + cabs2(cmul(A.gc, B.fa)));
+  const double2 id = crecip_nr(det);
+  const double2 P1 = cneg(cmul(cmul(B.fb, A.ga), id));
+  const double2 P2 = cmul(cmul(A.gc, B.fc), id);
+  const double2 R1 = cmul(cmul(B.fa, A.ga), id);
+  const double2 R2 = cneg(cmul(cmul(A.gb, B.fc), id));
+  tb[0] = cmul(B.fb, id); tb[st] = cneg(cmul(A.gc, id)); tb[2 * st] = cmul(A.gb, id); tb[3 * st] = cneg(cmul(B.fa, id));
+  tb[4 * st] = P1; tb[5 * st] = P2; tb[6 * st] = R1; tb[7 * st] = R2; tb[8 * st] = A.fc; tb[9 * st] = B.ga;
+  A.fb = cfma(A.fc, P1, A.fb);
+  A.fc = cmul(A.fc, P2);
+  A.ga = cmul(B.ga, R1);
+  A.gb = cfma(B.ga, R2, B.gb);
+  A.gc = B.gc;
+  return cfinite(id) && !sing;
+}
+}  // namespace
+
+// table row per frequency (complex): upper level h = 1 … LOGP − S with n_h = NX >> h merges at
+// 10(NX − 2n_h) + f·n_h + q (f = 0..9), the root (c0 c1 c2 c3: x_0 = c0 fd + c1 gd, x_{m−1} = c2 fd + c3 gd)
+// at 10(NX − 1), the build's verdict at 10(NX − 1) + 4 (.x = 1: a coefficient-only test failed)
+__host__ __device__ constexpr int trv_nx(int P) { return P >> ((P / 32) > 4 ? ((P / 32) == 8 ? 3 : 4) : 2); }
+__host__ __device__ constexpr int trv_ts(int P) { return 10 * (trv_nx(P) - 1) + 5; }
+
+template <int L, int MAXT, bool UNI, bool BUILD>
+__global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? CNPINT_TRIVAR_MINB * 128 / MAXT : 1)
+    k_trivar(const double2* __restrict__ what, double2* __restrict__ zhat, const double* __restrict__ lo,
+             const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
+             const double2* __restrict__ il2, double2* __restrict__ vtab, int m, int64_t W, int padsh, int smask,
+             double tau, int* __restrict__ status, const double2* __restrict__ lam1) {
+  constexpr int P = MAXT, G = MAXT / 32;
+  constexpr int LOGG = G == 1 ? 0 : G == 2 ? 1 : G == 4 ? 2 : G == 8 ? 3 : 4;
+  constexpr int S = LOGG > 2 ? LOGG : 2;  // tree levels inside each warp
+  constexpr int NX = P >> S;              // segments handed to warp 0 (<= 32)
+  constexpr int LOGP = 5 + LOGG;
+  constexpr int TS = trv_ts(P);
+  static_assert(NX == trv_nx(P) && NX <= 32, "hand-over to one warp");
+  if (!BUILD) pdl_enter();
+  TRV_STAMP(0);
+  extern __shared__ double2 smem[];
+  const int p = threadIdx.x, lane = p & 31, warp = p >> 5, k = blockIdx.x;
+  const int MP = tri_rows_alloc(m, padsh);
+  double2* const D = smem;          // [MP] rows; the hand-over to warp 0 while the rows are dead
+  double2* const CF = D + MP;       // [6P] levels 1..S: 6 coefficients per merge; then upper levels: P0, R0
+  double2* const BX = CF + 6 * P;   // [2·NX] boundary values handed back by warp 0
+  double2* const T = BX + 2 * NX;   // [TS] this frequency's table row (solve)
+  auto sidx = [&](int i) { return i ^ ((i >> padsh) & smask); };
+  const double2 il = __ldg(il2 + k), skk = __ldg(sk + k);
+  if (!BUILD) {
+    const double2* src = what + (int64_t)k * W;
+    for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
+    const double2* tr = vtab + (size_t)k * TS;
+    for (int i = p; i < TS; i += P) cp_async16(T + i, tr + i);
+  }
+  cp_async_commit();
+  const int Lmin = m / P, nlong = m - P * Lmin;
+  const int len = p < nlong ? Lmin + 1 : Lmin;
+  const int i0 = p < nlong ? p * (Lmin + 1) : nlong * (Lmin + 1) + (p - nlong) * Lmin;
+  const int i1 = i0 + len;
+  auto has = [&](int j) { return UNI ? (j < L - 1 || len == L) : j < len; };  // row j of the chunk exists
+  // the chunk's rows while the copy is in flight (lo, di, up are zero padded to ld >= m)
+  double ra[L], rc[L], rd[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const int i = has(j) ? i0 + j : i0;
+    ra[j] = __ldg(lo + i);
+    rc[j] = __ldg(up + i);
+    rd[j] = __ldg(di + i);
+  }
+  bool ok = true;
+  cp_async_wait<0>();
+  __syncthreads();
+  TRV_STAMP(1);
+  double2* const dst = zhat + (int64_t)k * W;
+  if (il.x == 0.0 && il.y == 0.0) {  // α = 1, k = N/2: λ2 = 0, the system is λ1 z = w (uniform per CTA)
+    if (!BUILD) {
+      const double2 r = crecip(lam1[k]);
+      for (int i = p; i < m; i += P) stg_cs2(dst + i, cmul(D[sidx(i)], r));
+      for (int i = m + p; i < W; i += P) dst[i] = make_double2(0.0, 0.0);
+    } else if (p == 0) {
+      vtab[(size_t)k * TS + TS - 1] = make_double2(0.0, 0.0);
+    }
+    return;
+  }
+  double2 dl[L], ap[L], gp[L];
+  Seg sg;
+#pragma unroll
+  for (int j = 0; j < L; ++j) dl[j] = (!BUILD && has(j)) ? cmul(D[sidx(i0 + j)], il) : make_double2(0.0, 0.0);
+  {
+    double2 alp = make_double2(0.0, 0.0), gam = alp, last = dl[0];
+#pragma unroll
+    for (int j = 1; j < L; ++j) {
+      if (has(j)) {
+        const double a = -tau * ra[j], c = -tau * rc[j];
+        const double2 bb = make_double2(skk.x - tau * rd[j], skk.y);
+        const double2 piv = (j == 1) ? bb : crfms(bb, a, gam);
+        const double2 inv = crecip_nr(piv);
+        if (BUILD) ok &= cfinite(inv) && !cancels(piv, cabs2(bb) + (j == 1 ? 0.0 : a * a * cabs2(gam)));
+        alp = (j == 1) ? cscale(inv, a) : cscale(cmul(alp, inv), -a);
+        gam = cscale(inv, c);
+        if (!BUILD) {
+          last = (j == 1) ? cmul(dl[1], inv) : cmul(crfms(dl[j], a, last), inv);
+          dl[j] = last;
+        }
+        ap[j] = alp;
+        gp[j] = gam;
+      }
+    }
+    sg.ga = alp;
+    sg.gb = make_double2(1.0, 0.0);
+    sg.gc = gam;
+    sg.gd = last;
+#pragma unroll
+    for (int j = L - 3; j >= 1; --j) {
+      if (UNI ? (j < L - 3 || len == L) : j <= len - 3) {
+        const double2 gj = gp[j];
+        if (!BUILD) dl[j] = cfms(dl[j], gj, dl[j + 1]);
+        ap[j] = cfms(ap[j], gj, ap[j + 1]);
+        gp[j] = cneg(cmul(gj, gp[j + 1]));
+      }
+    }
+    const double a0 = -tau * ra[0], c0 = -tau * rc[0];
+    const double2 b0 = make_double2(skk.x - tau * rd[0], skk.y);
+    sg.fa = make_double2(a0, 0.0);
+    if (len >= 3) {
+      sg.fb = crfms(b0, c0, ap[1]);
+      sg.fc = cscale(gp[1], -c0);
+      sg.fd = crfms(dl[0], c0, dl[1]);
+    } else {
+      sg.fb = b0;
+      sg.fc = make_double2(c0, 0.0);
+      sg.fd = dl[0];
+    }
+  }
+  TRV_STAMP(2);
+  auto put_cf = [&](int l, int q, const double2* cf) {
+    const int n = P >> l;
+    double2* c = CF + 6 * (P - 2 * n) + q;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) c[f * n] = cf[f];
+  };
+  auto get_cf = [&](int l, int q, double2* cf) {
+    const int n = P >> l;
+    const double2* c = CF + 6 * (P - 2 * n) + q;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) cf[f] = c[f * n];
+  };
+  // ---------------- tree levels 1..S inside each warp (lane ≡ chunk within the warp), generic merges
+#pragma unroll
+  for (int l = 1; l <= S; ++l) {
+    const Seg B = shfl_seg(sg, 1 << (l - 1));
+    if ((lane & ((1 << l) - 1)) == 0) {
+      double2 cf[6];
+      const bool mok = merge(sg, B, cf);
+      if (BUILD) ok &= mok;
+      else put_cf(l, p >> l, cf);
+    }
+  }
+  __syncthreads();  // every row read from D: the hand-over area may overwrite it
+  if ((lane & ((1 << S) - 1)) == 0) {
+    const int t = p >> S;
+    if (BUILD) {
+      D[t] = sg.fa; D[NX + t] = sg.fb; D[2 * NX + t] = sg.fc;
+      D[4 * NX + t] = sg.ga; D[5 * NX + t] = sg.gb; D[6 * NX + t] = sg.gc;
+    } else {
+      D[3 * NX + t] = sg.fd; D[7 * NX + t] = sg.gd;
+    }
+  }
+  if (BUILD) {
+    // ---------------- build: upper merges and the root into the table; the verdict of every test
+    const bool bad = __syncthreads_or(!ok);
+    if (warp == 0) {
+      Seg t;
+      const int u = lane < NX ? lane : 0;
+      t.fa = D[u]; t.fb = D[NX + u]; t.fc = D[2 * NX + u]; t.fd = make_double2(0.0, 0.0);
+      t.ga = D[4 * NX + u]; t.gb = D[5 * NX + u]; t.gc = D[6 * NX + u]; t.gd = t.fd;
+      double2* const tr = vtab + (size_t)k * TS;
+      bool wok = true;
+#pragma unroll
+      for (int h = 1; h <= LOGP - S; ++h) {
+        const Seg B = shfl_seg(t, 1 << (h - 1));
+        const int n = NX >> h;
+        if (lane < NX && (lane & ((1 << h) - 1)) == 0) wok &= merge_tab(t, B, tr + 10 * (NX - 2 * n) + (lane >> h), n);
+      }
+      if (lane == 0) {
+        const double2 det = csub(cmul(t.fb, t.gb), cmul(t.fc, t.ga));
+        const double2 id = crecip(det);
+        wok &= cfinite(id) && !cancels(det, cabs2(cmul(t.fb, t.gb)) + cabs2(cmul(t.fc, t.ga)));
+        double2* r = tr + 10 * (NX - 1);
+        r[0] = cmul(t.gb, id); r[1] = cneg(cmul(t.fc, id)); r[2] = cneg(cmul(t.ga, id)); r[3] = cmul(t.fb, id);
+      }
+      wok = !__any_sync(0xffffffffu, !wok);
+      if (lane == 0) tr[TS - 1] = make_double2((bad || !wok) ? 1.0 : 0.0, 0.0);
+    }
+    return;
+  }
+  __syncthreads();
+  TRV_STAMP(7);
+  // ---------------- levels S+1..LOGP, the root and the upper down levels in warp 0 (lane ≡ segment) from
+  // the table: the tree carries only (fd, gd) up and (x_s, x_e) down
+  if (warp == 0) {
+    const int u = lane < NX ? lane : 0;
+    double2 fd = D[3 * NX + u], gd = D[7 * NX + u];
+#pragma unroll
+    for (int h = 1; h <= LOGP - S; ++h) {
+      const int sft = 1 << (h - 1), n = NX >> h;
+      const double2 fdB = shfl_down<double2>(fd, sft), gdB = shfl_down<double2>(gd, sft);
+      if (lane < NX && (lane & ((1 << h) - 1)) == 0) {
+        const double2* cf = T + 10 * (NX - 2 * n) + (lane >> h);
+        const double2 P0 = cfma(cf[0], gd, cmul(cf[n], fdB));
+        const double2 R0 = cfma(cf[2 * n], fdB, cmul(cf[3 * n], gd));
+        double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + (lane >> h);
+        cu[0] = P0;
+        cu[n] = R0;
+        fd = cfms(fd, cf[8 * n], P0);
+        gd = cfms(gdB, cf[9 * n], R0);
+      }
+    }
+    double2 xs = make_double2(0.0, 0.0), xe = xs;
+    if (lane == 0) {
+      const double2* r = T + 10 * (NX - 1);
+      xs = cfma(r[0], fd, cmul(r[1], gd));
+      xe = cfma(r[2], fd, cmul(r[3], gd));
+    }
+#pragma unroll
+    for (int h = LOGP - S; h >= 1; --h) {
+      const int sft = 1 << (h - 1), n = NX >> h;
+      const bool left = lane < NX && (lane & ((1 << h) - 1)) == 0;
+      const bool right = lane < NX && (lane & ((1 << h) - 1)) == sft;
+      double2 xm = make_double2(0.0, 0.0), xm1 = xm;
+      if (left) {
+        const double2* cf = T + 10 * (NX - 2 * n) + (lane >> h);
+        const double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + (lane >> h);
+        xm = cfma(cf[5 * n], xe, cfma(cf[4 * n], xs, cu[0]));
+        xm1 = cfma(cf[7 * n], xe, cfma(cf[6 * n], xs, cu[n]));
+      }
+      const double2 rs = shfl_up2(xm1, sft), re = shfl_up2(xe, sft);
+      if (left) xe = xm;
+      if (right) { xs = rs; xe = re; }
+    }
+    if (lane < NX) { BX[lane] = xs; BX[NX + lane] = xe; }
+  }
+  __syncthreads();
+  TRV_STAMP(3);
+  // ---------------- down levels S..1 inside each warp
+  double2 xs = make_double2(0.0, 0.0), xe = xs;
+  if ((lane & ((1 << S) - 1)) == 0) { xs = BX[p >> S]; xe = BX[NX + (p >> S)]; }
+#pragma unroll
+  for (int l = S; l >= 1; --l) {
+    const int sft = 1 << (l - 1);
+    const bool left = (lane & ((1 << l) - 1)) == 0;
+    const bool right = (lane & ((1 << l) - 1)) == sft;
+    double2 xm = make_double2(0.0, 0.0), xm1 = xm;
+    if (left) {
+      double2 cf[6];
+      get_cf(l, p >> l, cf);
+      unmerge(cf, xs, xe, xm, xm1);
+    }
+    const double2 rs = shfl_up2(xm1, sft), re = shfl_up2(xe, sft);
+    if (left) xe = xm;
+    if (right) { xs = rs; xe = re; }
+  }
+  TRV_STAMP(4);
+  // ---------------- back-substitution into D (the hand-over area there is dead)
+  D[sidx(i0)] = xs;
+  D[sidx(i1 - 1)] = xe;
+#pragma unroll
+  for (int j = 1; j < L - 1; ++j)
+    if (UNI ? (j < L - 2 || len == L) : j <= len - 2) D[sidx(i0 + j)] = cfms(cfms(dl[j], ap[j], xs), gp[j], xe);
+  if (p == 0 && T[TS - 1].x != 0.0) atomicOr(status, 1);  // the build flagged this frequency (R29)
+  __syncthreads();
+  TRV_STAMP(5);
+  for (int i = p; i < m; i += P) stg_cs2(dst + i, D[sidx(i)]);
+  for (int i = m + p; i < W; i += P) dst[i] = make_double2(0.0, 0.0);
+  TRV_STAMP(6);
+}
+
 // Small-m path (m < 64): one thread per frequency, plain Thomas on the scaled system.
 __global__ void k_tridiag_small(const double2* __restrict__ what, double2* __restrict__ zhat,
                                 const double* __restrict__ lo, const double* __restrict__ di,
@@ -556,6 +879,65 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
   return cudaErrorInvalidValue;
 }
 
+template <int L, int MAXT, bool UNI, bool BUILD>
+static cudaError_t run_trivar_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+  {
+    int done = 0;
+    cudaError_t ce = cnp_dev_cached((const void*)k_trivar<L, MAXT, UNI, BUILD>, &done, [&](int* v) {
+      *v = 1;
+      return cudaFuncSetAttribute(k_trivar<L, MAXT, UNI, BUILD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024);
+    });
+    if (ce != cudaSuccess) return ce;
+  }
+  constexpr int P = MAXT, NX = trv_nx(P), TS = trv_ts(P);
+  const int MP = tri_rows_alloc(c->nx, t.padsh);
+  const size_t smem = (size_t)(MP + 6 * P + 2 * NX + TS) * sizeof(double2);
+  if (BUILD) {  // plain launch: not part of a PDL chain
+    k_trivar<L, MAXT, UNI, BUILD><<<c->H + 1, P, smem, c->stream>>>(
+        what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_vtab, c->nx, c->ld, t.padsh, t.smask,
+        c->tau_p, c->d_status, c->d_lam1);
+    return cudaGetLastError();
+  }
+  return cnp_launch(c, k_trivar<L, MAXT, UNI, BUILD>, dim3(c->H + 1), dim3(P), smem, what, zhat, c->d_lo, c->d_di,
+                    c->d_up, c->d_sk, c->d_il2, c->d_vtab, c->nx, c->ld, t.padsh, t.smask, c->tau_p, c->d_status,
+                    c->d_lam1);
+}
+
+template <int L, int MAXT, bool BUILD>
+static cudaError_t run_trivar_m(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+  return t.Lmin >= L - 1 ? run_trivar_t<L, MAXT, true, BUILD>(c, t, what, zhat)
+                         : run_trivar_t<L, MAXT, false, BUILD>(c, t, what, zhat);
+}
+
+template <int L, bool BUILD>
+static cudaError_t run_trivar(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
+  switch (t.G) {
+    case 1: return run_trivar_m<L, 32, BUILD>(c, t, what, zhat);
+    case 2: return run_trivar_m<L, 64, BUILD>(c, t, what, zhat);
+    case 4: return run_trivar_m<L, 128, BUILD>(c, t, what, zhat);
+    case 8: return run_trivar_m<L, 256, BUILD>(c, t, what, zhat);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// complex entries per frequency of the variable-row table (0: no table for this operator)
+int trivar_table_stride(int m) {
+  const TriCfg t = tri_cfg(m, 0);
+  return t.small || t.L < 0 ? 0 : trv_ts(32 * t.G);
+}
+
+// (Re)builds the per-handle variable-row table (cnpint_create, cnpint_set_debug); synchronous
+cudaError_t build_trivar_table(cnpint_ctx* c) {
+  if (c->dim != 1 || c->toeplitz || !c->d_vtab) return cudaSuccess;
+  const TriCfg t = tri_cfg(c->nx, 0);
+  if (t.small) return cudaSuccess;
+  cudaError_t e = t.L == 4 ? run_trivar<4, true>(c, t, nullptr, nullptr)
+                : t.L == 8 ? run_trivar<8, true>(c, t, nullptr, nullptr) : cudaErrorInvalidValue;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e;
+}
+
 // fault injection (debug bit 2048): the shifted solve reports a singular pivot, as a genuinely singular
 // system would — exercises the status-word path of cnpint_device_status / cnpint_gmres* deterministically
 __global__ void k_inject_singular(int* status) { atomicOr(status, 1); }
@@ -576,7 +958,10 @@ cudaError_t launch_shifted_solve(cnpint_ctx* c, const double2* what, double2* zh
     k_tridiag_small<<<(K + 127) / 128, 128, 0, c->stream>>>(what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2,
                                                             m, W, c->tau_p, K, c->d_status, c->d_lam1);
     e = cudaGetLastError();
-  } else if (!c->toeplitz) {
+  } else if (!c->toeplitz && !(c->debug & 512)) {
+    e = t.L == 4 ? run_trivar<4, false>(c, t, what, zhat) : t.L == 8 ? run_trivar<8, false>(c, t, what, zhat)
+                                                                      : cudaErrorInvalidValue;
+  } else if (!c->toeplitz) {  // debug 512: the first-generation variable-row kernel
     e = t.L == 4 ? run_tri<MODE_VAR, 4>(c, t, what, zhat) : t.L == 8 ? run_tri<MODE_VAR, 8>(c, t, what, zhat)
                                                                      : cudaErrorInvalidValue;
   } else if (t.fast && !(c->debug & 4)) {

@@ -192,6 +192,51 @@ def test_pinv_k3_tree_variants(name, debug):
     assert s.device_status() == 0
 
 
+@pytest.mark.parametrize("m", [100, 255, 333, 511, 700, 1023, 1500, 2048])
+def test_k3_variable_rows_kernels(m):
+    """Variable-row K3: the round-2 kernel (k_trivar, default: warp-shuffle lower tree, upper tree from the
+    per-handle table built on the device) and the first-generation kernel (debug 512: every merge
+    computed in the solve) agree to 1e-13 (the tabulated merges round differently) and match the oracle's
+    step (b); m spans every chunk configuration (G = 1 … 8 warps per system, 4- and
+    8-row chunks, ragged chunk lengths, the 2048-row maximum).  Bar: 1e-12 against the fp64 oracle up
+    to m = 1023; beyond, the fp64 Thomas oracle's own error nears 1e-12 (shifted systems with
+    ‖Ã‖ ~ m²), so the bar is reading R-tol against the same Thomas run in extended precision:
+    ≤ max(1e-12, 4 × the fp64 oracle's own error)."""
+    w = synth.scaled(synth.C3, m, 64, alpha=0.01)
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 5)[0]
+    N, K = w.N, w.N // 2 + 1
+    what_o = np.fft.fft(precond.gamma(N, w.alpha)[:, None] * v, axis=0)[:K]
+    l1, l2 = precond.lambdas_fft(N, w.alpha)
+    zhat_o = precond.shifted_solve(w, op, l1[:K], l2[:K], what_o)
+    what = s.empty_spec()
+    what[:, : w.n, 0] = torch.from_numpy(np.ascontiguousarray(what_o.real)).to(what.device)
+    what[:, : w.n, 1] = torch.from_numpy(np.ascontiguousarray(what_o.imag)).to(what.device)
+    out = {}
+    for dbg in (0, 512):
+        s.set_debug(dbg)
+        zhat = s.empty_spec()
+        s.shifted_solve(what, zhat)
+        out[dbg] = zhat.clone()
+    s.set_debug(0)
+    zh = torch.view_as_complex(out[0]).cpu().numpy()[:, : w.n]
+    z1 = torch.view_as_complex(out[512]).cpu().numpy()[:, : w.n]
+    assert rel(zh, z1) < 1e-13, (m, rel(zh, z1))
+    if m <= 1023:
+        err = rel(zh, zhat_o)
+        record(f"k3_var_m{m}", forward=err)
+        assert err < 1e-12, (m, err)
+    else:
+        cl = np.clongdouble
+        zt = precond.shifted_solve(w, op, l1[:K].astype(cl), l2[:K].astype(cl), what_o.astype(cl)).astype(complex)
+        err, own = rel(zh, zt), rel(zhat_o, zt)
+        record(f"k3_var_m{m}", forward_vs_extended=err, oracle_own=own)
+        assert err <= max(1e-12, 4 * own), (m, err, own)
+    assert float(out[0][:, w.n:].abs().max()) == 0.0 if s.ld > w.n else True
+    assert s.device_status() == 0
+
+
 @pytest.mark.parametrize("name", ["1d_N2048_C2", "1d_N2048_ragged", "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8",
                                   "1d_N32768"])
 @pytest.mark.parametrize("debug", [0, 16, 8])
