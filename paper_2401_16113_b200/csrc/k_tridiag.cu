@@ -495,8 +495,9 @@ CNP_DEV bool merge_tab(Seg& A, const Seg& B, double2* tb, int st) {
 __host__ __device__ constexpr int trv_nx(int P) { return P >> ((P / 32) > 4 ? ((P / 32) == 8 ? 3 : 4) : 2); }
 __host__ __device__ constexpr int trv_ts(int P) { return 10 * (trv_nx(P) - 1) + 5; }
 
-template <int L, int MAXT, bool UNI, bool BUILD>
-__global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? CNPINT_TRIVAR_MINB * 128 / MAXT : 1)
+template <int L, int MAXT, bool UNI, bool BUILD, bool APS>
+__global__ void __launch_bounds__(MAXT, ((APS ? CNPINT_TRIVAR_MINB + 1 : CNPINT_TRIVAR_MINB) * 128 / MAXT) > 0
+                                            ? (APS ? CNPINT_TRIVAR_MINB + 1 : CNPINT_TRIVAR_MINB) * 128 / MAXT : 1)
     k_trivar(const double2* __restrict__ what, double2* __restrict__ zhat, const double* __restrict__ lo,
              const double* __restrict__ di, const double* __restrict__ up, const double2* __restrict__ sk,
              const double2* __restrict__ il2, double2* __restrict__ vtab, int m, int64_t W, int padsh, int smask,
@@ -513,10 +514,14 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
   extern __shared__ double2 smem[];
   const int p = threadIdx.x, lane = p & 31, warp = p >> 5, k = blockIdx.x;
   const int MP = tri_rows_alloc(m, padsh);
-  double2* const D = smem;          // [MP] rows; the hand-over to warp 0 while the rows are dead
+  // APS: α' of the chunk rows goes to D (where its right-hand side was) and γ' to GP after the sweeps
+  // (fewer registers: four CTAs per SM), else both stay in registers
+  double2* const D = smem;          // [MP] rows; α' (APS) or the hand-over to warp 0 while the rows are dead
   double2* const CF = D + MP;       // [6P] levels 1..S: 6 coefficients per merge; then upper levels: P0, R0
   double2* const BX = CF + 6 * P;   // [2·NX] boundary values handed back by warp 0
   double2* const T = BX + 2 * NX;   // [TS] this frequency's table row (solve)
+  double2* const GP = T + TS;       // APS: [MP] γ'
+  double2* const HO = APS ? GP + MP : D;  // hand-over of the segments to warp 0 ([8·NX] build, [2·NX] solve)
   auto sidx = [&](int i) { return i ^ ((i >> padsh) & smask); };
   const double2 il = __ldg(il2 + k), skk = __ldg(sk + k);
   if (!BUILD) {
@@ -605,6 +610,15 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
       sg.fd = dl[0];
     }
   }
+  if (APS && !BUILD) {
+    __syncthreads();  // every row read from D before α' overwrites it
+#pragma unroll
+    for (int j = 1; j < L - 1; ++j)
+      if (UNI ? (j < L - 2 || len == L) : j <= len - 2) {
+        D[sidx(i0 + j)] = ap[j];
+        GP[sidx(i0 + j)] = gp[j];
+      }
+  }
   TRV_STAMP(2);
   auto put_cf = [&](int l, int q, const double2* cf) {
     const int n = P >> l;
@@ -629,14 +643,14 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
       else put_cf(l, p >> l, cf);
     }
   }
-  __syncthreads();  // every row read from D: the hand-over area may overwrite it
+  if (!APS) __syncthreads();  // every row read from D: the hand-over area may overwrite it
   if ((lane & ((1 << S) - 1)) == 0) {
     const int t = p >> S;
     if (BUILD) {
-      D[t] = sg.fa; D[NX + t] = sg.fb; D[2 * NX + t] = sg.fc;
-      D[4 * NX + t] = sg.ga; D[5 * NX + t] = sg.gb; D[6 * NX + t] = sg.gc;
+      HO[t] = sg.fa; HO[NX + t] = sg.fb; HO[2 * NX + t] = sg.fc;
+      HO[4 * NX + t] = sg.ga; HO[5 * NX + t] = sg.gb; HO[6 * NX + t] = sg.gc;
     } else {
-      D[3 * NX + t] = sg.fd; D[7 * NX + t] = sg.gd;
+      HO[t] = sg.fd; HO[NX + t] = sg.gd;
     }
   }
   if (BUILD) {
@@ -645,8 +659,8 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
     if (warp == 0) {
       Seg t;
       const int u = lane < NX ? lane : 0;
-      t.fa = D[u]; t.fb = D[NX + u]; t.fc = D[2 * NX + u]; t.fd = make_double2(0.0, 0.0);
-      t.ga = D[4 * NX + u]; t.gb = D[5 * NX + u]; t.gc = D[6 * NX + u]; t.gd = t.fd;
+      t.fa = HO[u]; t.fb = HO[NX + u]; t.fc = HO[2 * NX + u]; t.fd = make_double2(0.0, 0.0);
+      t.ga = HO[4 * NX + u]; t.gb = HO[5 * NX + u]; t.gc = HO[6 * NX + u]; t.gd = t.fd;
       double2* const tr = vtab + (size_t)k * TS;
       bool wok = true;
 #pragma unroll
@@ -673,21 +687,25 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
   // the table: the tree carries only (fd, gd) up and (x_s, x_e) down
   if (warp == 0) {
     const int u = lane < NX ? lane : 0;
-    double2 fd = D[3 * NX + u], gd = D[7 * NX + u];
+    double2 fd = HO[u], gd = HO[NX + u];
+    // every lane runs the arithmetic (lanes that do not merge at a level read a valid table slot and
+    // discard the result): no divergent branches on the serial chain of levels
 #pragma unroll
     for (int h = 1; h <= LOGP - S; ++h) {
-      const int sft = 1 << (h - 1), n = NX >> h;
+      const int sft = 1 << (h - 1), n = NX >> h, q = u >> h;
+      const bool left = lane < NX && (lane & ((1 << h) - 1)) == 0;
       const double2 fdB = shfl_down<double2>(fd, sft), gdB = shfl_down<double2>(gd, sft);
-      if (lane < NX && (lane & ((1 << h) - 1)) == 0) {
-        const double2* cf = T + 10 * (NX - 2 * n) + (lane >> h);
-        const double2 P0 = cfma(cf[0], gd, cmul(cf[n], fdB));
-        const double2 R0 = cfma(cf[2 * n], fdB, cmul(cf[3 * n], gd));
-        double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + (lane >> h);
+      const double2* cf = T + 10 * (NX - 2 * n) + q;
+      const double2 P0 = cfma(cf[0], gd, cmul(cf[n], fdB));
+      const double2 R0 = cfma(cf[2 * n], fdB, cmul(cf[3 * n], gd));
+      if (left) {
+        double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + q;
         cu[0] = P0;
         cu[n] = R0;
-        fd = cfms(fd, cf[8 * n], P0);
-        gd = cfms(gdB, cf[9 * n], R0);
       }
+      const double2 fdn = cfms(fd, cf[8 * n], P0), gdn = cfms(gdB, cf[9 * n], R0);
+      fd = left ? fdn : fd;
+      gd = left ? gdn : gd;
     }
     double2 xs = make_double2(0.0, 0.0), xe = xs;
     if (lane == 0) {
@@ -697,16 +715,13 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
     }
 #pragma unroll
     for (int h = LOGP - S; h >= 1; --h) {
-      const int sft = 1 << (h - 1), n = NX >> h;
+      const int sft = 1 << (h - 1), n = NX >> h, q = u >> h;
       const bool left = lane < NX && (lane & ((1 << h) - 1)) == 0;
       const bool right = lane < NX && (lane & ((1 << h) - 1)) == sft;
-      double2 xm = make_double2(0.0, 0.0), xm1 = xm;
-      if (left) {
-        const double2* cf = T + 10 * (NX - 2 * n) + (lane >> h);
-        const double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + (lane >> h);
-        xm = cfma(cf[5 * n], xe, cfma(cf[4 * n], xs, cu[0]));
-        xm1 = cfma(cf[7 * n], xe, cfma(cf[6 * n], xs, cu[n]));
-      }
+      const double2* cf = T + 10 * (NX - 2 * n) + q;
+      const double2* cu = CF + 6 * (P - NX) + 2 * (NX - 2 * n) + q;
+      const double2 xm = cfma(cf[5 * n], xe, cfma(cf[4 * n], xs, cu[0]));
+      const double2 xm1 = cfma(cf[7 * n], xe, cfma(cf[6 * n], xs, cu[n]));
       const double2 rs = shfl_up2(xm1, sft), re = shfl_up2(xe, sft);
       if (left) xe = xm;
       if (right) { xs = rs; xe = re; }
@@ -739,7 +754,10 @@ __global__ void __launch_bounds__(MAXT, (CNPINT_TRIVAR_MINB * 128 / MAXT) > 0 ? 
   D[sidx(i1 - 1)] = xe;
 #pragma unroll
   for (int j = 1; j < L - 1; ++j)
-    if (UNI ? (j < L - 2 || len == L) : j <= len - 2) D[sidx(i0 + j)] = cfms(cfms(dl[j], ap[j], xs), gp[j], xe);
+    if (UNI ? (j < L - 2 || len == L) : j <= len - 2) {
+      const int q = sidx(i0 + j);
+      D[q] = APS ? cfms(cfms(dl[j], D[q], xs), GP[q], xe) : cfms(cfms(dl[j], ap[j], xs), gp[j], xe);
+    }
   if (p == 0 && T[TS - 1].x != 0.0) atomicOr(status, 1);  // the build flagged this frequency (R29)
   __syncthreads();
   TRV_STAMP(5);
@@ -879,35 +897,39 @@ static cudaError_t run_tri(cnpint_ctx* c, const TriCfg& t, const double2* what, 
   return cudaErrorInvalidValue;
 }
 
-template <int L, int MAXT, bool UNI, bool BUILD>
+template <int L, int MAXT, bool UNI, bool BUILD, bool APS>
 static cudaError_t run_trivar_t(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
   {
     int done = 0;
-    cudaError_t ce = cnp_dev_cached((const void*)k_trivar<L, MAXT, UNI, BUILD>, &done, [&](int* v) {
+    cudaError_t ce = cnp_dev_cached((const void*)k_trivar<L, MAXT, UNI, BUILD, APS>, &done, [&](int* v) {
       *v = 1;
-      return cudaFuncSetAttribute(k_trivar<L, MAXT, UNI, BUILD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      return cudaFuncSetAttribute(k_trivar<L, MAXT, UNI, BUILD, APS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   227 * 1024);
     });
     if (ce != cudaSuccess) return ce;
   }
   constexpr int P = MAXT, NX = trv_nx(P), TS = trv_ts(P);
   const int MP = tri_rows_alloc(c->nx, t.padsh);
-  const size_t smem = (size_t)(MP + 6 * P + 2 * NX + TS) * sizeof(double2);
+  const size_t smem = (size_t)(MP + 6 * P + 2 * NX + TS + (APS ? MP + 2 * NX : 0)) * sizeof(double2);
   if (BUILD) {  // plain launch: not part of a PDL chain
-    k_trivar<L, MAXT, UNI, BUILD><<<c->H + 1, P, smem, c->stream>>>(
+    k_trivar<L, MAXT, UNI, BUILD, APS><<<c->H + 1, P, smem, c->stream>>>(
         what, zhat, c->d_lo, c->d_di, c->d_up, c->d_sk, c->d_il2, c->d_vtab, c->nx, c->ld, t.padsh, t.smask,
         c->tau_p, c->d_status, c->d_lam1);
     return cudaGetLastError();
   }
-  return cnp_launch(c, k_trivar<L, MAXT, UNI, BUILD>, dim3(c->H + 1), dim3(P), smem, what, zhat, c->d_lo, c->d_di,
+  return cnp_launch(c, k_trivar<L, MAXT, UNI, BUILD, APS>, dim3(c->H + 1), dim3(P), smem, what, zhat, c->d_lo, c->d_di,
                     c->d_up, c->d_sk, c->d_il2, c->d_vtab, c->nx, c->ld, t.padsh, t.smask, c->tau_p, c->d_status,
                     c->d_lam1);
 }
 
+#ifndef CNPINT_TRIVAR_APS
+#define CNPINT_TRIVAR_APS 1
+#endif
 template <int L, int MAXT, bool BUILD>
 static cudaError_t run_trivar_m(cnpint_ctx* c, const TriCfg& t, const double2* what, double2* zhat) {
-  return t.Lmin >= L - 1 ? run_trivar_t<L, MAXT, true, BUILD>(c, t, what, zhat)
-                         : run_trivar_t<L, MAXT, false, BUILD>(c, t, what, zhat);
+  constexpr bool APS = CNPINT_TRIVAR_APS && !BUILD;
+  return t.Lmin >= L - 1 ? run_trivar_t<L, MAXT, true, BUILD, APS>(c, t, what, zhat)
+                         : run_trivar_t<L, MAXT, false, BUILD, APS>(c, t, what, zhat);
 }
 
 template <int L, bool BUILD>
