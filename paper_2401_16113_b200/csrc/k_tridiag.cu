@@ -509,7 +509,6 @@ __global__ void __launch_bounds__(MAXT, ((APS ? CNPINT_TRIVAR_MINB + 1 : CNPINT_
   constexpr int LOGP = 5 + LOGG;
   constexpr int TS = trv_ts(P);
   static_assert(NX == trv_nx(P) && NX <= 32, "hand-over to one warp");
-  if (!BUILD) pdl_enter();
   TRV_STAMP(0);
   extern __shared__ double2 smem[];
   const int p = threadIdx.x, lane = p & 31, warp = p >> 5, k = blockIdx.x;
@@ -523,21 +522,15 @@ __global__ void __launch_bounds__(MAXT, ((APS ? CNPINT_TRIVAR_MINB + 1 : CNPINT_
   double2* const GP = T + TS;       // APS: [MP] γ'
   double2* const HO = APS ? GP + MP : D;  // hand-over of the segments to warp 0 ([8·NX] build, [2·NX] solve)
   auto sidx = [&](int i) { return i ^ ((i >> padsh) & smask); };
+  // create-time constants first (the frequency's scalars, the chunk's rows, the table row): with PDL
+  // their latency overlaps the previous kernel's tail; the system itself only after griddepcontrol.wait
   const double2 il = __ldg(il2 + k), skk = __ldg(sk + k);
-  if (!BUILD) {
-    const double2* src = what + (int64_t)k * W;
-    for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
-    const double2* tr = vtab + (size_t)k * TS;
-    for (int i = p; i < TS; i += P) cp_async16(T + i, tr + i);
-  }
-  cp_async_commit();
   const int Lmin = m / P, nlong = m - P * Lmin;
   const int len = p < nlong ? Lmin + 1 : Lmin;
   const int i0 = p < nlong ? p * (Lmin + 1) : nlong * (Lmin + 1) + (p - nlong) * Lmin;
   const int i1 = i0 + len;
   auto has = [&](int j) { return UNI ? (j < L - 1 || len == L) : j < len; };  // row j of the chunk exists
-  // the chunk's rows while the copy is in flight (lo, di, up are zero padded to ld >= m)
-  double ra[L], rc[L], rd[L];
+  double ra[L], rc[L], rd[L];  // lo, di, up are zero padded to ld >= m
 #pragma unroll
   for (int j = 0; j < L; ++j) {
     const int i = has(j) ? i0 + j : i0;
@@ -545,6 +538,14 @@ __global__ void __launch_bounds__(MAXT, ((APS ? CNPINT_TRIVAR_MINB + 1 : CNPINT_
     rc[j] = __ldg(up + i);
     rd[j] = __ldg(di + i);
   }
+  if (!BUILD) {
+    const double2* tr = vtab + (size_t)k * TS;
+    for (int i = p; i < TS; i += P) cp_async16(T + i, tr + i);
+    pdl_enter();
+    const double2* src = what + (int64_t)k * W;
+    for (int i = p; i < m; i += P) cp_async16(D + sidx(i), src + i);
+  }
+  cp_async_commit();
   bool ok = true;
   cp_async_wait<0>();
   __syncthreads();
