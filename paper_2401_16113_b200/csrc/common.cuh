@@ -48,12 +48,19 @@ CNP_DEV bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
 
 // Programmatic dependent launch: a kernel launched with the PDL attribute (cnp_launch) may become
 // resident while its predecessor drains; griddepcontrol.wait blocks until the predecessor grid has
-// completed and its writes are visible (a no-op for a plain launch), launch_dependents lets the next
-// kernel's launch begin.  Every kernel calls this before its first access to data another kernel
-// wrote, so the memory semantics are those of plain stream order.
+// completed and its writes are visible (a no-op for a plain launch).  Every kernel calls this before its
+// first access to data another kernel wrote, so the memory semantics are those of plain stream order.
+// The dependents' launch is triggered implicitly as each CTA exits: an explicit
+// griddepcontrol.launch_dependents right after the wait (round 1) let the next grid's CTAs become
+// resident for the whole life of the current one and cost 12 % at c5 n511 N1024 (49.4 vs 43.4 ms per
+// solve) and 10 % at c3 (2.83 vs 2.51 ms), while the exit trigger is as fast as or faster than both
+// that and plain launches at every BASELINE size (profiles/r02_pdl_trigger_ab.txt).
+// -DCNPINT_PDL_EARLY_TRIGGER restores the early trigger (A/B only).
 CNP_DEV void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef CNPINT_PDL_EARLY_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ reductions
