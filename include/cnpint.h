@@ -316,7 +316,9 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 16384 = the lean 2D time pass (k_tpass2.cu) also at N = 512 (default at N = 256, 1024; debug 64 turns
  * both register time passes off in favour of the cluster kernel); 32768 = the three-pass 2D P_α⁻¹: W⁻¹
  * and W each as one fused x+y sine pass (k_dstxy.cu, n + 1 ∈ {64, …, 512}; 48 instead of 80 B of HBM
- * traffic per unknown, but no faster on B200: the passes are bound on chip, K5). */
+ * traffic per unknown, but no faster on B200: the passes are bound on chip, K5);
+ * 131072 = no fusion of the 2D Gram update with the next x sine pass (k_upd_dst4; cnpint_gmres fuses them
+ * when the lean x pass applies and the next Arnoldi step is expected to run). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -32,7 +32,8 @@ struct CnpProf {
 
 static const char* const KNAMES[KID_COUNT] = {"K1_matvec", "K2_time_fft", "K3_tridiag", "K4_time_ifft",
                                               "K6_time_pass_2d", "K5_dst_x", "K5_dst_y", "K7_dots",
-                                              "K7_update", "reduce", "K8_small", "K5_dst_xy"};
+                                              "K7_update", "reduce", "K8_small", "K5_dst_xy",
+                                              "K7_update+K5_dst_x"};
 
 void cnp_prof_begin(cnpint_ctx* c, int kid) {
   CnpProf* p = (CnpProf*)c->prof;
@@ -420,7 +421,10 @@ cnpint_status pinv_dev(cnpint_ctx* c, const double* in, const double* vscale, do
       if (e != cudaErrorNotSupported) return cuda_fail(c, e, "launch_dstxy");
       (void)cudaGetLastError();
     }
-    CK(launch_dst_x(c, in, a, nullptr, 0));
+    // the first pass may already be done: the Gram update that wrote `in` also wrote its x pass into tmp1
+    const bool have_x = c->xdst_src == in && a == c->d_tmp1;
+    c->xdst_src = nullptr;
+    if (!have_x) CK(launch_dst_x(c, in, a, nullptr, 0));
     CK(launch_dst_y(c, a, b, 0));
     CK(launch_time_pass_2d(c, b, a, vscale));  // GMRES scale folded into the Γ-scaling
     CK(launch_dst_y(c, a, b, 1));
@@ -837,6 +841,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
                            cnpint_gmres_report* rep) {
   if (cnpint_status a = gmres_args(c, d_b, d_u, tol, restart, maxit)) return a;
   c->post = PostOp{};
+  c->xdst_src = nullptr;
   auto t0 = std::chrono::steady_clock::now();
   const int64_t vec = c->vec;
   double* h = c->h_pinned;
@@ -856,6 +861,9 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   // quantity of that step is then 0 or NaN and is discarded) and a non-finite b are handled
   std::vector<double*> Z(restart);
   for (int i = 0; i < restart; ++i) Z[i] = c->d_Z + (size_t)i * vec;
+  // the latest residual estimate (relative) and the one before, for the update + x-pass fusion: it is
+  // used when the next Arnoldi step is expected to run, est_next ≈ est·min(1, est/est_before) > tol
+  double est_now = 1.0, est_before = -1.0;
   while (true) {
     int jdone = 0;
     bool stop_inner = false;
@@ -873,7 +881,14 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
         // — the same two projections as classic CGS2, one reading pass fewer
         CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
         c->post = post_gram_finalize(c, j);
-        CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));
+        const double est_next = est_before > 0.0 ? est_now * std::min(1.0, est_now / est_before) : est_now;
+        if (upd_dst_ok(c) && j + 1 < restart && its + 1 < maxit && est_next > tol) {
+          // 2D: the update also writes the x sine pass of Ṽ_{j+1} (the first pass of the next P⁻¹)
+          CK(launch_cgs2_pass_dst(c, V.data(), nv, c->d_c1, w, c->d_part, c->d_cg, c->d_tmp1));
+          c->xdst_src = w;
+        } else {
+          CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));
+        }
       } else {
         if (nv <= CNP_MAX_DOT) {
           // w = 𝓜 z_j fused with CGS pass 1 (c1 = Ṽᵀw); classic second pass (debug bit 128)
@@ -903,6 +918,8 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       ++its;
       jdone = j + 1;
       est = h[1];
+      est_before = est_now;
+      est_now = est;
       if (rep && rep->history && its - 1 < rep->history_cap) rep->history[its - 1] = est;
       if (h[8] != 0.0) {  // the step's P⁻¹ met a singular shifted system: stop now (status word read back)
         cnpint_status ds = cnpint_device_status(c);
@@ -918,6 +935,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       if (est <= tol || its >= maxit || h[5] != 0.0) stop_inner = true;
     }
     // cycle end: y = H⁻¹g, u += Σ y_j z_j  (= P⁻¹ V y: the stored z_j make the extra P⁻¹ unnecessary)
+    c->xdst_src = nullptr;  // a speculative x pass of the last Ṽ_{j+1} is not used
     if (jdone <= CNP_MAX_DOT) {  // back-substitution inside the combine kernel
       CK(launch_combine_backsolve(c, Z.data(), jdone, 0, cycles == 0 ? nullptr : d_u, d_u));
     } else {

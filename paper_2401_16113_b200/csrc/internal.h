@@ -16,7 +16,7 @@
 // kernel classes for the per-class event profiler (cnpint_profile_*)
 enum {
   KID_MATVEC = 0, KID_FFT_FWD, KID_TRIDIAG, KID_FFT_INV, KID_TIMEPASS2D, KID_DST_X, KID_DST_Y,
-  KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_DST_XY, KID_COUNT
+  KID_DOTS, KID_UPDATE, KID_REDUCE, KID_SMALL, KID_DST_XY, KID_UPD_DST, KID_COUNT
 };
 
 // K3 launch configuration (k_tridiag.cu): G warps per system, L = max rows per thread chunk,
@@ -135,6 +135,9 @@ struct cnpint_ctx {
   int last_nv;            // basis vectors Ṽ_0..Ṽ_{last_nv−1} of that cycle
   double* h_stage_in;  // (lazily) pinned host staging not used; host API copies pageable memory
   int64_t launches;
+  // 2D right GMRES: the vector whose x sine pass the last Gram update already wrote into d_tmp1
+  // (k_upd_dst4); the next pinv_dev of exactly that vector skips its first pass, any pinv_dev clears it
+  const double* xdst_src;
   void* prof;          // CnpProf* (host event pools), null when profiling is off
   char err[512];
 };
@@ -192,6 +195,9 @@ cudaError_t launch_dots(cnpint_ctx* c, double* const* V, int nv, const double* w
 cudaError_t launch_reduce(cnpint_ctx* c, const double* part, int ncols, double* out, int accumulate_sq);
 cudaError_t launch_combine_backsolve(cnpint_ctx* c, double* const* X, int nv, int scaled, const double* u_in,
                                      double* u_out);
+bool upd_dst_ok(const cnpint_ctx* c);
+cudaError_t launch_cgs2_pass_dst(cnpint_ctx* c, double* const* Vp, int nv, const double* c1, double* w,
+                                 double* part, double* out, double* dout);
 cudaError_t launch_cgs2_pass(cnpint_ctx* c, double* const* V, int nv, const double* c1, const double* c2,
                              double* w, double* part, double* out, int phase);
 cudaError_t launch_update(cnpint_ctx* c, double* const* V, int nv, const double* coefsrc, int coefmode,

@@ -11,12 +11,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c5_n511_N1024")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--debug", type=int, default=0)
     a = ap.parse_args()
     import torch
     import synth
     from paper_2401_16113_b200 import problems
     w = synth.WORKLOADS[a.workload]
     s = problems.make_solver(w, restart_max=w.restart)
+    if a.debug:
+        s.set_debug(a.debug)
     b = problems.rhs(w, s)
     u = s.empty()
     st = torch.cuda.current_stream()
@@ -38,7 +41,7 @@ def main():
     prof = s.profile_read()
     s.profile_enable(False)
     ksum = sum(v[0] for v in prof.values()) / a.reps
-    print(json.dumps({"workload": a.workload, "pdl": os.environ.get("CNPINT_PDL", "1"), "event_ms": ev,
+    print(json.dumps({"workload": a.workload, "pdl": os.environ.get("CNPINT_PDL", "1"), "debug": a.debug, "event_ms": ev,
                       "host_wall_ms": wall, "report_seconds_ms": 1e3 * sum(r["seconds"] for r in reps) / a.reps,
                       "kernel_sum_ms": ksum, "gap_ms": ev - ksum, "iterations": reps[-1]["iterations"],
                       "classes": {k: round(v[0] / a.reps, 3) for k, v in prof.items()}}))

@@ -237,6 +237,34 @@ def test_k3_variable_rows_kernels(m):
     assert s.device_status() == 0
 
 
+@pytest.mark.parametrize("case", [(63, 64, 0.01), (127, 256, 0.01), (255, 512, 0.01), (31, 32, 0.1)])
+def test_gmres_update_fused_with_x_pass(case):
+    """2D right GMRES: the Gram update fused with the next P_α⁻¹'s x sine pass (k_upd_dst4, default) and
+    the separate kernels (debug 131072) give the same iterations, histories and solution (the fused
+    kernel's reductions sum in another order: 1e-12), and the solution matches sequential CN."""
+    n, N, alpha = case
+    w = synth.scaled(synth.C4, n, N, alpha=alpha)
+    s = solver_for(w, restart_max=w.restart)
+    b = problems.rhs(w, s)
+    out = {}
+    for dbg in (0, 131072):
+        s.set_debug(dbg)
+        u = s.empty()
+        rep = s.gmres(b, u, w.tol, w.restart)
+        assert rep["converged"], (case, dbg, rep)
+        out[dbg] = (rep, s.to_host(u))
+    s.set_debug(0)
+    (r0, u0), (r1, u1) = out[0], out[131072]
+    assert r0["iterations"] == r1["iterations"], (r0["iterations"], r1["iterations"])
+    h0, h1 = np.array(r0["history"]), np.array(r1["history"])
+    assert np.all(np.abs(h0 - h1) <= 1e-9 * np.abs(h1) + 1e-15), (h0, h1)
+    assert rel(u0, u1) < 1e-12, rel(u0, u1)
+    op = problem.build_operator(w)
+    useq = aao.solve_sequential(w, op, problem.assemble_rhs(w, op))
+    assert rel(u0, useq) < 1e-8
+    record(f"gmres_fused_x_n{n}_N{N}", its=r0["iterations"], fused_vs_separate=rel(u0, u1))
+
+
 @pytest.mark.parametrize("name", ["1d_N2048_C2", "1d_N2048_ragged", "1d_N4096_C2", "1d_N8192_C8", "1d_N16384_C8",
                                   "1d_N32768"])
 @pytest.mark.parametrize("debug", [0, 16, 8])
