@@ -318,7 +318,9 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * and W each as one fused x+y sine pass (k_dstxy.cu, n + 1 ∈ {64, …, 512}; 48 instead of 80 B of HBM
  * traffic per unknown, but no faster on B200: the passes are bound on chip, K5);
  * 131072 = no fusion of the 2D Gram update with the next x sine pass (k_upd_dst4; cnpint_gmres fuses them
- * when the lean x pass applies and the next Arnoldi step is expected to run). */
+ * when the lean x pass applies and the next Arnoldi step is expected to run);
+ * 262144 = the first-generation lean time pass (divide by λ1_k − λ2_kμ) instead of the second (k_tpass2
+ * GEN 2: ½/λ2_k folded into the forward output, then ÷ (c_k − μ) with c_k = λ1_k/λ2_k from per-mode tables). */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

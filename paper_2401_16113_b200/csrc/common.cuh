@@ -39,6 +39,15 @@ CNP_DEV double2 crecip_nr(double2 a) {
   r = fma(r, e, r);
   return make_double2(a.x * r, -a.y * r);
 }
+// 1/d for real d > 0: hardware reciprocal + two Newton steps (within an ulp, no slow path)
+CNP_DEV double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
 // multiply by -i (forward) or +i (inverse)
 template <bool INV>
 CNP_DEV double2 cmul_mi(double2 a) {

@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(FsGeo<MODE, LOG1, LOG2>::NT, FsGeo<MODE, LOG1,
           double2 z[F1::R2];
           if (j < F1::R1) {
             const int k1 = j;
-            double mua = 0.0, mub = 0.0;
+            double mua = 1.0, mub = 1.0;  // padding columns: μ = 1 (α = 1 has λ1_0 = 0; see k_tpass2.cu)
             if (colok && !padA) {
               const int yy = mycol / a.ld;
               mua = a.tau * (a.ex[xin] + a.ey[yy]) + a.tau_shift;

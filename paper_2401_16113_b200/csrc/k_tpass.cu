@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(TpPlan<LOGN>::NT, TpPlan<LOGN>::MINB)
     __syncthreads();
     double2 z[F::R3];
     if (r < F::T3) {
-      double mua = 0.0, mub = 0.0;
+      double mua = 1.0, mub = 1.0;  // padding columns: μ = 1 (α = 1 has λ1_0 = 0; see k_tpass2.cu)
       if (ok && !padA) {
         mua = tau * (ex[xin] + ey[yy]) + tau_shift;
         if (!padB) mub = tau * (ex[xin + 1] + ey[yy]) + tau_shift;

@@ -28,26 +28,30 @@ struct T2Plan {
   static constexpr size_t off_lam = off_tw + (size_t)N * 16;
   static constexpr size_t off_g = off_lam + (size_t)2 * (H + 1) * 16;
   static constexpr size_t bytes = off_g + (size_t)2 * N * 8;
+  // GEN 2: per-mode tables f_k = ½/λ2_k (complex) and (c_k = λ1_k/λ2_k, c_k.y², κ_k) instead of λ1, λ2
+  static constexpr size_t off_f2 = off_g + (size_t)2 * N * 8;
+  static constexpr size_t bytes2 = off_f2 + (size_t)(H + 1) * 16;
   static_assert(F3 == B1, "forward output items = inverse input items");
   static_assert(F1 >= 1 && F2 >= 1 && F3 >= 1 && B2 >= 1 && B3 >= 1, "every step has whole items per thread");
 };
 
-template <int LOGN>
+template <int LOGN, int GEN>
 __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
     k_tpass2(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ vscale, int64_t W,
              int ld, int nx, const double* __restrict__ gam, const double* __restrict__ igam,
-             const double2* __restrict__ lam1, const double2* __restrict__ lam2, const double* __restrict__ ex,
-             const double* __restrict__ ey, double tau, double tau_shift, const double2* __restrict__ twN,
-             int debug_sign) {
+             const double2* __restrict__ lam1, const double2* __restrict__ lam2, const double2* __restrict__ sk,
+             const double2* __restrict__ il2, const double* __restrict__ ex, const double* __restrict__ ey,
+             double tau, double tau_shift, const double2* __restrict__ twN, int debug_sign) {
   using PL = T2Plan<LOGN>;
   constexpr int N = PL::N, H = PL::H, TP = PL::TP, P = PL::P, NT = PL::NT, RS = PL::RS;
   constexpr int R1 = PL::R1, R2 = PL::R2, R3 = PL::R3;
   char* const smem = reinterpret_cast<char*>(fft_smem);
   double2* const tw = reinterpret_cast<double2*>(smem + PL::off_tw);   // ω_N^q
-  double2* const l1s = reinterpret_cast<double2*>(smem + PL::off_lam);
-  double2* const l2s = l1s + (H + 1);
+  double2* const l1s = reinterpret_cast<double2*>(smem + PL::off_lam);  // GEN 1: λ1_k; GEN 2: (c_k.x, c_k.y)
+  double2* const l2s = l1s + (H + 1);                                   // GEN 1: λ2_k; GEN 2: (c_k.y², κ_k)
   double* const gs = reinterpret_cast<double*>(smem + PL::off_g);      // γ_t
   double* const igs = gs + N;                                          // 1/(N γ_t)
+  double2* const fs = reinterpret_cast<double2*>(smem + PL::off_f2);    // GEN 2: f_k = ½/λ2_k (½/λ1_k if λ2_k = 0)
   const int tid = threadIdx.x, pr = tid % P, r = tid / P;
   double2* const A = reinterpret_cast<double2*>(smem) + pr * RS;
   const double sg = debug_sign ? -1.0 : 1.0;
@@ -59,8 +63,20 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
     igs[q] = igam[q];
   }
   for (int q = tid; q <= H; q += NT) {
-    l1s[q] = lam1[q];
-    l2s[q] = lam2[q];
+    if constexpr (GEN == 1) {
+      l1s[q] = lam1[q];
+      l2s[q] = lam2[q];
+    } else {
+      // 1/(λ1 − λ2 μ) = (1/λ2)·1/(c − μ), c = λ1/λ2 (host long double); α = 1, k = N/2 has λ2 = 0:
+      // there 1/λ1 with c = 1, κ = 0 (no μ term)
+      const double2 i2 = il2[q];
+      const bool z = i2.x == 0.0 && i2.y == 0.0;
+      const double2 cq = z ? make_double2(1.0, 0.0) : sk[q];
+      const double2 fq = z ? crecip(lam1[q]) : i2;
+      l1s[q] = cq;
+      l2s[q] = make_double2(cq.y * cq.y, z ? 0.0 : 1.0);
+      fs[q] = cscale(fq, 0.5);
+    }
   }
   pdl_enter();  // PDL: tables above are create-time constants; the basis scale and the input come from earlier kernels
   const double s = vscale ? *vscale : 1.0;
@@ -121,11 +137,20 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
     for (int i = 0; i < PL::F3; ++i) {
       const int q = r + i * TP;
 #pragma unroll
-      for (int k3 = 0; k3 < R3; ++k3) A[q + R1 * R2 * k3] = z[i][k3];
+      for (int k3 = 0; k3 < R3; ++k3) {
+        if constexpr (GEN >= 2) {
+          const int k = q + R1 * R2 * k3;
+          const double2 f = k <= H ? fs[k] : cconj(fs[N - k]);
+          z[i][k3] = cmul(z[i][k3], f);
+        }
+        A[q + R1 * R2 * k3] = z[i][k3];
+      }
     }
     __syncthreads();
     // ---- Hermitian separation, the per-mode division, re-packing (frequencies k of this thread)
-    double mua = 0.0, mub = 0.0;
+    // padding columns (input and output exactly 0) take μ = 1: with α = 1 the k = 0 mode has λ1 = 0,
+    // and μ = 0 there would put 0·∞ = NaN into the partner column of the packed pair
+    double mua = 1.0, mub = 1.0;
     if (!padA) mua = tau * (ex[xin] + ey[yy]) + tau_shift;
     if (!padB) mub = tau * (ex[xin + 1] + ey[yy]) + tau_shift;
 #pragma unroll
@@ -135,14 +160,29 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
       for (int k3 = 0; k3 < R3; ++k3) {
         const int k = q + R1 * R2 * k3;
         const double2 zk = z[i][k3], zm = A[(N - k) & (N - 1)];
-        double2 xa = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-        double2 xb = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
-        const double2 l1 = k <= H ? l1s[k] : cconj(l1s[N - k]);
-        const double2 l2 = k <= H ? l2s[k] : cconj(l2s[N - k]);
-        // the divide by a Newton-refined reciprocal (no IEEE-division slow path; within an ulp):
-        // N = 256 416 → 397 µs at c5 n511, N = 1024 neutral (profiles/r02_div_ab.txt)
-        xa = cmul(xa, crecip_nr(csub(l1, cscale(l2, mua))));
-        xb = cmul(xb, crecip_nr(csub(l1, cscale(l2, mub))));
+        double2 xa, xb;
+        if constexpr (GEN == 1) {
+          xa = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+          xb = make_double2(0.5 * (zk.y + zm.y), 0.5 * (zm.x - zk.x));
+          const double2 l1 = k <= H ? l1s[k] : cconj(l1s[N - k]);
+          const double2 l2 = k <= H ? l2s[k] : cconj(l2s[N - k]);
+          // the divide by a Newton-refined reciprocal (no IEEE-division slow path; within an ulp):
+          // N = 256 416 → 397 µs at c5 n511, N = 1024 neutral (profiles/r02_div_ab.txt)
+          xa = cmul(xa, crecip_nr(csub(l1, cscale(l2, mua))));
+          xb = cmul(xb, crecip_nr(csub(l1, cscale(l2, mub))));
+        } else {
+          // zk, zm already carry ½/λ2 (f_{N−k} = conj f_k), so xa = X_a/λ2; then ÷ (c − κμ):
+          // × conj(c − κμ) / |c − κμ|² (12 fp64 per column instead of 17)
+          xa = make_double2(zk.x + zm.x, zk.y - zm.y);
+          xb = make_double2(zk.y + zm.y, zm.x - zk.x);
+          const int kk = k <= H ? k : N - k;
+          const double2 cc = l1s[kk], cq = l2s[kk];
+          const double cy = k <= H ? cc.y : -cc.y;
+          const double ra = fma(-cq.y, mua, cc.x), rb = fma(-cq.y, mub, cc.x);
+          const double na = rcp_nr(fma(ra, ra, cq.x)), nb = rcp_nr(fma(rb, rb, cq.x));
+          xa = make_double2(fma(xa.x, ra, xa.y * cy) * na, fma(xa.y, ra, -xa.x * cy) * na);
+          xb = make_double2(fma(xb.x, rb, xb.y * cy) * nb, fma(xb.y, rb, -xb.x * cy) * nb);
+        }
         z[i][k3] = (k == 0 || k == H) ? make_double2(xa.x, xb.x) : make_double2(xa.x - xb.y, xa.y + xb.x);
       }
     }
@@ -200,16 +240,17 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
   }
 }
 
-template <int LOGN>
+template <int LOGN, int GEN>
 static cudaError_t run_tpass2(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   using PL = T2Plan<LOGN>;
-  auto kern = k_tpass2<LOGN>;
+  auto kern = k_tpass2<LOGN, GEN>;
+  constexpr size_t bytes = GEN == 1 ? PL::bytes : PL::bytes2;
   int grid_max = 0;
   cudaError_t ce = cnp_dev_cached((const void*)kern, &grid_max, [&](int* v) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::bytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PL::NT, PL::bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PL::NT, bytes);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     *v = per_sm * c->num_sms;
     return cudaSuccess;
@@ -217,19 +258,23 @@ static cudaError_t run_tpass2(cnpint_ctx* c, const double* in, double* out, cons
   if (ce != cudaSuccess) return ce;
   const int ntiles = (int)((c->slice / 2 + PL::P - 1) / PL::P);
   const int grid = ntiles < grid_max ? ntiles : grid_max;
-  return cnp_launch(c, kern, dim3(grid), dim3(PL::NT), PL::bytes, in, out, vscale, c->slice, (int)c->ld, c->nx,
+  return cnp_launch(c, kern, dim3(grid), dim3(PL::NT), bytes, in, out, vscale, c->slice, (int)c->ld, c->nx,
                     (const double*)c->d_gam, (const double*)c->d_igam, (const double2*)c->d_lam1,
-                    (const double2*)c->d_lam2, (const double*)c->d_ex, (const double*)c->d_ey, c->tau_p,
-                    c->tau_p * c->shift, (const double2*)c->d_tw, c->debug & 1);
+                    (const double2*)c->d_lam2, (const double2*)c->d_sk, (const double2*)c->d_il2,
+                    (const double*)c->d_ex, (const double*)c->d_ey, c->tau_p, c->tau_p * c->shift,
+                    (const double2*)c->d_tw, c->debug & 1);
 }
 
-// 2D time pass through the lean kernel for N ∈ {256, 512, 1024}; else NotSupported
+// 2D time pass through the lean kernel for N ∈ {256, 512, 1024}; else NotSupported.  Debug 262144 keeps the
+// first generation (divide by λ1 − λ2μ) instead of GEN 2 (divide through the per-mode tables f_k, c_k:
+// c5 n511 N1024 1994 → 1925 µs, N256 388 → 381 µs; profiles/r02_tpass2_gen2_ab.txt).
 cudaError_t launch_tpass2(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
   if (c->dim != 2) return cudaErrorNotSupported;
+  const bool g1 = (c->debug & 262144) != 0;
   switch (c->N) {
-    case 256: return run_tpass2<8>(c, in, out, vscale);
-    case 512: return run_tpass2<9>(c, in, out, vscale);
-    case 1024: return run_tpass2<10>(c, in, out, vscale);
+    case 256: return g1 ? run_tpass2<8, 1>(c, in, out, vscale) : run_tpass2<8, 2>(c, in, out, vscale);
+    case 512: return g1 ? run_tpass2<9, 1>(c, in, out, vscale) : run_tpass2<9, 2>(c, in, out, vscale);
+    case 1024: return g1 ? run_tpass2<10, 1>(c, in, out, vscale) : run_tpass2<10, 2>(c, in, out, vscale);
     default: return cudaErrorNotSupported;
   }
 }

@@ -55,6 +55,11 @@ SMALL = {
     # register 2D time pass (k_tpass.cu): N = 256 and 512
     "2d_n15_N512": synth.scaled(synth.C4, 15, 512, alpha=0.01),
     "2d_n31_N256": synth.scaled(synth.C4, 31, 256, alpha=0.02),
+    # k_tpass2 with a ragged last tile (7·8/2 = 28 column pairs: 3.5 tiles of 8) and P₁ (α = 1: λ2 = 0 at k = N/2)
+    "2d_n7_N256": synth.scaled(synth.C4, 7, 256, alpha=0.05),
+    "2d_n31_N1024_p1": synth.scaled(synth.C4, 31, 1024, alpha=1.0),
+    "2d_n15_N512_p1": synth.scaled(synth.C4, 15, 512, alpha=1.0),
+    "2d_n15_N2048_p1": synth.scaled(synth.C4, 15, 2048, alpha=1.0),
     # NEXT #1: time-dependent operator 𝓛(t) = d(t)𝓛 (Eq. 5.8)
     "1d_tv": synth.scaled(synth.C1T, 63, 64, alpha=0.01),
     "1d_tv_price": synth.scaled(synth.C3, 127, 128, alpha=0.01, dt_rate=0.3),
@@ -319,12 +324,15 @@ def test_dst_paths(name, debug):
     assert s.device_status() == 0
 
 
-@pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2", "2d_n15_N512", "2d_n31_N256"])
-@pytest.mark.parametrize("debug", [0, 16, 64, 16384])
+@pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2", "2d_n15_N512", "2d_n31_N256", "2d_n7_N256",
+                                  "2d_n31_N1024_p1", "2d_n15_N512_p1", "2d_n15_N2048_p1"])
+@pytest.mark.parametrize("debug", [0, 16, 64, 16384, 262144, 16384 | 262144])
 def test_timepass_2d_paths(name, debug):
     """2D time pass: the three-phase four-step kernel (N >= 2048), the lean register kernel k_tpass2
-    (N = 256, 1024; forced at 512 by debug 16384), the register kernel k_tpass_r (N = 512) — defaults
-    (debug 0) — and the cluster kernel (debug 64; debug 16 at N >= 2048) all give the oracle's P⁻¹."""
+    (N = 256, 1024; forced at 512 by debug 16384; its first generation by debug 262144), the register
+    kernel k_tpass_r (N = 512) — defaults (debug 0) — and the cluster kernel (debug 64; debug 16 at
+    N >= 2048) all give the oracle's P⁻¹, also on a ragged last tile and for P₁ (α = 1: λ1_0 = 0, so a
+    padding column packed with a real one must not divide by λ1_0 − λ2_0·0)."""
     w = SMALL[name]
     s = solver_for(w)
     s.set_debug(debug)
