@@ -512,6 +512,7 @@ cnpint_status cnpint_create(cnpint_ctx** out, int N, double T, double alpha, con
   if (!c) return CNPINT_EINVAL;
   std::memset(c, 0, sizeof(*c));
   { const char* e = getenv("CNPINT_PDL"); c->pdl = (e && atoi(e) == 0) ? 0 : 1; }
+  { const char* e = getenv("CNPINT_L2PF"); c->l2pf = (e && atoi(e) == 0) ? 0 : 1; }
   c->dim = op->dim; c->nx = op->nx; c->ny = op->dim == 2 ? op->ny : 1; c->N = N; c->H = N / 2;
   c->toeplitz = op->dim == 2 ? 1 : op->toeplitz;
   c->ld = ld_of(op->nx); c->slice = (int64_t)c->ny * c->ld; c->vec = (int64_t)N * c->slice;

@@ -189,6 +189,11 @@ template <int N>
 CNP_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+// Bulk prefetch of [p, p + bytes) into L2 (TMA unit; p 16-B aligned, bytes a multiple of 16): no
+// registers, no shared memory, no completion to wait for — the later loads of that range hit L2.
+CNP_DEV void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 // Named barrier over `count` threads (multiple of 32); id 1..15 (0 is __syncthreads).
 CNP_DEV void named_sync(int id, int count) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory"); }
 

@@ -112,6 +112,7 @@ struct cnpint_ctx {
   double* d_G;         // [(restart_max+1)²] Gram matrix Ṽᵢᵀ Ṽₖ of the cycle's basis (Gram CGS2)
   double* d_cg;        // [CNP_MAX_DOT+1] the Gram-CGS2 update's fold [‖w‖², Ṽᵀw]
   int pdl;              // launch the GMRES-loop kernels with programmatic dependent launch
+  int l2pf;             // sine / time passes prefetch their next tile into L2 (CNPINT_L2PF=0: off, A/B)
   double* d_part;      // [CNP_RED_BLOCKS][CNP_MAX_DOT+1]
   double* d_c1;        // [restart_max+1] raw dots (pass 1)
   double* d_c2;        // [restart_max+1] raw dots (pass 2)

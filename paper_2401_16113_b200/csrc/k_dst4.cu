@@ -59,7 +59,7 @@ template <int LOGM>
 __global__ void __launch_bounds__(256, DST4_MINB)
     k_dst4(const double* __restrict__ in, double* __restrict__ out, int nlines, int64_t ld,
            const double* __restrict__ pre, const double* __restrict__ post, const double2* __restrict__ tw2M,
-           int accumulate, int debug_sign) {
+           int accumulate, int debug_sign, int l2pf) {
   using PL = D4Plan<LOGM>;
   constexpr int M = PL::M, H = PL::H, n = PL::n, TP = PL::TP, P = PL::P;
   constexpr int R1 = PL::R1, R2 = PL::R2, R3 = PL::R3;
@@ -129,6 +129,10 @@ __global__ void __launch_bounds__(256, DST4_MINB)
 #pragma unroll
       for (int k1 = 0; k1 < R1; ++k1) A[k1 * (M / R1) + m] = k1 ? cmul(v[k1], T1[k1 * (M / R1) + m]) : v[0];
     }
+    // the pair's next two rows (2·ld contiguous doubles; with accumulate also the output rows) into L2
+    // while this pair computes: its step-1 loads then hit L2 (ncu: 21 % of the stall samples)
+    if (l2pf && r < (accumulate ? 2 : 1) && g + stride < npairs)
+      prefetch_l2((r == 0 ? ra : out + (ra - in)) + 2 * (int64_t)stride * ld, (unsigned)(2 * ld * 8));
     pair_sync(bar, TP);
     // ---- step 2: item (k1, m3): B[k1][m3 + R3 m2] → DFT_R2 → ω_M^{R1 m3 k2} → C (in place, swizzled)
     double2 u[PL::I2][R2];
@@ -246,7 +250,7 @@ static cudaError_t run_dst4(cnpint_ctx* c, const double* in, double* out, const 
   const int ntiles = (nlines / 2 + PL::P - 1) / PL::P;
   const int grid = ntiles < grid_max ? ntiles : grid_max;
   return cnp_launch(c, kern, dim3(grid), dim3(PL::NT), PL::bytes, in, out, nlines, c->ld, pre, post,
-                    (const double2*)c->d_twx, accumulate, c->debug & 1);
+                    (const double2*)c->d_twx, accumulate, c->debug & 1, c->l2pf);
 }
 
 // x pass (rows) through the lean kernel when nx + 1 ∈ {64, …, 512} and ld = nx + 1; else NotSupported

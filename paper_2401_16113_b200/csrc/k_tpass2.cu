@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
              int ld, int nx, const double* __restrict__ gam, const double* __restrict__ igam,
              const double2* __restrict__ lam1, const double2* __restrict__ lam2, const double2* __restrict__ sk,
              const double2* __restrict__ il2, const double* __restrict__ ex, const double* __restrict__ ey,
-             double tau, double tau_shift, const double2* __restrict__ twN, int debug_sign) {
+             double tau, double tau_shift, const double2* __restrict__ twN, int debug_sign, int l2pf) {
   using PL = T2Plan<LOGN>;
   constexpr int N = PL::N, H = PL::H, TP = PL::TP, P = PL::P, NT = PL::NT, RS = PL::RS;
   constexpr int R1 = PL::R1, R2 = PL::R2, R3 = PL::R3;
@@ -104,6 +104,13 @@ __global__ void __launch_bounds__(T2Plan<LOGN>::NT, T2Plan<LOGN>::MINB)
       dftR<R1, false>(v);
 #pragma unroll
       for (int k1 = 0; k1 < R1; ++k1) A[k1 * (N / R1) + m] = k1 ? cmul(v[k1], twf(m * k1)) : v[0];
+    }
+    // the CTA's next tile (N rows × P pairs = 128 B per row) into L2 while this one computes: its step-1
+    // loads then hit L2 (ncu: 25 % of the stall samples were those loads waiting on HBM)
+    if (l2pf && tile + (int)gridDim.x < ntiles) {
+      const int64_t c2 = 2 * (int64_t)(tile + gridDim.x) * P;
+      const unsigned nb = (unsigned)(2 * (npairs - (tile + (int)gridDim.x) * P < P ? npairs - (tile + (int)gridDim.x) * P : P) * 8);
+      for (int t = tid; t < N; t += NT) prefetch_l2(in + (int64_t)t * W + c2, nb);
     }
     __syncthreads();
     // ---- forward step 2: item (k1, m3): B[k1][m3 + R3 m2] → DFT_R2 → ω_N^{R1 m3 k2}
@@ -262,7 +269,7 @@ static cudaError_t run_tpass2(cnpint_ctx* c, const double* in, double* out, cons
                     (const double*)c->d_gam, (const double*)c->d_igam, (const double2*)c->d_lam1,
                     (const double2*)c->d_lam2, (const double2*)c->d_sk, (const double2*)c->d_il2,
                     (const double*)c->d_ex, (const double*)c->d_ey, c->tau_p, c->tau_p * c->shift,
-                    (const double2*)c->d_tw, c->debug & 1);
+                    (const double2*)c->d_tw, c->debug & 1, c->l2pf);
 }
 
 // 2D time pass through the lean kernel for N ∈ {256, 512, 1024}; else NotSupported.  Debug 262144 keeps the
