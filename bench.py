@@ -332,6 +332,30 @@ def run_gpu(args, rank, world, local):
     total_prof_ms = sum(v[0] for v in prof.values())
     traffic = ncu_traffic(dominant, w.name)
 
+    # ---------------- 2D: the same solves with the time pass as Eq. 3.2's transform (Γ_α·FFT, ÷, iFFT·Γ_α⁻¹ on chip,
+    # debug 524288) instead of the default recurrence form (k_tscan.cu) — both compute the same P_α⁻¹
+    k6_alt = None
+    if w.dim == 2:
+        s.set_debug(524288)
+        s.gmres(b, u, w.tol, w.restart)
+        s.profile_enable(True)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        nalt = max(2, min(5, args.steps))
+        for _ in range(nalt):
+            ralt = s.gmres(b, u, w.tol, w.restart)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        palt = s.profile_read()
+        s.profile_enable(False)
+        s.set_debug(0)
+        k6 = palt.get("K6_time_pass_2d")
+        k6_alt = {"transform_path_ms_per_step": f0.elapsed_time(f1) / nalt, "iterations": ralt["iterations"],
+                  "K6_transform_avg_launch_us": 1e3 * k6[0] / k6[1] if k6 else None,
+                  "K6_default_avg_launch_us": kernels.get("K6_time_pass_2d", {}).get("avg_launch_us"),
+                  "note": "default = recurrence form of the alpha-circulant time block (k_tscan); transform = "
+                          "cnpint_set_debug(524288): FFT along time, divide by lambda1_k - lambda2_k*mu, inverse FFT"}
+
     # ---------------- standalone P⁻¹ applies/s and matvec GB/s
     pinv_s, mv_s = time_ops(s, w, stream, 2 if w.unknowns > 1e8 else 4, max(10, args.steps))
     pinv_d, mv_d = op_rates(w, pinv_s, mv_s, peak)
@@ -377,6 +401,7 @@ def run_gpu(args, rank, world, local):
                      "share_of_step": d_ms / total_prof_ms if total_prof_ms else None,
                      "frac_of_same_run_copy": achieved / copy_best if copy_best else None},
         "kernels": kernels,
+        "time_pass_variants": k6_alt,
         "gpu_launches": launches,
         "e2e": e2e,
         "clocks": clk,

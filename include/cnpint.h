@@ -140,7 +140,11 @@ cnpint_status cnpint_apply_P(cnpint_ctx* ctx, const double* d_z, double* d_v);
  * (Eq. 3.2), solving only k = 0..N/2 (Remark 3.1).
  * v must be real (the conjugate halving relies on it).  1D: K2 (Γ_α-scaled real FFT along t)
  * → K3 (N/2+1 complex tridiagonal solves) → K4 (C2R inverse FFT, Γ_α⁻¹, 1/N).
- * 2D: DST fast diagonalisation in space around a fused time pass. */
+ * 2D: DST fast diagonalisation in space around a fused time pass, which per
+ * spatial mode μ inverts the N×N α-circulant C1^(α) − μC2^(α) — by Eq. 3.2's transform on chip
+ * (Γ_α·FFT, ÷ (λ1_k − λ2_kμ), iFFT·Γ_α⁻¹) or, by default when every mode is stable (μ < 0), as the
+ * equivalent first-order recurrence (1 − μ/2) z_t − (1 + μ/2) z_{t−1} = v_t, z_{−1} = α z_{N−1}, run as a
+ * chunked scan over the time axis (k_tscan.cu; cnpint_set_debug bit 524288 selects the transform). */
 cnpint_status cnpint_apply_Pinv(cnpint_ctx* ctx, const double* d_v, double* d_z);
 
 /* Stage entry points of the 1D P_α⁻¹ (per-kernel parity tests and timing).
@@ -320,7 +324,12 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 131072 = no fusion of the 2D Gram update with the next x sine pass (k_upd_dst4; cnpint_gmres fuses them
  * when the lean x pass applies and the next Arnoldi step is expected to run);
  * 262144 = the first-generation lean time pass (divide by λ1_k − λ2_kμ) instead of the second (k_tpass2
- * GEN 2: ½/λ2_k folded into the forward output, then ÷ (c_k − μ) with c_k = λ1_k/λ2_k from per-mode tables). */
+ * GEN 2: ½/λ2_k folded into the forward output, then ÷ (c_k − μ) with c_k = λ1_k/λ2_k from per-mode tables);
+ * 524288 = the 2D time pass as Eq. 3.2's transform (Γ_α·FFT along time, ÷ (λ1_k − λ2_kμ), iFFT·Γ_α⁻¹ on chip)
+ * instead of the default recurrence form of the same α-circulant solve (k_tscan.cu: per spatial mode
+ * (1 − μ/2) z_t − (1 + μ/2) z_{t−1} = v_t with z_{−1} = α z_{N−1}, a chunked scan over the time axis; used when
+ * every mode has μ < 0 and N is a power of two in [8, 2048]).  Bits 1, 2, 8, 16, 64, 16384 and 262144 — the
+ * transform's negative controls and kernel selections — also keep the transform path. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 
 #ifdef __cplusplus

@@ -367,6 +367,8 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
     }
   }
   if (c->dim == 2) {
+    long double emax[2] = {0.0L, 0.0L};
+    int axis_i = 0;
     auto axis = [&](int n, double s, double d, double u, size_t offi, size_t offd, size_t offe, size_t offtw,
                     int64_t elen) {
       std::vector<double> Di(n), Dd(n), e(elen, 0.0);
@@ -378,7 +380,9 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
         Di[j - 1] = (double)powl(rho, -(long double)j);
         Dd[j - 1] = (double)(powl(rho, (long double)j) * 2.0L / (long double)(n + 1));
         e[j - 1] = (double)((long double)d + 2.0L * sq * cosl(PI * (long double)j / (long double)(n + 1)));
+        if (j == 1 || (long double)e[j - 1] > emax[axis_i]) emax[axis_i] = (long double)e[j - 1];
       }
+      ++axis_i;
       std::vector<double2> t2(2 * (n + 1));
       for (int q = 0; q < 2 * (n + 1); ++q) {
         long double th = PI * (long double)q / (long double)(n + 1);
@@ -389,6 +393,7 @@ void make_tables(cnpint_ctx* c, const cnpint_operator* op, std::vector<char>& im
     };
     axis(c->nx, op->xs, op->xd, op->xu, L.dxi, L.dx, L.ex, L.twx, c->ld);
     axis(c->ny, op->ys, op->yd, op->yu, L.dyi, L.dy, L.ey, L.twy, c->ny);
+    c->mu_max = (double)((long double)c->tau_p * (emax[0] + emax[1] + (long double)c->shift));
   }
 }
 

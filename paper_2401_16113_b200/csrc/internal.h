@@ -104,6 +104,8 @@ struct cnpint_ctx {
   double* d_dy;        // [ny]
   double* d_ex;        // [nx] eigenvalues of L_x
   double* d_ey;        // [ny] eigenvalues of L_y
+  double mu_max;       // 2D: max over the spatial modes of μ' = τ_p(e_x + e_y + shift); < 0 ⇒ the time
+                       // recurrence of every mode is stable (k_tscan.cu)
   double2* d_twx;      // [nx+1] e^{-2πiq/(2(nx+1))}
   double2* d_twy;      // [ny+1]
   // GMRES
@@ -188,6 +190,8 @@ cudaError_t launch_tfft_pass_2d(cnpint_ctx* c, const double* in, double* out, co
 cudaError_t launch_dst_x(cnpint_ctx* c, const double* in, double* out, const double* vscale, int inverse);
 cudaError_t launch_dst_y(cnpint_ctx* c, const double* in, double* out, int inverse);
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
+bool tscan_ok(const cnpint_ctx* c);  // the recurrence form of the 2D time pass applies (k_tscan.cu)
+cudaError_t launch_tscan_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 
 // GMRES helpers
 cudaError_t launch_norm2(cnpint_ctx* c, const double* w, double* part, double* out);  // out = Σ w²

@@ -235,6 +235,12 @@ cudaError_t launch_time_ifft(cnpint_ctx* c, const double2* zhat, double* z, int 
 cudaError_t launch_tpass2(cnpint_ctx* c, const double* in, double* out, const double* vscale);
 
 cudaError_t launch_time_pass_2d(cnpint_ctx* c, const double* in, double* out, const double* vscale) {
+  // the recurrence form (k_tscan.cu: no transform, 3 fp64 instructions per unknown) when every mode is
+  // stable; debug 524288 (or any transform-selecting bit) keeps the transform kernels below
+  if (tscan_ok(c)) {
+    const cudaError_t e = launch_tscan_2d(c, in, out, vscale);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (!(c->debug & 8) && !(c->debug & 16) && fstep_ok(c)) return launch_fstep_pass_2d(c, in, out, vscale);
   // the lean time pass (k_tpass2.cu) at N = 256 and 1024 (c5 n511 N1024 2758 → 1990 µs, N256 577 → 417 µs;
   // at N = 512 it ties k_tpass_r: 225 vs 222 µs, profiles/r02_tpass2_ab.txt); debug 16384 forces it at

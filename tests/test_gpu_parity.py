@@ -326,9 +326,10 @@ def test_dst_paths(name, debug):
 
 @pytest.mark.parametrize("name", ["2d_n63_N2048", "2d_N1024_C2", "2d_n15_N512", "2d_n31_N256", "2d_n7_N256",
                                   "2d_n31_N1024_p1", "2d_n15_N512_p1", "2d_n15_N2048_p1"])
-@pytest.mark.parametrize("debug", [0, 16, 64, 16384, 262144, 16384 | 262144])
+@pytest.mark.parametrize("debug", [0, 524288, 16, 64, 16384, 262144, 16384 | 262144])
 def test_timepass_2d_paths(name, debug):
-    """2D time pass: the three-phase four-step kernel (N >= 2048), the lean register kernel k_tpass2
+    """2D time pass: the recurrence form k_tscan (debug 0: every mode is stable here) and, behind debug
+    524288, the transform kernels — the three-phase four-step kernel (N >= 2048), the lean register kernel k_tpass2
     (N = 256, 1024; forced at 512 by debug 16384; its first generation by debug 262144), the register
     kernel k_tpass_r (N = 512) — defaults (debug 0) — and the cluster kernel (debug 64; debug 16 at
     N >= 2048) all give the oracle's P⁻¹, also on a ragged last tile and for P₁ (α = 1: λ1_0 = 0, so a
@@ -346,6 +347,70 @@ def test_timepass_2d_paths(name, debug):
         if s.ld > w.n:
             assert float(z[..., w.n:].abs().max()) == 0.0
     assert s.device_status() == 0
+
+
+@pytest.mark.parametrize("N", [8, 16, 32, 64, 128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("alpha", [0.01, 1.0])
+def test_timepass_2d_recurrence_sizes(N, alpha):
+    """k_tscan at every supported N = CS·NW·L (L = 1 … 16 rows per thread, cluster sizes 1 … 8), with a
+    ragged last 64-column tile (n = 15: ld·ny/2 = 120 pairs) and a padding column, for P_α and P₁: the
+    oracle's P⁻¹ (steps (a)-(c) by FFT) at 1e-12, equal to the transform kernels (debug 524288) to 1e-12."""
+    w = synth.scaled(synth.C4, 15, N, alpha=alpha)
+    s = solver_for(w)
+    op = problem.build_operator(w)
+    v = synth.random_vectors(w, 1, 71 + N)[0]
+    z = s.empty()
+    s.apply_Pinv(s.to_device(v), z)
+    zg = s.to_host(z)
+    assert float(z[..., w.n:].abs().max()) == 0.0
+    fwd = rel(zg, precond.pinv_dft(w, op, v))
+    record(f"pinv_tscan_n15_N{N}_a{alpha}", forward=fwd)
+    assert fwd < 1e-12, (N, alpha, fwd)
+    assert rel(aao.apply_P(w, op, zg), v) < 1e-12
+    s.set_debug(524288)
+    z2 = s.empty()
+    s.apply_Pinv(s.to_device(v), z2)
+    assert rel(zg, s.to_host(z2)) < 1e-12
+    assert s.device_status() == 0
+
+
+@pytest.mark.parametrize("cfg", ["4,8", "8,8", "4,16", "8,16", "16,16", "16,8"])
+def test_timepass_2d_recurrence_configs(cfg, monkeypatch):
+    """The other chunk shapes of k_tscan (CNPINT_TSCAN_CFG = rows per thread, warps per CTA) at N = 512
+    and 1024: same result as the default shape to 1e-13 and the oracle's to 1e-12."""
+    for N in (512, 1024):
+        L, NW = (int(t) for t in cfg.split(","))
+        if N // (L * NW) > 8:
+            continue
+        w = synth.scaled(synth.C4, 15, N, alpha=0.01)
+        s = solver_for(w)
+        op = problem.build_operator(w)
+        v = synth.random_vectors(w, 1, 73)[0]
+        z0, z1 = s.empty(), s.empty()
+        s.apply_Pinv(s.to_device(v), z0)
+        monkeypatch.setenv("CNPINT_TSCAN_CFG", cfg)
+        s.apply_Pinv(s.to_device(v), z1)
+        monkeypatch.delenv("CNPINT_TSCAN_CFG")
+        assert rel(s.to_host(z1), s.to_host(z0)) < 1e-13, (cfg, N)
+        assert rel(s.to_host(z1), precond.pinv_dft(w, op, v)) < 1e-12, (cfg, N)
+
+
+def test_timepass_2d_unstable_mode_keeps_transform():
+    """A spatial mode with μ' = τ(e_x + e_y + shift) ≥ 0 (here a positive reaction term) makes the forward
+    recurrence unstable (|ρ| ≥ 1): the handle keeps the transform kernels, and P⁻¹ still matches the oracle."""
+    from oracle.problem import Operator2D
+    n, N = 15, 64
+    kw = dict(xs=1.0, xd=-2.0, xu=1.0, ys=0.8, yd=-1.7, yu=0.9, shift=3.9)
+    spec = OperatorSpec(dim=2, nx=n, ny=n, **kw)
+    w = synth.scaled(synth.C4, n, N, alpha=0.1)
+    op = Operator2D(n=n, x=np.arange(1, n + 1) / (n + 1.0), h=1.0 / (n + 1), **kw)
+    s = Solver(N, w.T, w.alpha, spec)
+    v = np.random.default_rng(5).standard_normal((N, n, n))
+    z = s.empty()
+    s.apply_Pinv(s.to_device(v), z)
+    zg = s.to_host(z)
+    assert rel(zg, precond.pinv_dft(w, op, v)) < 1e-12
+    assert rel(aao.apply_P(w, op, zg), v) < 1e-12
 
 
 @pytest.mark.parametrize("debug", [1, 2])

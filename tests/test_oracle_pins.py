@@ -93,6 +93,37 @@ def test_lambda_closed_form_and_set(N, alpha):
     np.testing.assert_allclose(l1[1:], np.conj(l1[1:][::-1]), atol=1e-13)   # conjugate pairs
 
 
+@pytest.mark.parametrize("N,alpha", [(5, 0.3), (16, 0.01), (64, 1.0)])
+def test_alpha_circulant_time_block_is_a_first_order_recurrence(N, alpha):
+    """The identity the CUDA path's 2D time pass uses (k_tscan.cu): for a spatial mode μ the time block
+    C1^(α) − μC2^(α) (dense) is (1 − μ/2)I − (1 + μ/2)S_α, so its inverse is the recurrence
+    z_t = ρ z_{t−1} + c v_t with z_{−1} = α z_{N−1}, whose closure is z_{N−1} = G/(1 − αρ^N) — here written
+    as a plain loop and held against the dense solve and against the oracle's transform steps (a)-(c)."""
+    rng = np.random.default_rng(N)
+    for mu in (-1e-3, -0.37, -5.0, -400.0):
+        T = aao.C1(N, alpha) - mu * aao.C2(N, alpha)
+        S = np.eye(N, k=-1)
+        S[0, N - 1] = alpha
+        assert np.abs(T - ((1 - mu / 2) * np.eye(N) - (1 + mu / 2) * S)).max() < 1e-15 * (1 + abs(mu))
+        v = rng.standard_normal(N)
+        rho, c = (1 + mu / 2) / (1 - mu / 2), 1 / (1 - mu / 2)
+        s = np.zeros(N)
+        acc = 0.0
+        for t in range(N):                      # scan from a zero state
+            acc = rho * acc + c * v[t]
+            s[t] = acc
+        zl = s[N - 1] / (1 - alpha * rho**N)     # cyclic closure
+        z = s + rho ** np.arange(1, N + 1) * alpha * zl
+        assert rel(z, np.linalg.solve(T, v)) < 1e-12
+        # the oracle's diagonalisation of the same block: Γ_α, DFT, ÷ (λ1_k − λ2_k μ), inverse, Γ_α⁻¹
+        l1, l2 = precond.lambdas(N, alpha)
+        g = precond.gamma(N, alpha)
+        F = precond.fourier_matrix(N)
+        zt = (F.conj().T @ ((F @ (g * v)) / (l1 - l2 * mu))) / g
+        assert np.abs(zt.imag).max() < 1e-12 * np.abs(zt).max()
+        assert rel(z, zt.real) < 1e-12
+
+
 @pytest.mark.parametrize("N,alpha", [(5, 0.3), (8, 0.1)])
 def test_lambda_diagonalises_alpha_circulant(N, alpha):
     """C_ℓ = V_α D_ℓ V_α⁻¹ with V_α = Λ_α⁻¹𝔽* (PAPER.md:270-276), checked against the dense
