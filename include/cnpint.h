@@ -328,7 +328,10 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 524288 = the 2D time pass as Eq. 3.2's transform (Γ_α·FFT along time, ÷ (λ1_k − λ2_kμ), iFFT·Γ_α⁻¹ on chip)
  * instead of the default recurrence form of the same α-circulant solve (k_tscan.cu: per spatial mode
  * (1 − μ/2) z_t − (1 + μ/2) z_{t−1} = v_t with z_{−1} = α z_{N−1}, a chunked scan over the time axis; used when
- * every mode has μ < 0 and N is a power of two in [8, 2048]).  Bits 1, 2, 8, 16, 64, 16384 and 262144 — the
+ * every mode has μ < 0 and N is a power of two in [8, 2048]);
+ * 1048576 = the register 2D matvec (k_matvec2d: own row and both y neighbours loaded into registers, four
+ * time rows per batch) instead of the staged one (k_matvec2d_s: rows of u through a cp.async shared-memory
+ * ring, eight time rows in flight per warp); the same arithmetic per element.  Bits 1, 2, 8, 16, 64, 16384 and 262144 — the
  * transform's negative controls and kernel selections — also keep the transform path. */
 cnpint_status cnpint_set_debug(cnpint_ctx* ctx, int flags);
 

@@ -89,6 +89,26 @@ static int mv_tchunk(const cnpint_ctx* c) {
   return v ? v : (c->N >= 4096 ? 32 : 16);
 }
 
+// rows of the time chunk a 2D block walks (CNPINT_MV2_TCHUNK: tuning override)
+static bool mv2d_staged(const cnpint_ctx* c, int ns);
+// ns = vectors read beside u (b of the residual modes, the Ṽ_i of the fused dots).  The staged kernel takes
+// longer chunks (its ring fills and drains once per block): 64 rows alone, 128 with side vectors (one or two
+// CTAs per SM), halved while the grid would have fewer than four waves of resident blocks.
+static int mv2_tchunk(const cnpint_ctx* c, int ns) {
+  static const int v = [] {
+    const char* e = getenv("CNPINT_MV2_TCHUNK");
+    const int t = e ? atoi(e) : 0;
+    return (t == 8 || t == 16 || t == 32 || t == 64 || t == 128) ? t : 0;
+  }();
+  if (v) return v;
+  if (!mv2d_staged(c, ns)) return 16;
+  int t = ns == 0 ? 64 : 128;
+  const int64_t tiles = ((c->ld + 63) / 64) * (int64_t)((c->ny + 7) / 8);
+  const int64_t want = 4LL * c->num_sms * (ns == 0 ? 3 : ns == 1 ? 2 : 1);
+  while (t > 16 && tiles * ((c->N + t - 1) / t) < want) t /= 2;
+  return t;
+}
+
 // ------------------------------------------------------------------------------- K1 1D
 // MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  MODE 3: as 2 without storing y (norm
 // only).  NORM: per-block Σ y².
@@ -245,7 +265,10 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   }
   double acc = 0.0;
   // rows in batches whose loads are all issued before use (see k_matvec1d)
-  constexpr int TB = NVD <= 1 ? 4 : NVD <= 3 ? 2 : 1;
+#ifndef MV2D_TB0
+#define MV2D_TB0 4
+#endif
+  constexpr int TB = NVD == 0 ? MV2D_TB0 : NVD <= 1 ? 4 : NVD <= 3 ? 2 : 1;
   for (int tb = t0; tb < t1; tb += TB) {
     double2 cvb[TB], cdb[TB], cub[TB], bvb[TB], vvb[TB][NVD > 0 ? NVD : 1];
     double clb[TB], crb[TB];
@@ -310,6 +333,178 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   }
 }
 
+
+// ------------------------------------------------------------------------------- K1 2D, staged (round 2)
+// The same block tile (64 columns × 8 rows, one warp per y row, a chunk of time rows), but every vector
+// arrives through a shared-memory ring filled by cp.async: MVS_NG groups of MVS_G time rows; a slot holds
+// the 10 × 66 patch of u (rows y0−1 … y0+8, columns x0−1 … x0+64) of one time row and the 8 × 64 tile of
+// each of the NS vectors read alongside it (b for the residual modes, the Ṽ_i of the fused dots).  A thread
+// keeps no load in registers, so two groups (8 time rows of every stream) stay in flight per CTA while a
+// third is computed — k_matvec2d holds one batch of ≤ 4 rows in registers (own row and both y neighbours)
+// and waits for it (a plain 𝓜u ran at 0.67 of HBM, latency-bound; this one 0.80-0.82).  The y neighbours
+// come from the ring instead of L1 re-reads; one CTA barrier per group.  Positions outside the domain
+// are never written and stay 0.  NS ≤ 3 (65 / 114 / 164 / 213 KB of ring: 3 / 2 / 1 / 1 CTAs per SM);
+// more dot vectors go through k_matvec2d.
+constexpr int MVS_G = 4, MVS_NG = 3, MVS_ROWS = 10, MVS_RW = 68;  // row: [1] = x0−1, [2..65] = the tile, [66] = x0+64
+constexpr int MVS_MAXNVD = 3;
+constexpr int mvs_slot(int ns) { return MVS_ROWS * MVS_RW + ns * 512; }  // doubles per slot
+constexpr size_t mvs_bytes(int ns) { return (size_t)MVS_G * MVS_NG * mvs_slot(ns) * sizeof(double); }
+
+template <int MODE, bool NORM, int NVD = 0>
+__global__ void __launch_bounds__(256, (NVD + (MODE >= 2)) == 0 ? 3 : (NVD + (MODE >= 2)) == 1 ? 2 : 1)
+    k_matvec2d_s(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ b, int N, int nx,
+                 int ny, int64_t ld, double htau, double alpha, double cxs, double cxu, double cys, double cyu,
+                 double cdiag, int tchunk, double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                 DotPtrs vd = DotPtrs{}, const double* __restrict__ dt = nullptr, PostOp post = PostOp{}) {
+  constexpr int NS = NVD + (MODE >= 2 ? 1 : 0), SLOT = mvs_slot(NS);
+  static_assert(MODE < 2 || NVD == 0, "the residual modes carry no fused dots");
+  extern __shared__ __align__(16) double mvs_ring[];
+  const int lane = threadIdx.x, wy = threadIdx.y;
+  for (int i = wy * 32 + lane; i < MVS_G * MVS_NG * SLOT; i += 256) mvs_ring[i] = 0.0;
+  __syncthreads();
+  pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
+  double dacc[NVD > 0 ? NVD : 1];
+#pragma unroll
+  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
+  const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
+  const int yrow = blockIdx.y * 8 + wy;
+  const int t0 = ((MODE >= 2 && MV_REVERSE) ? (int)(gridDim.z - 1 - blockIdx.z) : (int)blockIdx.z) * tchunk;
+  const int t1 = min(N, t0 + tchunk);
+  const bool act = x0 < ld && yrow < ny;
+  const bool hasL = act && lane == 0 && x0 > 0;
+  const bool hasR = act && lane == 31 && x0 + 2 < ld;
+  const bool hasD = act && yrow > 0;
+  const bool hasU = act && yrow + 1 < ny;
+  const int64_t slice = (int64_t)ny * ld;
+  const int64_t off = (int64_t)yrow * ld + x0;
+  double* const mine = mvs_ring + (wy + 1) * MVS_RW + 2 + 2 * lane;         // this thread's pair of u in slot 0
+  double* const minev = mvs_ring + MVS_ROWS * MVS_RW + wy * 64 + 2 * lane;  // … of the first side vector
+
+  auto issue_group = [&](int g) {
+#pragma unroll
+    for (int q = 0; q < MVS_G; ++q) {
+      const int t = t0 + g * MVS_G + q;
+      if (t < t1) {
+        const int so = ((g % MVS_NG) * MVS_G + q) * SLOT;
+        double* const d = mine + so;
+        const int64_t go = (int64_t)t * slice + off;
+        const double* const r = u + go;
+        if (act) cp_async16(d, r);
+        if (hasL) cp_async8(d - 1, r - 1);
+        if (hasR) cp_async8(d + 2, r + 2);
+        if (wy == 0 && hasD) cp_async16(d - MVS_RW, r - ld);
+        if (wy == 7 && hasU) cp_async16(d + MVS_RW, r + ld);
+        if (act) {
+          if (MODE >= 2) cp_async16(minev + so, b + go);
+#pragma unroll
+          for (int i = 0; i < NVD; ++i) cp_async16(minev + so + i * 512, vd.p[i] + go);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  const int ngroups = (t1 - t0 + MVS_G - 1) / MVS_G;
+#pragma unroll
+  for (int g = 0; g < MVS_NG - 1; ++g) issue_group(g);  // rows past t1 issue nothing; the group is still committed
+
+  auto ld2 = [&](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
+  double2 pv = make_double2(0, 0), pd = pv, pu = pv;
+  double pl = 0, pr = 0;
+  if (t0 > 0 || MODE == 1) {
+    const double sc = (t0 > 0) ? 1.0 : alpha;
+    const double* r = u + (int64_t)((t0 > 0) ? t0 - 1 : N - 1) * slice + off;
+    if (act) pv = ld2(r);
+    if (hasD) pd = ld2(r - ld);
+    if (hasU) pu = ld2(r + ld);
+    if (hasL) pl = r[-1];
+    if (hasR) pr = r[2];
+    pv.x *= sc; pv.y *= sc; pd.x *= sc; pd.y *= sc; pu.x *= sc; pu.y *= sc; pl *= sc; pr *= sc;
+  }
+  double acc = 0.0;
+  for (int g = 0; g < ngroups; ++g) {
+    cp_async_wait<MVS_NG - 2>();  // this thread's copies of group g have landed
+    __syncthreads();              // … everyone's; and group g − 1 is computed: its slots are free
+    issue_group(g + MVS_NG - 1);
+    const int go = (g % MVS_NG) * MVS_G * SLOT;
+#pragma unroll
+    for (int q = 0; q < MVS_G; ++q) {
+      const int t = t0 + g * MVS_G + q;
+      if (t >= t1) break;
+      const double* const d = mine + go + q * SLOT;
+      const double2 cv = *reinterpret_cast<const double2*>(d);
+      const double2 cd = *reinterpret_cast<const double2*>(d - MVS_RW);
+      const double2 cu = *reinterpret_cast<const double2*>(d + MVS_RW);
+      const double cl = lane == 0 ? d[-1] : 0.0, cr = lane == 31 ? d[2] : 0.0;
+      const double2 s = make_double2(cv.x + pv.x, cv.y + pv.y);
+      const double2 sd = make_double2(cd.x + pd.x, cd.y + pd.y);  // row y−1
+      const double2 su = make_double2(cu.x + pu.x, cu.y + pu.y);  // row y+1
+      double sl = __shfl_up_sync(0xffffffffu, s.y, 1);
+      double sr = __shfl_down_sync(0xffffffffu, s.x, 1);
+      if (lane == 0) sl = cl + pl;
+      if (lane == 31) sr = cr + pr;
+      const double ht = dt ? htau * dt[t] : htau;  // row t of D̃B2 (Eq. 5.8)
+      double y0 = (cv.x - pv.x) - ht * (cxs * sl + cxu * s.y + cys * sd.x + cyu * su.x + cdiag * s.x);
+      double y1 = (cv.y - pv.y) - ht * (cxs * s.x + cxu * sr + cys * sd.y + cyu * su.y + cdiag * s.y);
+      if (x0 >= nx) y0 = 0.0;
+      if (x0 + 1 >= nx) y1 = 0.0;
+      if (act) {
+        const double* const dv = minev + go + q * SLOT;
+        if (MODE >= 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(dv);
+          y0 = bv.x - y0;
+          y1 = bv.y - y1;
+        }
+        if (MODE != 3) stg_cs2(reinterpret_cast<double2*>(y + (int64_t)t * slice + off), make_double2(y0, y1));
+        if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
+#pragma unroll
+          for (int i = 0; i < NVD; ++i) {
+            const double2 vv = *reinterpret_cast<const double2*>(dv + i * 512);
+            dacc[i] = fma(vv.x, y0, fma(vv.y, y1, dacc[i]));
+          }
+        }
+        if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
+      }
+      pv = cv; pd = cd; pu = cu; pl = cl; pr = cr;
+    }
+  }
+  cp_async_wait<0>();
+  if (NORM) block_partial<256>(acc, part, out, counter, post);
+  if constexpr (NVD > 0) {
+    block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
+    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+  }
+}
+
+// 2D launch: the staged kernel by default (≤ MVS_MAXNVD dot vectors), k_matvec2d behind
+// cnpint_set_debug(1048576) (A/B, parity) and for more dot vectors
+// (CNPINT_MVS_MAXNS: the largest number of side vectors that still takes the staged kernel; A/B)
+static bool mv2d_staged(const cnpint_ctx* c, int ns) {
+  static const int maxns = [] {
+    const char* e = getenv("CNPINT_MVS_MAXNS");
+    return e ? atoi(e) : 0;
+  }();
+  return !(c->debug & 1048576) && ns <= maxns && ns <= MVS_MAXNVD;
+}
+
+template <int MODE, bool NORM, int NVD, typename... Args>
+static cudaError_t launch_mv2d(cnpint_ctx* c, dim3 grid, Args... args) {
+  dim3 block(32, 8);
+  if constexpr (NVD <= MVS_MAXNVD) {
+    if (mv2d_staged(c, NVD + (MODE >= 2 ? 1 : 0))) {
+      constexpr size_t bytes = mvs_bytes(NVD + (MODE >= 2 ? 1 : 0));
+      auto kern = k_matvec2d_s<MODE, NORM, NVD>;
+      int done = 0;
+      cudaError_t ce = cnp_dev_cached((const void*)kern, &done, [&](int* v) {
+        *v = 1;
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      });
+      if (ce != cudaSuccess) return ce;
+      return cnp_launch(c, kern, grid, block, bytes, args...);
+    }
+  }
+  return cnp_launch(c, k_matvec2d<MODE, NORM, NVD>, grid, block, 0, args...);
+}
+
 // ----------------------------------------------------------------------------------- launcher
 template <int MODE, bool NORM>
 static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const double* b, double* part,
@@ -328,12 +523,11 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
                                      c->N, c->ld, htau, c->alpha, tchunk, part, out, c->d_counter, DotPtrs{}, dt, post);
     if (e != cudaSuccess) return e;
   } else {
-    const int tchunk = 16;
-    dim3 block(32, 8);
+    const int tchunk = mv2_tchunk(c, MODE >= 2 ? 1 : 0);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    const cudaError_t e = cnp_launch(c, k_matvec2d<MODE, NORM>, grid, block, 0, u, y, b, c->N, c->nx, c->ny, c->ld,
-                                     htau, c->alpha, c->xs, c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
-                                     part, out, c->d_counter, DotPtrs{}, dt, post);
+    const cudaError_t e = launch_mv2d<MODE, NORM, 0>(c, grid, u, y, b, c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs,
+                                                     c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk, part, out,
+                                                     c->d_counter, DotPtrs{}, dt, post);
     if (e != cudaSuccess) return e;
   }
   cnp_prof_end(c, KID_MATVEC, (MODE == 2 ? 24.0 : 16.0) * cnp_units(c));  // mode 3: 2 reads
@@ -354,13 +548,12 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
                                      c->d_counter, vd, c->d_dt, PostOp{});
     if (e != cudaSuccess) return e;
   } else {
-    const int tchunk = 16;
-    dim3 block(32, 8);
+    const int tchunk = mv2_tchunk(c, NVD);
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    const cudaError_t e = cnp_launch(c, k_matvec2d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr,
-                                     c->N, c->nx, c->ny, c->ld, htau, c->alpha, c->xs, c->xu, c->ys, c->yu,
-                                     c->xd + c->yd + c->shift, tchunk, part, out, c->d_counter, vd, c->d_dt,
-                                     PostOp{});
+    const cudaError_t e = launch_mv2d<0, false, NVD>(c, grid, u, y, (const double*)nullptr, c->N, c->nx, c->ny, c->ld,
+                                                     htau, c->alpha, c->xs, c->xu, c->ys, c->yu,
+                                                     c->xd + c->yd + c->shift, tchunk, part, out, c->d_counter, vd,
+                                                     (const double*)c->d_dt, PostOp{});
     if (e != cudaSuccess) return e;
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
@@ -389,7 +582,7 @@ int matvec_partial_blocks(const cnpint_ctx* c) {
     const int tchunk = mv_tchunk(c);
     return (int)(((c->ld / 2 + 127) / 128) * ((c->N + tchunk - 1) / tchunk));
   }
-  return (int)(((c->ld + 63) / 64) * ((c->ny + 7) / 8) * ((c->N + 15) / 16));
+  return (int)(((c->ld + 63) / 64) * ((c->ny + 7) / 8) * ((c->N + 7) / 8));  // the smallest 2D time chunk
 }
 
 cudaError_t launch_matvec(cnpint_ctx* c, const double* u, double* y, int mode, const double* b, double* part,

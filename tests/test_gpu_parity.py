@@ -110,6 +110,35 @@ def test_apply_A_and_P(name):
         assert float(y[..., w.n:].abs().max()) == 0.0 if s.ld > w.n else True
 
 
+@pytest.mark.parametrize("n,N", [(127, 64), (15, 8), (255, 16), (31, 128), (63, 32)])
+def test_matvec2d_staged_equals_register_kernel(n, N):
+    """K1 2D: the default kernel (rows of u staged through a cp.async shared-memory ring, k_matvec2d_s)
+    and the register kernel (debug 1048576) do the same arithmetic per element: 𝓜u, P_αu and b − 𝓜u
+    bitwise equal; the fused dots / norms (different block partitions of the same sums) to 1e-14 — over
+    several x and y blocks with ragged last blocks, one and several time chunks."""
+    w = synth.scaled(synth.C4, n, N, alpha=0.05)
+    s = solver_for(w, restart_max=10)
+    op = problem.build_operator(w)
+    vh = synth.random_vectors(w, 1, 5)[0]
+    v = s.to_device(vh)
+    b = problems.rhs(w, s)
+    outs = {}
+    for dbg in (0, 1048576):
+        s.set_debug(dbg)
+        y, p, u = s.empty(), s.empty(), s.empty()
+        s.apply_A(v, y)
+        s.apply_P(v, p)
+        rep = s.gmres(b, u, 1e-10, 10)
+        outs[dbg] = (y, p, u, rep)
+    s.set_debug(0)
+    assert torch.equal(outs[0][0], outs[1048576][0]) and torch.equal(outs[0][1], outs[1048576][1])
+    assert rel(s.to_host(outs[0][0]), aao.apply_M(w, op, vh)) < 1e-12
+    assert outs[0][3]["iterations"] == outs[1048576][3]["iterations"]
+    assert rel(s.to_host(outs[0][2]), s.to_host(outs[1048576][2])) < 1e-13
+    h0, h1 = np.array(outs[0][3]["history"]), np.array(outs[1048576][3]["history"])
+    assert np.all(np.abs(h0 - h1) <= 1e-12 * np.abs(h1) + 1e-16), (h0, h1)
+
+
 # ------------------------------------------------------------------------------ P_α⁻¹
 @pytest.mark.parametrize("name", list(SMALL))
 def test_pinv_small(name):
