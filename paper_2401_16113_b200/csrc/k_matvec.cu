@@ -101,10 +101,13 @@ static int mv2_tchunk(const cnpint_ctx* c, int ns) {
     return (t == 8 || t == 16 || t == 32 || t == 64 || t == 128) ? t : 0;
   }();
   if (v) return v;
-  if (!mv2d_staged(c, ns)) return 16;
-  int t = ns == 0 ? 64 : 128;
+  // the register kernel (two CTAs per SM) also gains from long chunks — the rows of t0 − 1 are a dependent
+  // round trip before the first batch: 16 → 64 rows, K1 class of a c5 n511 N1024 solve 1557 → 1410 µs
+  // (profiles/r02_mvs_ab.txt)
+  const bool st = mv2d_staged(c, ns);
+  int t = (!st || ns == 0) ? 64 : 128;
   const int64_t tiles = ((c->ld + 63) / 64) * (int64_t)((c->ny + 7) / 8);
-  const int64_t want = 4LL * c->num_sms * (ns == 0 ? 3 : ns == 1 ? 2 : 1);
+  const int64_t want = 4LL * c->num_sms * (!st ? 2 : ns == 0 ? 3 : ns == 1 ? 2 : 1);
   while (t > 16 && tiles * ((c->N + t - 1) / t) < want) t /= 2;
   return t;
 }
