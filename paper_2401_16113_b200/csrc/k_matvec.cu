@@ -4,8 +4,9 @@
 // −(I + ½Ã) below it, Ã = τ L_h.  Row t:  y_t = Q1 u_t − Q2 u_{t−1} = (u_t − u_{t−1}) − ½τ L_h (u_t + u_{t−1}),
 // u_{−1} = 0.  PAPER.md:344-350: P_α adds −αQ2 u_{N−1} to row 0, i.e. the same formula with
 // u_{−1} := α u_{N−1}.  One HBM pass: each thread walks a chunk of time rows keeping u_{t−1} in
-// registers; x-neighbours come from warp shuffles, y-neighbours (2D) from a shared-memory row
-// exchange.  16 B/unknown of compulsory traffic (read u, write y).
+// registers; x-neighbours come from warp shuffles, y-neighbours (2D) from L1 re-reads (register kernel,
+// k_matvec2d: the launches with side vectors) or from the cp.async shared-memory ring of the staged
+// kernel (k_matvec2d_s: the plain 𝓜u / P_αu).  16 B/unknown of compulsory traffic (read u, write y).
 #include "common.cuh"
 #include "internal.h"
 #include "post_op.cuh"
@@ -220,9 +221,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
 }
 
 // ------------------------------------------------------------------------------- K1 2D
-// Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread walks a
-// chunk of t.  y-neighbours of s = u_t + u_{t-1} are exchanged through a double-buffered shared
-// row array; the edge warps also carry the halo rows y0-1 and y0+8.
+// Register kernel.  Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread
+// walks a chunk of t in batches of TB rows whose loads (own row, rows y−1 and y+1 through L1, side
+// vectors) are all issued before the first is used.
 template <int MODE, bool NORM, int NVD = 0>
 __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
