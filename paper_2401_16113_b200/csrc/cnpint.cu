@@ -804,6 +804,11 @@ static PostOp post_finalize(const cnpint_ctx* c, int j) {
   p.hmap = c->d_hmap; p.status = c->d_status;
   return p;
 }
+static PostOp post_gram_probe(const cnpint_ctx* c, int j) {  // op 5: see gram_probe_dev (post_op.cuh)
+  PostOp p = post_finalize(c, j);
+  p.op = 5; p.G = c->d_G; p.c2w = c->d_c2;
+  return p;
+}
 static PostOp post_gram_finalize(const cnpint_ctx* c, int j) {
   PostOp p = post_finalize(c, j);
   p.op = 4; p.cg = c->d_cg; p.G = c->d_G; p.c2w = c->d_c2;
@@ -873,6 +878,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
   while (true) {
     int jdone = 0;
     bool stop_inner = false;
+    bool last_skipped = false;  // the cycle's last step took its norm from the Gram matrix: no Ṽ_{jdone} written
     for (int j = 0; j < restart && !stop_inner; ++j) {
       // z_j = P_α⁻¹ v_j  (v_j = s_j Ṽ_j; the scale is folded into the Γ-scaling), kept for the update
       cnpint_status st = pinv_dev(c, V[j], c->d_scl + j, Z[j], 0);
@@ -885,15 +891,34 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
         // c2 = Ṽᵀ(w − Ṽs²c1) = c1 − G̃s²c1 from the stored Gram matrix and which also reduces ‖w‖²
         // and the Gram row Ṽᵀw of the new vector (post op 4 stores it, then the Arnoldi finalize)
         // — the same two projections as classic CGS2, one reading pass fewer
+        const double est_next = est_before > 0.0 ? est_now * std::min(1.0, est_now / est_before) : est_now;
+        // A step expected to be the last (2D): its new basis vector would never be used, only its norm
+        // h_{j+1,j} — which the Gram matrix gives without a pass over the vectors (post op 5, run by the
+        // matvec's folding block: β² = ww − 2aᵀc1 + aᵀG̃a, trusted when β² ≥ 1e-8·ww).  If the estimate
+        // then meets the tolerance, the update pass is skipped; otherwise the probe is taken back and the
+        // step runs as usual.  debug 2097152 turns the probe off, 4194304 probes every step (tests: the
+        // take-back path).
+        if (c->dim == 2 && !(c->debug & 2097152) && est_before > 0.0 && (est_next <= tol || (c->debug & 4194304))) {
+          c->post = post_gram_probe(c, j);
+          CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1, 1));
+          CK(cudaStreamSynchronize(c->stream));
+          if (h[6] != 0.0 && h[1] <= tol && h[3] == 0.0 && h[5] == 0.0 && h[8] == 0.0) {
+            last_skipped = true;
+          } else {
+            if (h[6] != 0.0) CK(launch_small(c, 3, j, 0));
+            c->post = post_gram_finalize(c, j);
+            CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));
+          }
+        } else {
         CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1));
         c->post = post_gram_finalize(c, j);
-        const double est_next = est_before > 0.0 ? est_now * std::min(1.0, est_now / est_before) : est_now;
         if (upd_dst_ok(c) && j + 1 < restart && its + 1 < maxit && est_next > tol) {
           // 2D: the update also writes the x sine pass of Ṽ_{j+1} (the first pass of the next P⁻¹)
           CK(launch_cgs2_pass_dst(c, V.data(), nv, c->d_c1, w, c->d_part, c->d_cg, c->d_tmp1));
           c->xdst_src = w;
         } else {
           CK(launch_cgs2_pass(c, V.data(), nv, c->d_c1, c->d_c2, w, c->d_part, c->d_cg, 2));
+        }
         }
       } else {
         if (nv <= CNP_MAX_DOT) {
@@ -953,7 +978,7 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
       }
     }
     c->last_v0 = V[0];     // cnpint_krylov_basis (test hook): this cycle's basis
-    c->last_nv = jdone + 1;
+    c->last_nv = last_skipped ? jdone : jdone + 1;
     // true residual ‖b − 𝓜u‖: when the estimate says converged only its norm is needed (mode 3, no
     // store); otherwise r is written into the workspace slot of Ṽ_0 for the next cycle (b is kept)
     V[0] = c->d_V;

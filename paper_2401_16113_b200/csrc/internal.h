@@ -161,7 +161,7 @@ cudaError_t launch_tpass_2d(cnpint_ctx* c, const double* in, double* out, const 
 cudaError_t launch_fstep_fwd(cnpint_ctx* c, const double* v, const double* vscale, double2* what);
 cudaError_t launch_fstep_inv(cnpint_ctx* c, const double2* zhat, double* z, int accumulate);
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
-                               double* out);
+                               double* out, int ww = 0);
 // host-layout repack for the *_host entry points: dir 0 packed → padded, 1 padded → packed
 cudaError_t launch_repack(cnpint_ctx* c, const double* src, double* dst, int dir);
 

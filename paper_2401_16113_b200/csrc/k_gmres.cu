@@ -402,7 +402,16 @@ cudaError_t launch_scal_to_host(cnpint_ctx* c) {
   return cudaGetLastError();
 }
 
-// op 0: cycle_start(first = arg); op 1: arnoldi_finalize(j); op 2: backsolve(k = j)
+// takes back the derived-norm probe's finalize of column j (post op 5): g[j] as it was before
+__global__ void k_probe_undo(int j, double* g, double* scal) {
+  if (threadIdx.x == 0) {
+    g[j] = scal[13];
+    g[j + 1] = 0.0;
+    scal[6] = 0.0;
+  }
+}
+
+// op 0: cycle_start(first = arg); op 1: arnoldi_finalize(j); op 2: backsolve(k = j); op 3: undo the probe of column j
 cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg) {
   const int ldh = c->restart_max + 1;
   cnp_prof_begin(c, KID_SMALL);
@@ -410,6 +419,7 @@ cudaError_t launch_small(cnpint_ctx* c, int op, int j, int arg) {
   else if (op == 1)
     k_arnoldi_finalize<<<1, 32, 0, c->stream>>>(j, ldh, c->d_c1, c->d_c2, c->d_scl, c->d_H, c->d_cs, c->d_sn, c->d_g,
                                                 c->d_scal);
+  else if (op == 3) k_probe_undo<<<1, 32, 0, c->stream>>>(j, c->d_g, c->d_scal);
   else k_backsolve<<<1, 32, 0, c->stream>>>(j, ldh, c->d_H, c->d_g, c->d_scl, c->d_y, c->d_coef);
   cnp_prof_end(c, KID_SMALL, 0.0);
   return cudaGetLastError();

@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
 // Register kernel.  Block: 32 lanes along x (2 columns each = 64 columns) x 8 warps along y.  Each thread
 // walks a chunk of t in batches of TB rows whose loads (own row, rows y−1 and y+1 through L1, side
 // vectors) are all issued before the first is used.
-template <int MODE, bool NORM, int NVD = 0>
+// WW (with NVD > 0): also ww = yᵀy as column NVD of the folded dots, and the pending post-fold step
+// (the derived-norm probe of cnpint_gmres, post op 5) run by the folding block.
+template <int MODE, bool NORM, int NVD = 0, bool WW = false>
 __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, int N, int nx, int ny, int64_t ld,
                                                   double htau, double alpha, double cxs, double cxu, double cys,
@@ -236,9 +238,9 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   // Warp wy of the block owns y row ybase + wy; its y−1 / y+1 neighbours are read straight from
   // global memory through L1 (the block's other warps load the same rows, so most of those reads
   // hit L1) — no shared-memory exchange and no barrier per time row.  x-neighbours by __shfl.
-  double dacc[NVD > 0 ? NVD : 1];
+  double dacc[NVD > 0 ? NVD + (WW ? 1 : 0) : 1];
 #pragma unroll
-  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
+  for (int i = 0; i < (NVD > 0 ? NVD + (WW ? 1 : 0) : 1); ++i) dacc[i] = 0.0;
   const int lane = threadIdx.x, wy = threadIdx.y;
   const int64_t x0 = (int64_t)blockIdx.x * 64 + 2 * lane;
   const int yrow = blockIdx.y * 8 + wy;
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
         if constexpr (NVD > 0) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
 #pragma unroll
           for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
+          if constexpr (WW) dacc[NVD] = fma(y0, y0, fma(y1, y1, dacc[NVD]));
         }
         if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
       }
@@ -332,8 +335,12 @@ __global__ void __launch_bounds__(256) k_matvec2d(const double* __restrict__ u, 
   }
   if (NORM) block_partial<256>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
-    block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+    constexpr int NC = NVD + (WW ? 1 : 0);
+    block_reduce_nv<NC>(dacc, part, CNP_MAX_DOT + 1);
+    const bool folded = grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NC, out, counter);
+    if constexpr (WW) {
+      if (folded) run_post(post);
+    }
   }
 }
 
@@ -540,7 +547,7 @@ static cudaError_t run_matvec(cnpint_ctx* c, const double* u, double* y, const d
 
 template <int NVD>
 static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, const DotPtrs& vd, double* part,
-                                   double* out) {
+                                   double* out, int ww) {
   const double htau = 0.5 * c->tau;
   cnp_prof_begin(c, KID_MATVEC);
   if (c->dim == 1) {
@@ -552,31 +559,41 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
                                      c->d_counter, vd, c->d_dt, PostOp{});
     if (e != cudaSuccess) return e;
   } else {
-    const int tchunk = mv2_tchunk(c, NVD);
+    const int tchunk = ww ? mv2_tchunk(c, MVS_MAXNVD + 1) : mv2_tchunk(c, NVD);  // ww: always the register kernel
     dim3 grid((unsigned)((c->ld + 63) / 64), (unsigned)((c->ny + 7) / 8), (unsigned)((c->N + tchunk - 1) / tchunk));
-    const cudaError_t e = launch_mv2d<0, false, NVD>(c, grid, u, y, (const double*)nullptr, c->N, c->nx, c->ny, c->ld,
-                                                     htau, c->alpha, c->xs, c->xu, c->ys, c->yu,
-                                                     c->xd + c->yd + c->shift, tchunk, part, out, c->d_counter, vd,
-                                                     (const double*)c->d_dt, PostOp{});
+    cudaError_t e;
+    if (ww) {  // + ww = yᵀy and the pending post-fold step (the derived-norm probe of cnpint_gmres)
+      const PostOp post = c->post;
+      c->post = PostOp{};
+      e = cnp_launch(c, k_matvec2d<0, false, NVD, true>, grid, dim3(32, 8), 0, u, y, (const double*)nullptr, c->N,
+                     c->nx, c->ny, c->ld, htau, c->alpha, c->xs, c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk,
+                     part, out, c->d_counter, vd, (const double*)c->d_dt, post);
+    } else {
+      e = launch_mv2d<0, false, NVD>(c, grid, u, y, (const double*)nullptr, c->N, c->nx, c->ny, c->ld, htau, c->alpha,
+                                     c->xs, c->xu, c->ys, c->yu, c->xd + c->yd + c->shift, tchunk, part, out,
+                                     c->d_counter, vd, (const double*)c->d_dt, PostOp{});
+    }
     if (e != cudaSuccess) return e;
   }
   cnp_prof_end(c, KID_MATVEC, (16.0 + 8.0 * NVD) * cnp_units(c));
   return cudaGetLastError();
 }
 
+// ww (2D only): also out[nv] = yᵀy, and c->post runs in the folding block
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
-                               double* out) {
+                               double* out, int ww) {
+  if (ww && c->dim != 2) return cudaErrorNotSupported;
   DotPtrs vd{};
   for (int i = 0; i < nv && i < CNP_MAX_DOT; ++i) vd.p[i] = V[i];
   switch (nv) {
-    case 1: return run_matvec_dots<1>(c, u, y, vd, part, out);
-    case 2: return run_matvec_dots<2>(c, u, y, vd, part, out);
-    case 3: return run_matvec_dots<3>(c, u, y, vd, part, out);
-    case 4: return run_matvec_dots<4>(c, u, y, vd, part, out);
-    case 5: return run_matvec_dots<5>(c, u, y, vd, part, out);
-    case 6: return run_matvec_dots<6>(c, u, y, vd, part, out);
-    case 7: return run_matvec_dots<7>(c, u, y, vd, part, out);
-    case 8: return run_matvec_dots<8>(c, u, y, vd, part, out);
+    case 1: return run_matvec_dots<1>(c, u, y, vd, part, out, ww);
+    case 2: return run_matvec_dots<2>(c, u, y, vd, part, out, ww);
+    case 3: return run_matvec_dots<3>(c, u, y, vd, part, out, ww);
+    case 4: return run_matvec_dots<4>(c, u, y, vd, part, out, ww);
+    case 5: return run_matvec_dots<5>(c, u, y, vd, part, out, ww);
+    case 6: return run_matvec_dots<6>(c, u, y, vd, part, out, ww);
+    case 7: return run_matvec_dots<7>(c, u, y, vd, part, out, ww);
+    case 8: return run_matvec_dots<8>(c, u, y, vd, part, out, ww);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -70,6 +70,35 @@ CNP_DEV void gram_store_dev(int j, int ldh, const double* cg, double* G, double*
   scal[2] = cg[0];
 }
 
+//   op 5 (derived-norm probe of a step expected to be the last; run by the fused-dots matvec that also
+//   folded ww = wᵀw into c1[j+1]): with a = S²(c1 + c2) the new vector would be w − Ṽa, whose norm follows
+//   from the Gram matrix without a pass over the vectors, β² = ww − 2aᵀc1 + aᵀG̃a.  The difference cancels
+//   to β²/ww, so it is trusted only when β² ≥ 1e-8·ww (relative error of β² ≤ ~1e-7); then column j is
+//   finalized with it (g[j] saved in scal[13] so the host can take the step back) and scal[6] = 1.
+CNP_DEV void gram_probe_dev(const PostOp& p) {
+  const int j = p.j, ldh = p.ldh;
+  gram_c2_dev(j, ldh, p.G, p.scl, p.c1, p.c2w);
+  const double ww = p.c1[j + 1];
+  double lin = 0.0, quad = 0.0;
+  for (int i = 0; i <= j; ++i) {
+    const double ai = p.scl[i] * p.scl[i] * (p.c1[i] + p.c2w[i]);
+    lin += ai * p.c1[i];
+    double row = 0.0;
+    for (int k = 0; k <= j; ++k) row += p.G[(size_t)i * ldh + k] * (p.scl[k] * p.scl[k] * (p.c1[k] + p.c2w[k]));
+    quad += ai * row;
+  }
+  const double b2 = ww - 2.0 * lin + quad;
+  const bool safe = isfinite(b2) && isfinite(ww) && ww > 0.0 && b2 >= 1e-8 * ww;
+  p.scal[14] = b2;
+  p.scal[15] = ww;
+  p.scal[6] = safe ? 1.0 : 0.0;
+  if (safe) {
+    p.scal[13] = p.g[j];
+    p.scal[2] = b2;
+    arnoldi_finalize_dev(j, ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
+  }
+}
+
 // Called by the whole last block after grid_fold returned true (its thread 0 wrote scal[2]).
 CNP_DEV void run_post(const PostOp& p) {
   if (p.op == 0) return;
@@ -82,7 +111,8 @@ CNP_DEV void run_post(const PostOp& p) {
       if (p.j + 1 < p.ldh) gram_store_dev(p.j, p.ldh, p.cg, p.G, p.scal);
       else p.scal[2] = p.cg[0];
       arnoldi_finalize_dev(p.j, p.ldh, p.c1, p.c2, p.scl, p.H, p.cs, p.sn, p.g, p.scal);
-    } else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax, p.G);
+    } else if (p.op == 5) gram_probe_dev(p);
+    else cycle_start_dev(p.scl, p.g, p.scal, p.first, p.rmax, p.G);
     if (p.hmap && p.op != 3) {
       for (int i = 0; i < 8; ++i) p.hmap[i] = p.scal[i];
       p.hmap[8] = (double)*p.status;

@@ -139,6 +139,41 @@ def test_matvec2d_staged_equals_register_kernel(n, N):
     assert np.all(np.abs(h0 - h1) <= 1e-12 * np.abs(h1) + 1e-16), (h0, h1)
 
 
+@pytest.mark.parametrize("case", ["c4_small", "c5_n127_N256", "2d_restart3", "2d_tight"])
+def test_gmres_derived_norm_probe(case):
+    """cnpint_gmres (2D): a step expected to be the last takes h_{j+1,j} from the Gram matrix and skips the
+    update pass when the estimate then meets the tolerance (default).  Against the plain steps (debug
+    2097152): the same count, the same iterate (1e-12), the last estimate within 1e-5 relative (derived vs
+    measured norm); with every step probed (debug 4194304: the take-back path after each failed probe) the
+    same again; and the default must actually have skipped the last vector where the count allows it."""
+    w = {"c4_small": synth.scaled(synth.C4, 63, 64, restart=40), "c5_n127_N256": synth.c5(127, 256),
+         "2d_restart3": synth.scaled(synth.C4, 31, 64, alpha=0.3, restart=3),
+         "2d_tight": synth.scaled(synth.C4, 63, 128, restart=40).with_(tol=1e-12)}[case]
+    s = solver_for(w, restart_max=w.restart)
+    b = problems.rhs(w, s)
+    res = {}
+    for dbg in (2097152, 0, 4194304):
+        s.set_debug(dbg)
+        u = s.empty()
+        rep = s.gmres(b, u, w.tol, w.restart, maxit=200)
+        vecs, _ = s.krylov_basis()
+        res[dbg] = (u, rep, len(vecs))
+    s.set_debug(0)
+    u0, r0, n0 = res[2097152]
+    assert r0["converged"]
+    for dbg in (0, 4194304):
+        u1, r1, n1 = res[dbg]
+        assert r1["converged"] and r1["iterations"] == r0["iterations"] and r1["restarts"] == r0["restarts"], (r0, r1)
+        assert float((u1 - u0).norm() / u0.norm()) < 1e-12
+        h0, h1 = np.array(r0["history"]), np.array(r1["history"])
+        assert np.all(np.abs(h0 - h1) <= 1e-5 * np.abs(h0) + 1e-300), (h0, h1)
+        assert r1["relres_true"] <= w.tol
+    record(f"probe_{case}", iterations=r0["iterations"], basis_plain=n0, basis_default=res[0][2],
+           basis_forced=res[4194304][2])
+    if case in ("c4_small", "c5_n127_N256"):
+        assert res[0][2] == n0 - 1, (res[0][2], n0)   # the last vector was not written
+
+
 # ------------------------------------------------------------------------------ P_α⁻¹
 @pytest.mark.parametrize("name", list(SMALL))
 def test_pinv_small(name):
