@@ -332,7 +332,7 @@ cnpint_status cnpint_shard_reduced_host(int K, int R, int rank, const double* re
  * 1048576 = the register 2D matvec (k_matvec2d: own row and both y neighbours loaded into registers, four
  * time rows per batch) instead of the staged one (k_matvec2d_s: rows of u through a cp.async shared-memory
  * ring, eight time rows in flight per warp); the same arithmetic per element;
- * 2097152 = no derived-norm probe in cnpint_gmres (2D): by default a step expected to be the last takes
+ * 2097152 = no derived-norm probe in cnpint_gmres: by default a step expected to be the last takes
  * h_{j+1,j} from the Gram matrix (β² = ww − 2aᵀc1 + aᵀG̃a, trusted when β² ≥ 1e-8·wᵀw) and, if the estimate
  * then meets the tolerance, skips the update pass that would write a basis vector nobody reads;
  * 4194304 = probe every step (exercises the take-back path; the results are those of the plain steps).  Bits 1, 2, 8, 16, 64, 16384 and 262144 — the

@@ -892,13 +892,13 @@ cnpint_status cnpint_gmres(cnpint_ctx* c, const double* d_b, double* d_u, double
         // and the Gram row Ṽᵀw of the new vector (post op 4 stores it, then the Arnoldi finalize)
         // — the same two projections as classic CGS2, one reading pass fewer
         const double est_next = est_before > 0.0 ? est_now * std::min(1.0, est_now / est_before) : est_now;
-        // A step expected to be the last (2D): its new basis vector would never be used, only its norm
+        // A step expected to be the last: its new basis vector would never be used, only its norm
         // h_{j+1,j} — which the Gram matrix gives without a pass over the vectors (post op 5, run by the
         // matvec's folding block: β² = ww − 2aᵀc1 + aᵀG̃a, trusted when β² ≥ 1e-8·ww).  If the estimate
         // then meets the tolerance, the update pass is skipped; otherwise the probe is taken back and the
         // step runs as usual.  debug 2097152 turns the probe off, 4194304 probes every step (tests: the
         // take-back path).
-        if (c->dim == 2 && !(c->debug & 2097152) && est_before > 0.0 && (est_next <= tol || (c->debug & 4194304))) {
+        if (!(c->debug & 2097152) && est_before > 0.0 && (est_next <= tol || (c->debug & 4194304))) {
           c->post = post_gram_probe(c, j);
           CK(launch_matvec_dots(c, Z[j], w, V.data(), nv, c->d_part, c->d_c1, 1));
           CK(cudaStreamSynchronize(c->stream));

@@ -116,7 +116,9 @@ static int mv2_tchunk(const cnpint_ctx* c, int ns) {
 // ------------------------------------------------------------------------------- K1 1D
 // MODE 0: y = 𝓜u.  MODE 1: y = P_α u.  MODE 2: y = b − 𝓜u.  MODE 3: as 2 without storing y (norm
 // only).  NORM: per-block Σ y².
-template <int MODE, bool NORM, int NVD = 0>
+// WW (with NVD > 0): also ww = yᵀy as column NVD of the folded dots, and the pending post-fold step run by
+// the folding block (the derived-norm probe of cnpint_gmres, post op 5).
+template <int MODE, bool NORM, int NVD = 0, bool WW = false>
 __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, double* __restrict__ y,
                                                   const double* __restrict__ b, const double* __restrict__ lo,
                                                   const double* __restrict__ di, const double* __restrict__ up,
@@ -125,9 +127,9 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
                                                   unsigned* counter, DotPtrs vd = DotPtrs{},
                                                   const double* __restrict__ dt = nullptr, PostOp post = PostOp{}) {
   pdl_enter();  // PDL: wait for the previous kernel on the stream before any global access
-  double dacc[NVD > 0 ? NVD : 1];
+  double dacc[NVD > 0 ? NVD + (WW ? 1 : 0) : 1];
 #pragma unroll
-  for (int i = 0; i < (NVD > 0 ? NVD : 1); ++i) dacc[i] = 0.0;
+  for (int i = 0; i < (NVD > 0 ? NVD + (WW ? 1 : 0) : 1); ++i) dacc[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int64_t gx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // column pair
   const bool active = 2 * gx < ld;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
       if (NVD > 0 && active) {  // fused first CGS pass: partial dots Ṽ_iᵀ y
 #pragma unroll
         for (int i = 0; i < NVD; ++i) dacc[i] = fma(vvb[q][i].x, y0, fma(vvb[q][i].y, y1, dacc[i]));
+        if constexpr (WW) dacc[NVD] = fma(y0, y0, fma(y1, y1, dacc[NVD]));
       }
       if (NORM) acc = fma(y0, y0, fma(y1, y1, acc));
       pv = cv; pl = cl; pr = cr;
@@ -215,8 +218,12 @@ __global__ void __launch_bounds__(128) k_matvec1d(const double* __restrict__ u, 
   }
   if (NORM) block_partial<128>(acc, part, out, counter, post);
   if constexpr (NVD > 0) {
-    block_reduce_nv<NVD>(dacc, part, CNP_MAX_DOT + 1);
-    grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NVD, out, counter);
+    constexpr int NC = NVD + (WW ? 1 : 0);
+    block_reduce_nv<NC>(dacc, part, CNP_MAX_DOT + 1);
+    const bool folded = grid_fold(part, gridDim.x * gridDim.y * gridDim.z, CNP_MAX_DOT + 1, NC, out, counter);
+    if constexpr (WW) {
+      if (folded) run_post(post);
+    }
   }
 }
 
@@ -554,9 +561,16 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
     const int tchunk = mv_tchunk(c);
     dim3 block(128);
     dim3 grid((unsigned)((c->ld / 2 + 127) / 128), (unsigned)((c->N + tchunk - 1) / tchunk));
-    const cudaError_t e = cnp_launch(c, k_matvec1d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr,
-                                     c->d_lo, c->d_di, c->d_up, c->N, c->ld, htau, c->alpha, tchunk, part, out,
-                                     c->d_counter, vd, c->d_dt, PostOp{});
+    cudaError_t e;
+    if (ww) {  // + ww = yᵀy and the pending post-fold step (the derived-norm probe of cnpint_gmres)
+      const PostOp post = c->post;
+      c->post = PostOp{};
+      e = cnp_launch(c, k_matvec1d<0, false, NVD, true>, grid, block, 0, u, y, (const double*)nullptr, c->d_lo, c->d_di,
+                     c->d_up, c->N, c->ld, htau, c->alpha, tchunk, part, out, c->d_counter, vd, c->d_dt, post);
+    } else {
+      e = cnp_launch(c, k_matvec1d<0, false, NVD>, grid, block, 0, u, y, (const double*)nullptr, c->d_lo, c->d_di,
+                     c->d_up, c->N, c->ld, htau, c->alpha, tchunk, part, out, c->d_counter, vd, c->d_dt, PostOp{});
+    }
     if (e != cudaSuccess) return e;
   } else {
     const int tchunk = ww ? mv2_tchunk(c, MVS_MAXNVD + 1) : mv2_tchunk(c, NVD);  // ww: always the register kernel
@@ -579,10 +593,9 @@ static cudaError_t run_matvec_dots(cnpint_ctx* c, const double* u, double* y, co
   return cudaGetLastError();
 }
 
-// ww (2D only): also out[nv] = yᵀy, and c->post runs in the folding block
+// ww: also out[nv] = yᵀy, and c->post runs in the folding block
 cudaError_t launch_matvec_dots(cnpint_ctx* c, const double* u, double* y, double* const* V, int nv, double* part,
                                double* out, int ww) {
-  if (ww && c->dim != 2) return cudaErrorNotSupported;
   DotPtrs vd{};
   for (int i = 0; i < nv && i < CNP_MAX_DOT; ++i) vd.p[i] = V[i];
   switch (nv) {

@@ -139,16 +139,18 @@ def test_matvec2d_staged_equals_register_kernel(n, N):
     assert np.all(np.abs(h0 - h1) <= 1e-12 * np.abs(h1) + 1e-16), (h0, h1)
 
 
-@pytest.mark.parametrize("case", ["c4_small", "c5_n127_N256", "2d_restart3", "2d_tight"])
+@pytest.mark.parametrize("case", ["c4_small", "c5_n127_N256", "2d_restart3", "2d_tight", "c1", "1d_price", "1d_restart2"])
 def test_gmres_derived_norm_probe(case):
-    """cnpint_gmres (2D): a step expected to be the last takes h_{j+1,j} from the Gram matrix and skips the
+    """cnpint_gmres: a step expected to be the last takes h_{j+1,j} from the Gram matrix and skips the
     update pass when the estimate then meets the tolerance (default).  Against the plain steps (debug
     2097152): the same count, the same iterate (1e-12), the last estimate within 1e-5 relative (derived vs
     measured norm); with every step probed (debug 4194304: the take-back path after each failed probe) the
     same again; and the default must actually have skipped the last vector where the count allows it."""
     w = {"c4_small": synth.scaled(synth.C4, 63, 64, restart=40), "c5_n127_N256": synth.c5(127, 256),
          "2d_restart3": synth.scaled(synth.C4, 31, 64, alpha=0.3, restart=3),
-         "2d_tight": synth.scaled(synth.C4, 63, 128, restart=40).with_(tol=1e-12)}[case]
+         "2d_tight": synth.scaled(synth.C4, 63, 128, restart=40).with_(tol=1e-12), "c1": synth.C1,
+         "1d_price": synth.scaled(synth.C3, 127, 256, restart=40),
+         "1d_restart2": synth.scaled(synth.C1, 63, 64, alpha=0.5, restart=2)}[case]
     s = solver_for(w, restart_max=w.restart)
     b = problems.rhs(w, s)
     res = {}
@@ -170,7 +172,7 @@ def test_gmres_derived_norm_probe(case):
         assert r1["relres_true"] <= w.tol
     record(f"probe_{case}", iterations=r0["iterations"], basis_plain=n0, basis_default=res[0][2],
            basis_forced=res[4194304][2])
-    if case in ("c4_small", "c5_n127_N256"):
+    if case in ("c4_small", "c5_n127_N256", "c1", "1d_price"):
         assert res[0][2] == n0 - 1, (res[0][2], n0)   # the last vector was not written
 
 
