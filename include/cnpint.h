@@ -235,7 +235,9 @@ cnpint_status cnpint_stream_copy(const double* d_src, double* d_dst, size_t n, v
  * restart cycle of the most recent cnpint_gmres call, v_i = s_i·Ṽ_i with 0 <= i < *count (count may
  * be read with i = 0 even when the call fails).  *d_vec = Ṽ_i (device, the vector layout above; the
  * first cycle's Ṽ_0 is the caller's b; valid until the next call on the handle), *scale = s_i (host
- * copy; synchronises the stream).  Any out pointer may be NULL.  EINVAL for i out of range. */
+ * copy; synchronises the stream).  *count = steps of the cycle + 1, or = steps when the cycle's last step
+ * took its norm from the Gram matrix and wrote no vector (the derived-norm probe, debug 2097152 off).
+ * Any out pointer may be NULL.  EINVAL for i out of range. */
 cnpint_status cnpint_krylov_basis(cnpint_ctx* ctx, int i, const double** d_vec, double* scale, int* count);
 
 /* Same-run compute ceilings: enqueues on cuda_stream a kernel of 8 CTAs x 256
